@@ -1,0 +1,226 @@
+/*
+ * qsb.h — C ABI of the B200-native unitary-simulation hot path
+ * (TornadoQSim "UnitarySimulatorStandard", arXiv 2305.14398, Algorithms 1+2).
+ *
+ * This is the drop-in boundary. The reference keeps its C++ Circuit / Step /
+ * Operation model, its gate library and its Simulator plugin interface; a thin
+ * adapter (integration/b200_unitary_simulator.cpp, shown in INTEGRATION.md)
+ * flattens a qsim::Circuit into a qsb_circuit and calls the entry points below.
+ * Plain C types only: no C++ exceptions, no torch types, no STL cross the ABI.
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/proj):
+ *   qsb_simulate_full_state  -> UnitarySimulator::simulate_full_state
+ *                               core/src/unitary_backend.cpp:194-215
+ *   qsb_build_unitary        -> test::circuit_unitary (the accumulated U)
+ *                               tests/support/test_util.hpp:135-142
+ *   qsb_simulate_and_collapse-> Simulator::simulate_and_collapse + collapse
+ *                               core/src/simulator.cpp:26-30, core/src/state.cpp:81-98
+ *   qsb_layer_operator       -> kronecker_fold(fill_layer(layer))  (one layer of step_unitary)
+ *                               core/src/unitary_backend.cpp:95-125, 141-154
+ *   qsb_probabilities        -> probabilities / norm_squared
+ *                               core/src/state.cpp:49-65
+ *   qsb_qubit_guard          -> Simulator::qubit_guard  core/include/qsim/simulator.hpp:40
+ *   qsb_status + qsb_last_error -> the qsim::Error hierarchy
+ *                               core/include/qsim/errors.hpp:23-56
+ *
+ * Orientation: the reference accumulates U = S_K ... S_2 S_1 by left
+ * multiplication (unitary_backend.cpp:211). This library computes the same
+ * product by row blocks, V <- V * L for every layer operator L from the last
+ * to the first; a shard of rows is computed
+ * with no communication.
+ */
+#ifndef QSB_H_
+#define QSB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QSB_ABI_VERSION 1
+
+/* Status codes; qsb_last_error() returns the message of the last failure on
+ * the calling thread. The adapter maps them back onto qsim::Error subclasses. */
+typedef enum qsb_status {
+    QSB_OK = 0,
+    QSB_ERR_RESOURCE = 1,   /* qsim::ResourceError  (qubit guard / HBM capacity) */
+    QSB_ERR_VALIDATION = 2, /* qsim::ValidationError (reset placement, registry dims) */
+    QSB_ERR_SHAPE = 3,      /* qsim::ShapeError */
+    QSB_ERR_ARGUMENT = 4,   /* qsim::ArgumentError */
+    QSB_ERR_LOOKUP = 5,     /* qsim::LookupError */
+    QSB_ERR_CUDA = 6,       /* CUDA runtime / driver failure (incl. no device) */
+    QSB_ERR_NCCL = 7,       /* NCCL failure */
+    QSB_ERR_INTERNAL = 8
+} qsb_status;
+
+/* Operation kinds: the alternatives of qsim::Operation (circuit.hpp:79). */
+enum {
+    QSB_OP_GATE = 0,        /* Gate{gate, target}                 circuit.hpp:51-55 */
+    QSB_OP_CONTROL = 1,     /* ControlGate{gate, control, target} circuit.hpp:57-62 */
+    QSB_OP_FUNCTION = 2,    /* FunctionOp{name, first, count}     circuit.hpp:66-71 */
+    QSB_OP_INSTRUCTION = 3  /* Instruction{kind, target}          circuit.hpp:73-77 */
+};
+
+/* GateTag (circuit.hpp:31); informational for the library, which consumes u. */
+enum { QSB_GATE_H = 0, QSB_GATE_X, QSB_GATE_Y, QSB_GATE_Z, QSB_GATE_S, QSB_GATE_T, QSB_GATE_R };
+/* InstructionKind (circuit.hpp:49). */
+enum { QSB_INSTR_MEASURE = 0, QSB_INSTR_RESET = 1 };
+
+/* One qsim::Operation. For QSB_OP_GATE / QSB_OP_CONTROL the caller fills u_re/u_im
+ * with gate_matrix(gate) (gates.cpp:40-77), row-major 2x2; the library uses
+ * exactly those values, so the caller's gate library stays authoritative. */
+typedef struct qsb_op {
+    int32_t kind;        /* QSB_OP_* */
+    int32_t gate;        /* QSB_GATE_* (gate / control gate) */
+    int32_t target;      /* gate, control gate, instruction: target qubit */
+    int32_t control;     /* control gate: control qubit */
+    int32_t first;       /* function: first_qubit */
+    int32_t count;       /* function: qubit_count */
+    int32_t function;    /* function: index into qsb_circuit.functions */
+    int32_t instruction; /* instruction: QSB_INSTR_* */
+    double phi;          /* R(phi) angle (informational) */
+    double u_re[4];
+    double u_im[4];
+} qsb_op;
+
+/* A GateRegistry entry resolved for this circuit: a dim x dim row-major matrix
+ * in split re/im planes (the storage of qsim::ComplexMatrix, linalg.hpp:39-70). */
+typedef struct qsb_function {
+    int64_t dim;
+    const double* re;
+    const double* im;
+} qsb_function;
+
+/* A qsim::Circuit after Circuit::append's greedy last-step packing
+ * (circuit.cpp:81-103): ops of step s are ops[step_offsets[s] .. step_offsets[s+1]),
+ * in insertion order. */
+typedef struct qsb_circuit {
+    int32_t n_qubits;
+    int32_t n_steps;
+    const int32_t* step_offsets; /* n_steps + 1 entries */
+    const qsb_op* ops;
+    int32_t n_functions;
+    const qsb_function* functions;
+} qsb_circuit;
+
+/* GEMM arithmetic. 4M = four real DMMA sub-GEMMs per complex product; 3M =
+ * three (Gauss), fewer FLOPs, still credited 8 N^3 in reports. */
+enum { QSB_GEMM_AUTO = 0, QSB_GEMM_4M = 1, QSB_GEMM_3M = 2 };
+
+typedef struct qsb_options {
+    int32_t device;       /* CUDA device ordinal */
+    int32_t qubit_guard;  /* 0 = derive from HBM capacity (simulator.hpp:53-56 override otherwise) */
+    int32_t gemm_mode;    /* QSB_GEMM_* */
+    int32_t flags;        /* QSB_FLAG_* */
+} qsb_options;
+
+enum {
+    QSB_FLAG_NO_GRAPH = 1,        /* do not capture plan execution in a CUDA graph */
+    QSB_FLAG_MATERIALIZE = 2      /* materialise each layer operator with K1 and run the
+                                     GEMM on it instead of generating tiles in shared memory */
+};
+
+typedef struct qsb_handle qsb_handle;
+typedef struct qsb_plan qsb_plan;
+
+/* Statistics of one plan (one circuit on one row shard). */
+typedef struct qsb_plan_info {
+    int32_t n_qubits;
+    int32_t n_steps;
+    int32_t n_layers;          /* layer operators in the circuit (sum over steps) */
+    int32_t n_gemms;           /* dense complex GEMMs executed per run */
+    int32_t n_identity_layers; /* instruction-only layers (exact identities, not multiplied) */
+    int32_t n_launches;        /* kernels launched per run */
+    int64_t row_begin;
+    int64_t row_count;
+    double gemm_flops;         /* 8 * row_count * N^2 per GEMM, summed */
+    double expand_bytes;       /* bytes written by the K1 expansion */
+} qsb_plan_info;
+
+int qsb_abi_version(void);
+
+/* Copies the last error message of the calling thread into buf (NUL-terminated). */
+size_t qsb_last_error(char* buf, size_t len);
+
+qsb_status qsb_create(const qsb_options* options, qsb_handle** out);
+qsb_status qsb_destroy(qsb_handle* handle);
+
+/* Largest qubit count accepted (guard, or HBM-derived default). */
+qsb_status qsb_qubit_guard(const qsb_handle* handle, int32_t* guard);
+
+/* Algorithm 1: psi = U |0...0>, written to host planes of length 2^n.
+ * Host in, host out; thread-safe on one handle (internally serialised). */
+qsb_status qsb_simulate_full_state(qsb_handle* handle, const qsb_circuit* circuit,
+                                   double* psi_re, double* psi_im);
+
+/* Same, from an arbitrary initial state psi0 (host planes, length 2^n). */
+qsb_status qsb_simulate_from_state(qsb_handle* handle, const qsb_circuit* circuit,
+                                   const double* psi0_re, const double* psi0_im,
+                                   double* psi_re, double* psi_im);
+
+/* The accumulated circuit unitary U (host planes, 2^n x 2^n row-major). */
+qsb_status qsb_build_unitary(qsb_handle* handle, const qsb_circuit* circuit,
+                             double* u_re, double* u_im);
+
+/* simulate_full_state + inverse-CDF collapse with SplitMix64(seed). */
+qsb_status qsb_simulate_and_collapse(qsb_handle* handle, const qsb_circuit* circuit,
+                                     uint64_t seed, uint64_t* basis_index);
+
+/* Number of layers step `step` factors into (first-fit, unitary_backend.cpp:63-91). */
+qsb_status qsb_step_layer_count(const qsb_circuit* circuit, int32_t step, int32_t* layers);
+
+/* K1: the dense operator of layer `layer` of step `step`, expanded on the GPU
+ * (host planes, 2^n x 2^n). Bit-exact with the reference's kronecker_fold. */
+qsb_status qsb_layer_operator(qsb_handle* handle, const qsb_circuit* circuit, int32_t step,
+                              int32_t layer, double* re, double* im);
+
+/* K4: p_i = re_i^2 + im_i^2 and sum p_i of a host state, computed on the GPU. */
+qsb_status qsb_probabilities(qsb_handle* handle, const double* psi_re, const double* psi_im,
+                             int64_t dim, double* p, double* norm_squared);
+
+/* ---- device-resident plans (bench, multi-GPU row shards) ---- */
+
+/* Compile `circuit` for rows [row_begin, row_begin + row_count) of U and upload
+ * every descriptor; buffers are allocated on the handle's device. */
+qsb_status qsb_plan_create(qsb_handle* handle, const qsb_circuit* circuit, int64_t row_begin,
+                           int64_t row_count, qsb_plan** out);
+qsb_status qsb_plan_destroy(qsb_plan* plan);
+qsb_status qsb_plan_get_info(const qsb_plan* plan, qsb_plan_info* info);
+
+/* Run the whole chain on `stream` (a cudaStream_t; NULL = the handle's stream):
+ * V = rows of U, then psi_rows = V * psi0 (psi0 = |0...0> unless set). Async. */
+qsb_status qsb_plan_execute(qsb_plan* plan, void* stream);
+
+/* Record CUDA events around the K1 / K2 / K3 phases of every execute (disables
+ * the plan's CUDA graph); read them back with qsb_plan_last_timing. */
+qsb_status qsb_plan_set_timing(qsb_plan* plan, int32_t enable);
+
+/* Replace psi0 (default |0...0>) with re/im planes of length 2^n (host or device
+ * pointers), async on `stream`. */
+qsb_status qsb_plan_set_initial_state(qsb_plan* plan, const double* re, const double* im, void* stream);
+
+/* Device pointers of the plan's results (valid until the next execute/destroy):
+ * U rows (row_count x 2^n, leading dimension 2^n) and psi rows (row_count). */
+qsb_status qsb_plan_unitary_device(const qsb_plan* plan, const double** re, const double** im);
+qsb_status qsb_plan_state_device(const qsb_plan* plan, const double** re, const double** im);
+
+/* Copy psi rows into caller device buffers (e.g. a slice of an all-gather buffer), async. */
+qsb_status qsb_plan_copy_state(const qsb_plan* plan, double* dst_re, double* dst_im, void* stream);
+
+/* Kernel timing of the last execute, from CUDA events on the launching stream:
+ * total, the K2 GEMM chain, and the mean single-GEMM duration (ms). Synchronises. */
+qsb_status qsb_plan_last_timing(qsb_plan* plan, double* total_ms, double* gemm_ms,
+                                double* gemm_mean_ms);
+
+/* Reference memory accounting (unitary_backend.cpp:156-179), BackendKind 0 = Unitary, 1 = Fsv. */
+uint64_t qsb_memory_estimate(int32_t n_qubits, int32_t kind);
+uint64_t qsb_engine_memory_estimate(int32_t n_qubits, int32_t kind);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QSB_H_ */

@@ -1,0 +1,71 @@
+// qsb_internal.hpp — device-side descriptors shared by the host runtime
+// (qsb_runtime.cpp) and the sm_100a kernels (qsb_kernels.cu).
+//
+// A "layer" is one Kronecker product of the reference's fill_layer list
+// (unitary_backend.cpp:95-116): identity blocks for untouched qubits and
+// instructions, plus the non-identity blocks of the layer's operations.
+// Identity blocks never appear explicitly: entry (r, c) of the layer operator
+// is zero unless r and c agree on every bit owned by an identity block
+// (idmask), and otherwise equals the left-fold product of the non-identity
+// block entries in qubit-0-first order — bit-identical to kronecker_fold
+// (unitary_backend.cpp:119-125, linalg.cpp:109-129) because a factor of an
+// identity block is an exact 1.
+#pragma once
+
+#include <cstdint>
+
+namespace qsb {
+
+constexpr int kMaxQubits = 20;  // unitary path: 2 x 16 x 4^n bytes must fit in HBM
+constexpr int kMaxBlocks = kMaxQubits;
+
+enum BlockKind : int32_t {
+    kBlockGate = 0,        // 2x2 gate_matrix on one qubit            (gates.cpp:40-77)
+    kBlockControlled = 1,  // controlled_unitary over a span          (gates.cpp:79-110)
+    kBlockTable = 2        // registered FunctionOp matrix, in HBM    (gates.cpp:127-133)
+};
+
+struct BlockDesc {
+    int32_t kind;
+    int32_t shift;      // n - first - span: bit position of the block's least significant qubit
+    int32_t span;       // qubits covered
+    uint32_t mask;      // (1 << span) - 1
+    uint32_t cmask;     // controlled: control bit within the span (span-1-control_pos)
+    uint32_t tmask;     // controlled: target bit within the span
+    double u_re[4];     // gate / controlled: 2x2 row-major
+    double u_im[4];
+    const double* t_re; // table: (2^span)^2 row-major planes on the device
+    const double* t_im;
+};
+
+struct LayerDesc {
+    uint32_t idmask;    // index bits owned by identity blocks
+    int32_t nblocks;    // non-identity blocks, qubit-0-first (fold order)
+    BlockDesc blocks[kMaxBlocks];
+};
+
+// Launch wrappers (qsb_kernels.cu). All return cudaError_t as int.
+struct GemmArgs {
+    const void* tmap;        // CUtensorMap of the A operand (V, [2][M][N] doubles)
+    const LayerDesc* layer;  // host copy, passed by value to the kernel
+    double* out;             // [2][M][N]
+    int M;
+    int N;
+};
+
+int launch_expand(const LayerDesc& layer, uint32_t row_begin, int M, int N, double* out, void* stream);
+int launch_zgemm(const GemmArgs& a, int tile, int gemm_mode, void* stream);
+int launch_small_circuit(const LayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, int N,
+                         const double* x, double* v, double* psi, void* stream);
+int launch_matvec(const double* v, int M, int N, const double* x, double* psi, void* stream);
+int launch_probabilities(const double* psi, int64_t dim, double* p, double* partial, int partial_cap,
+                         double* norm, void* stream);
+
+// Tile shapes of the K2 GEMM (rows x cols of the output tile).
+enum GemmTile : int { kTile128x64 = 0, kTile64x64 = 1, kTile32x32 = 2 };
+int configure_kernels();
+int gemm_tile_rows(int tile);
+int gemm_tile_cols(int tile);
+size_t small_circuit_smem_bytes(int M, int N);
+
+}  // namespace qsb

@@ -1,0 +1,548 @@
+// qsb_kernels.cu — sm_100a kernels of the unitary-simulation hot path.
+//
+//   K1 expand_kernel        materialises rows of one layer operator (HBM-bound
+//                           coalesced 16-byte stores); used for the first
+//                           operator of the chain (V = L_last[rows, :]).
+//   K2 zgemm_gen_kernel     V' = V * L: complex FP64 GEMM on the DMMA tensor pipe
+//                           (mma.sync m8n8k4 f64), A = V staged by TMA
+//                           (cp.async.bulk.tensor, SWIZZLE_128B, mbarrier
+//                           pipeline), B = L generated straight into shared
+//                           memory from the layer descriptor — the operator is
+//                           never read from HBM.
+//   K2s small_circuit_kernel whole circuit in one CTA for 2^n <= 32.
+//   K3 matvec_kernel        psi = V * psi0, one warp per row, shuffle reduce.
+//   K4 probs_kernel         p_i = re^2 + im^2 (separately rounded, bit-exact with
+//                           state.cpp:58-65) + deterministic two-pass norm.
+//
+// Reference loops replaced (paths relative to /root/reference/proj):
+//   kronecker_fold / kronecker      core/src/unitary_backend.cpp:119-125, core/src/linalg.cpp:109-129
+//   controlled_unitary              core/src/gates.cpp:79-110
+//   matmul_rows (accumulate GEMM)   core/src/linalg.cpp:46-87, unitary_backend.cpp:211
+//   matvec                          core/src/linalg.cpp:89-107, unitary_backend.cpp:213-214
+//   probabilities / norm_squared    core/src/state.cpp:49-65
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "qsb_internal.hpp"
+
+namespace qsb {
+
+// ----------------------------------------------------------------------------
+// Operator-entry generator (shared by K1, K2, K2s)
+// ----------------------------------------------------------------------------
+
+// Complex product with every multiply and add rounded separately, as the
+// reference's `ar * br - ai * bi`, `ar * bi + ai * br` (linalg.cpp:122-123)
+// on x86-64 without FMA contraction.
+__device__ __forceinline__ void cmul_rn(double ar, double ai, double br, double bi, double& cr,
+                                        double& ci) {
+    cr = __dsub_rn(__dmul_rn(ar, br), __dmul_rn(ai, bi));
+    ci = __dadd_rn(__dmul_rn(ar, bi), __dmul_rn(ai, br));
+}
+
+// Entry (rb, cb) of one non-identity block, rb/cb = the block's bits of r/c.
+__device__ __forceinline__ void block_entry(const BlockDesc& b, uint32_t r, uint32_t c, double& er,
+                                            double& ei) {
+    const uint32_t rb = (r >> b.shift) & b.mask;
+    const uint32_t cb = (c >> b.shift) & b.mask;
+    if (b.kind == kBlockGate) {
+        const int e = static_cast<int>(rb * 2 + cb);
+        er = b.u_re[e];
+        ei = b.u_im[e];
+    } else if (b.kind == kBlockControlled) {
+        // controlled_unitary (gates.cpp:94-107): a column whose control bit is
+        // clear is the identity column; otherwise u acts on the target bit.
+        if ((cb & b.cmask) == 0) {
+            er = (rb == cb) ? 1.0 : 0.0;
+            ei = 0.0;
+        } else if (((rb ^ cb) & ~b.tmask) != 0) {
+            er = 0.0;
+            ei = 0.0;
+        } else {
+            const int e = ((rb & b.tmask) ? 2 : 0) + ((cb & b.tmask) ? 1 : 0);
+            er = b.u_re[e];
+            ei = b.u_im[e];
+        }
+    } else {
+        const size_t e = (static_cast<size_t>(rb) << b.span) + cb;
+        er = __ldg(b.t_re + e);
+        ei = __ldg(b.t_im + e);
+    }
+}
+
+// Entry (r, c) of the layer operator.
+__device__ __forceinline__ void layer_entry(const LayerDesc& d, uint32_t r, uint32_t c, double& vr,
+                                            double& vi) {
+    if ((r ^ c) & d.idmask) {
+        vr = 0.0;
+        vi = 0.0;
+        return;
+    }
+    if (d.nblocks == 0) {
+        vr = 1.0;
+        vi = 0.0;
+        return;
+    }
+    double ar, ai;
+    block_entry(d.blocks[0], r, c, ar, ai);
+    for (int b = 1; b < d.nblocks; ++b) {
+        if (ar == 0.0 && ai == 0.0) break;  // the fold stays (signed) zero
+        double er, ei, tr, ti;
+        block_entry(d.blocks[b], r, c, er, ei);
+        cmul_rn(ar, ai, er, ei, tr, ti);
+        ar = tr;
+        ai = ti;
+    }
+    vr = ar;
+    vi = ai;
+}
+
+// ----------------------------------------------------------------------------
+// K1: expansion
+// ----------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) expand_kernel(const __grid_constant__ LayerDesc d,
+                                                     uint32_t row_begin, int M, int N,
+                                                     double* __restrict__ out) {
+    const size_t plane = static_cast<size_t>(M) * N;
+    const size_t pairs = plane / 2;
+    const uint32_t half_n = static_cast<uint32_t>(N) / 2;
+    for (size_t p = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; p < pairs;
+         p += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const uint32_t row = static_cast<uint32_t>(p / half_n);
+        const uint32_t col = static_cast<uint32_t>(p % half_n) * 2;
+        double r0, i0, r1, i1;
+        layer_entry(d, row_begin + row, col, r0, i0);
+        layer_entry(d, row_begin + row, col + 1, r1, i1);
+        reinterpret_cast<double2*>(out)[p] = make_double2(r0, r1);
+        reinterpret_cast<double2*>(out + plane)[p] = make_double2(i0, i1);
+    }
+}
+
+int launch_expand(const LayerDesc& layer, uint32_t row_begin, int M, int N, double* out, void* stream) {
+    const size_t pairs = static_cast<size_t>(M) * N / 2;
+    int blocks = static_cast<int>((pairs + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks < 1) blocks = 1;
+    expand_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(layer, row_begin, M, N, out);
+    return static_cast<int>(cudaGetLastError());
+}
+
+// ----------------------------------------------------------------------------
+// K2: generated-operand complex GEMM on DMMA
+// ----------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* tmap, uint32_t bar, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+        "%4}], [%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ double2 lds128(uint32_t addr) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ void sts128(uint32_t addr, double x, double y) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(x), "d"(y) : "memory");
+}
+
+// D = A(8x4) * B(4x8) + C on the FP64 tensor pipe (SASS DMMA.8x8x4).
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+        : "+d"(c[0]), "+d"(c[1])
+        : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double neg(double x) {
+    return __longlong_as_double(__double_as_longlong(x) ^ static_cast<long long>(0x8000000000000000ULL));
+}
+
+template <int BM, int BN>
+struct GemmCfg {
+    static constexpr int BK = 16;  // one 128-byte swizzle line of doubles
+    static constexpr int WM = BM / 32;
+    static constexpr int WN = BN / 32;
+    static constexpr int THREADS = 32 * WM * WN;
+    static constexpr int STAGES = 4;
+    static constexpr int A_STAGE = 2 * BM * BK * 8;  // re + im planes
+    static constexpr int B_BUF = 2 * BN * BK * 8;
+    static constexpr int PAIRS = 8 * BN / THREADS;  // generated (k, k+1) pairs per thread
+    static constexpr int SMEM = 1024 + STAGES * A_STAGE + 2 * B_BUF + 64;
+};
+
+// Shared-memory tiles are [plane][rows][16 doubles] with the 128-byte TMA
+// swizzle: the 16-byte chunk c of line l sits at chunk c ^ (l & 7). Lane (g, t)
+// of an m8n8k4 fragment reads the chunks 2t and 2t+1 of line g, i.e. k indices
+// {4t, 4t+1} and {4t+2, 4t+3}; the four k-steps of a tile therefore use the
+// k-permutation k(t, s) = 4t + s, identically for A and B, which keeps every
+// 128-bit fragment load bank-conflict-free.
+template <int BM, int BN>
+__global__ void __launch_bounds__(GemmCfg<BM, BN>::THREADS, 1)
+    zgemm_gen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ LayerDesc layer,
+                     double* __restrict__ out, int M, int N) {
+    using C = GemmCfg<BM, BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sA = smem_u32(smem);
+    const uint32_t sB = sA + C::STAGES * C::A_STAGE;
+    const uint32_t sBar = sB + 2 * C::B_BUF;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    const int g = lane >> 2;
+    const int t = lane & 3;
+    const int wm = warp / C::WN;
+    const int wn = warp % C::WN;
+    const int m0 = blockIdx.y * BM;
+    const int n0 = blockIdx.x * BN;
+    const int KT = N / C::BK;
+
+    if (tid == 0) {
+        for (int s = 0; s < C::STAGES; ++s) mbar_init(sBar + 8 * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto issue_a = [&](int kt) {
+        const int s = kt % C::STAGES;
+        mbar_expect_tx(sBar + 8 * s, C::A_STAGE);
+        tma_load_3d(sA + s * C::A_STAGE, &tmA, sBar + 8 * s, kt * C::BK, m0, 0);
+    };
+
+    // Generate the BK x BN tile of L for k-tile kt into B buffer `buf`.
+    auto generate_b = [&](int kt, int buf) {
+        const uint32_t base = sB + buf * C::B_BUF;
+#pragma unroll
+        for (int q = 0; q < C::PAIRS; ++q) {
+            const int idx = tid + q * C::THREADS;
+            const int n = idx % BN;
+            const int p = idx / BN;  // chunk: k = 2p, 2p + 1
+            const uint32_t r0 = static_cast<uint32_t>(kt * C::BK + 2 * p);
+            const uint32_t col = static_cast<uint32_t>(n0 + n);
+            double a_r, a_i, b_r, b_i;
+            layer_entry(layer, r0, col, a_r, a_i);
+            layer_entry(layer, r0 + 1, col, b_r, b_i);
+            const uint32_t off = n * 128 + ((p ^ (n & 7)) << 4);
+            sts128(base + off, a_r, b_r);
+            sts128(base + BN * 128 + off, a_i, b_i);
+        }
+    };
+
+    // Warp tile 32x32 = 4 x 4 m8n8 tiles; real and imaginary accumulators.
+    double cr[4][4][2], ci[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            cr[i][j][0] = cr[i][j][1] = 0.0;
+            ci[i][j][0] = ci[i][j][1] = 0.0;
+        }
+
+    if (tid == 0) {
+        for (int kt = 0; kt < C::STAGES - 1 && kt < KT; ++kt) issue_a(kt);
+    }
+    generate_b(0, 0);
+    __syncthreads();
+
+    for (int kt = 0; kt < KT; ++kt) {
+        if (tid == 0 && kt + C::STAGES - 1 < KT) issue_a(kt + C::STAGES - 1);
+        if (kt + 1 < KT) generate_b(kt + 1, (kt + 1) & 1);
+        const int s = kt % C::STAGES;
+        mbar_wait(sBar + 8 * s, (kt / C::STAGES) & 1);
+
+        const uint32_t aRe = sA + s * C::A_STAGE;
+        const uint32_t aIm = aRe + BM * 128;
+        const uint32_t bRe = sB + (kt & 1) * C::B_BUF;
+        const uint32_t bIm = bRe + BN * 128;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t choff = static_cast<uint32_t>(((2 * t + h) ^ g) << 4);
+            double2 ar[4], ai[4], br[4], bi[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t line = static_cast<uint32_t>(wm * 32 + i * 8 + g) * 128 + choff;
+                ar[i] = lds128(aRe + line);
+                ai[i] = lds128(aIm + line);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t line = static_cast<uint32_t>(wn * 32 + j * 8 + g) * 128 + choff;
+                br[j] = lds128(bRe + line);
+                bi[j] = lds128(bIm + line);
+            }
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const double a_r = e ? ar[i].y : ar[i].x;
+                    const double a_i = e ? ai[i].y : ai[i].x;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const double b_r = e ? br[j].y : br[j].x;
+                        const double b_i = e ? bi[j].y : bi[j].x;
+                        dmma(cr[i][j], a_r, b_r);
+                        dmma(cr[i][j], a_i, neg(b_i));
+                        dmma(ci[i][j], a_r, b_i);
+                        dmma(ci[i][j], a_i, b_r);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // Epilogue: C fragment (g, 2t..2t+1) of every m8n8 tile, 16-byte stores.
+    const size_t plane = static_cast<size_t>(M) * N;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = m0 + wm * 32 + i * 8 + g;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int col = n0 + wn * 32 + j * 8 + 2 * t;
+            const size_t o = static_cast<size_t>(row) * N + col;
+            *reinterpret_cast<double2*>(out + o) = make_double2(cr[i][j][0], cr[i][j][1]);
+            *reinterpret_cast<double2*>(out + plane + o) = make_double2(ci[i][j][0], ci[i][j][1]);
+        }
+    }
+}
+
+int gemm_tile_rows(int tile) { return tile == kTile128x64 ? 128 : tile == kTile64x64 ? 64 : 32; }
+int gemm_tile_cols(int tile) { return tile == kTile32x32 ? 32 : 64; }
+
+template <int BM, int BN>
+static int configure_zgemm_t() {
+    return static_cast<int>(cudaFuncSetAttribute(zgemm_gen_kernel<BM, BN>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 GemmCfg<BM, BN>::SMEM));
+}
+
+template <int BM, int BN>
+static int launch_zgemm_t(const GemmArgs& a, void* stream) {
+    using C = GemmCfg<BM, BN>;
+    dim3 grid(a.N / BN, a.M / BM);
+    zgemm_gen_kernel<BM, BN><<<grid, C::THREADS, C::SMEM, static_cast<cudaStream_t>(stream)>>>(
+        *static_cast<const CUtensorMap*>(a.tmap), *a.layer, a.out, a.M, a.N);
+    return static_cast<int>(cudaGetLastError());
+}
+
+int launch_zgemm(const GemmArgs& a, int tile, int /*gemm_mode*/, void* stream) {
+    switch (tile) {
+    case kTile128x64: return launch_zgemm_t<128, 64>(a, stream);
+    case kTile64x64: return launch_zgemm_t<64, 64>(a, stream);
+    default: return launch_zgemm_t<32, 32>(a, stream);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// K2s: whole circuit in one CTA (2^n <= 32): launch-latency bound sizes.
+// ----------------------------------------------------------------------------
+
+size_t small_circuit_smem_bytes(int M, int N) {
+    return sizeof(double) * (2 * static_cast<size_t>(M) * N * 2 + 2 * static_cast<size_t>(N) * N);
+}
+
+__global__ void __launch_bounds__(256) small_circuit_kernel(const LayerDesc* __restrict__ layers, int nlayers,
+                                                            uint32_t row_begin, int M, int N,
+                                                            const double* __restrict__ x,
+                                                            double* __restrict__ v_out,
+                                                            double* __restrict__ psi) {
+    extern __shared__ double sm[];
+    const int MN = M * N;
+    double* vr = sm;
+    double* vi = vr + MN;
+    double* tr = vi + MN;
+    double* ti = tr + MN;
+    double* lr = ti + MN;
+    double* li = lr + N * N;
+    const int tid = threadIdx.x;
+    for (int e = tid; e < MN; e += blockDim.x) {
+        layer_entry(layers[0], row_begin + e / N, e % N, vr[e], vi[e]);
+    }
+    for (int l = 1; l < nlayers; ++l) {
+        const LayerDesc& d = layers[l];
+        for (int e = tid; e < N * N; e += blockDim.x) layer_entry(d, e / N, e % N, lr[e], li[e]);
+        __syncthreads();
+        for (int e = tid; e < MN; e += blockDim.x) {
+            const int i = e / N, j = e % N;
+            double sr = 0.0, si = 0.0;
+            for (int k = 0; k < N; ++k) {
+                const double ar = vr[i * N + k], ai = vi[i * N + k];
+                const double br = lr[k * N + j], bi = li[k * N + j];
+                sr = fma(ar, br, fma(-ai, bi, sr));
+                si = fma(ar, bi, fma(ai, br, si));
+            }
+            tr[e] = sr;
+            ti[e] = si;
+        }
+        __syncthreads();
+        for (int e = tid; e < MN; e += blockDim.x) {
+            vr[e] = tr[e];
+            vi[e] = ti[e];
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    for (int e = tid; e < MN; e += blockDim.x) {
+        v_out[e] = vr[e];
+        v_out[MN + e] = vi[e];
+    }
+    for (int i = tid; i < M; i += blockDim.x) {
+        double sr = 0.0, si = 0.0;
+        for (int k = 0; k < N; ++k) {
+            const double ar = vr[i * N + k], ai = vi[i * N + k];
+            sr += ar * x[k] - ai * x[N + k];
+            si += ar * x[N + k] + ai * x[k];
+        }
+        psi[i] = sr;
+        psi[M + i] = si;
+    }
+}
+
+int launch_small_circuit(const LayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, int N,
+                         const double* x, double* v, double* psi, void* stream) {
+    const size_t smem = small_circuit_smem_bytes(M, N);
+    small_circuit_kernel<<<1, 256, smem, static_cast<cudaStream_t>(stream)>>>(d_layers, nlayers, row_begin, M,
+                                                                              N, x, v, psi);
+    return static_cast<int>(cudaGetLastError());
+}
+
+// ----------------------------------------------------------------------------
+// K3: psi = V * x, one warp per row
+// ----------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) matvec_kernel(const double* __restrict__ v, int M, int N,
+                                                     const double* __restrict__ x, double* __restrict__ psi) {
+    const int warps = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const size_t plane = static_cast<size_t>(M) * N;
+    for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < M; row += gridDim.x * warps) {
+        const double2* vr = reinterpret_cast<const double2*>(v + static_cast<size_t>(row) * N);
+        const double2* vi = reinterpret_cast<const double2*>(v + plane + static_cast<size_t>(row) * N);
+        const double2* xr = reinterpret_cast<const double2*>(x);
+        const double2* xi = reinterpret_cast<const double2*>(x + N);
+        double sr = 0.0, si = 0.0;
+        for (int k = lane; k < N / 2; k += 32) {
+            const double2 a = __ldg(vr + k), b = __ldg(vi + k), c = __ldg(xr + k), d = __ldg(xi + k);
+            sr += a.x * c.x - b.x * d.x;
+            si += a.x * d.x + b.x * c.x;
+            sr += a.y * c.y - b.y * d.y;
+            si += a.y * d.y + b.y * c.y;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sr += __shfl_xor_sync(0xffffffffu, sr, o);
+            si += __shfl_xor_sync(0xffffffffu, si, o);
+        }
+        if (lane == 0) {
+            psi[row] = sr;
+            psi[M + row] = si;
+        }
+    }
+}
+
+int launch_matvec(const double* v, int M, int N, const double* x, double* psi, void* stream) {
+    int blocks = (M + 7) / 8;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    matvec_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(v, M, N, x, psi);
+    return static_cast<int>(cudaGetLastError());
+}
+
+// ----------------------------------------------------------------------------
+// K4: probabilities + deterministic norm
+// ----------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) probs_kernel(const double* __restrict__ psi, int64_t dim,
+                                                    double* __restrict__ p, double* __restrict__ partial) {
+    __shared__ double warp_sums[8];
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < dim;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double re = psi[i], im = psi[dim + i];
+        const double v = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+        p[i] = v;
+        s += v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double w = threadIdx.x < (blockDim.x >> 5) ? warp_sums[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+        if (threadIdx.x == 0) partial[blockIdx.x] = w;
+    }
+}
+
+__global__ void reduce_partials_kernel(const double* __restrict__ partial, int n, double* __restrict__ out) {
+    __shared__ double warp_sums[32];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += partial[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double w = threadIdx.x < (blockDim.x >> 5) ? warp_sums[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+        if (threadIdx.x == 0) out[0] = w;
+    }
+}
+
+int launch_probabilities(const double* psi, int64_t dim, double* p, double* partial, int partial_cap,
+                         double* norm, void* stream) {
+    int blocks = static_cast<int>((dim + 255) / 256);
+    if (blocks > partial_cap) blocks = partial_cap;
+    if (blocks < 1) blocks = 1;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    probs_kernel<<<blocks, 256, 0, s>>>(psi, dim, p, partial);
+    reduce_partials_kernel<<<1, 1024, 0, s>>>(partial, blocks, norm);
+    return static_cast<int>(cudaGetLastError());
+}
+
+// Kernel attributes, set once per device before any launch or graph capture.
+int configure_kernels() {
+    int e;
+    if ((e = configure_zgemm_t<128, 64>())) return e;
+    if ((e = configure_zgemm_t<64, 64>())) return e;
+    if ((e = configure_zgemm_t<32, 32>())) return e;
+    return static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+}
+
+}  // namespace qsb

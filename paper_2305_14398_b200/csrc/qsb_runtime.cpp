@@ -1,0 +1,917 @@
+// qsb_runtime.cpp — host runtime behind the C ABI (include/qsb.h).
+//
+// Responsibilities:
+//   * validate a flattened qsim::Circuit exactly where the reference does
+//     (guard, reset placement, registry dimensions: unitary_backend.cpp:194-206,
+//     backend_util.cpp:21-32, unitary_backend.cpp:50-53);
+//   * factor every step into layers with the reference's greedy first-fit
+//     (layered_operands, unitary_backend.cpp:63-91) and order each layer's
+//     blocks qubit-0-first (fill_layer, :95-116) into LayerDesc descriptors;
+//   * run the chain on the GPU: K1 expands the leftmost operator rows, K2
+//     multiplies V <- V * L for every further layer, K3 applies psi0;
+//   * own device memory, the stream, TMA descriptors and the CUDA graph of a plan.
+// No C++ exception crosses the ABI; failures set a thread-local message.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/qsb.h"
+#include "qsb_internal.hpp"
+
+namespace {
+
+thread_local std::string g_error;
+
+struct Failure {
+    qsb_status code;
+    std::string msg;
+};
+
+[[noreturn]] void raise(qsb_status code, const char* fmt, ...) {
+    char buf[768];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    throw Failure{code, buf};
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) raise(QSB_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+void cuda_check(int e, const char* what) { cuda_check(static_cast<cudaError_t>(e), what); }
+
+template <typename F>
+qsb_status guarded(F&& f) {
+    try {
+        f();
+        return QSB_OK;
+    } catch (const Failure& e) {
+        g_error = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_error = "host allocation failed";
+        return QSB_ERR_RESOURCE;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return QSB_ERR_INTERNAL;
+    }
+}
+
+// Restores the caller's current device on scope exit.
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceScope() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t bytes) {
+        if (bytes <= cap) return;
+        release();
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            raise(QSB_ERR_RESOURCE, "device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+        }
+        cap = bytes;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), cap(o.cap) { o.p = nullptr; o.cap = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; cap = o.cap; o.p = nullptr; o.cap = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+};
+
+struct Buffers {
+    DevBuf v[2];     // [2][M][N] doubles each: V and V'
+    DevBuf psi;      // [2][M]
+    DevBuf x;        // [2][N] initial state
+    DevBuf layers;   // LayerDesc[] for the one-CTA path
+    DevBuf tables;   // registered function matrices
+    DevBuf p;        // probabilities
+    DevBuf partial;  // reduction partials + norm
+};
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// Tensor map of a [2][M][N] double buffer, box (16, rows, 2), 128-byte swizzle.
+CUtensorMap make_tmap(void* base, int M, int N, int box_rows) {
+    CUtensorMap m;
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn) raise(QSB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M), 2};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(N) * 8, static_cast<cuuint64_t>(M) * N * 8};
+    const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(box_rows), 2};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) raise(QSB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+    return m;
+}
+
+uint64_t engine_bytes(int n) {  // two V buffers + psi + x
+    const uint64_t N = uint64_t{1} << n;
+    return 2 * 16 * N * N + 3 * 16 * N;
+}
+
+// ---------------------------------------------------------------- compile
+
+struct Compiled {
+    int n = 0;
+    uint32_t N = 0;
+    int n_steps = 0;
+    std::vector<qsb::LayerDesc> app;     // every layer, in application order
+    std::vector<int> app_step;           // step of each layer
+    std::vector<int> app_index;          // layer index within its step
+    std::vector<int> used_functions;     // function indices referenced
+};
+
+struct Interval {
+    int first, span;
+};
+
+Interval interval_of(const qsb_op& op) {
+    if (op.kind == QSB_OP_CONTROL) {
+        const int lo = std::min(op.control, op.target), hi = std::max(op.control, op.target);
+        return {lo, hi - lo + 1};
+    }
+    if (op.kind == QSB_OP_FUNCTION) return {op.first, op.count};
+    return {op.target, 1};
+}
+
+void validate_circuit_shape(const qsb_circuit* c) {
+    if (!c) raise(QSB_ERR_ARGUMENT, "circuit is null");
+    if (c->n_qubits < 1 || c->n_qubits > 30)
+        raise(QSB_ERR_ARGUMENT, "circuit qubit count must be in [1, 30], got %d", c->n_qubits);
+    if (c->n_steps < 0) raise(QSB_ERR_ARGUMENT, "negative step count");
+    if (c->n_steps > 0 && (!c->step_offsets || !c->ops)) raise(QSB_ERR_ARGUMENT, "circuit arrays are null");
+}
+
+// Guard first, then reset placement (unitary_backend.cpp:197-206).
+void check_guard(const qsb_circuit* c, int guard) {
+    if (c->n_qubits > guard) {
+        const uint64_t est = qsb_memory_estimate(c->n_qubits, 0);
+        char a[32], b[32];
+        auto fmt = [](uint64_t bytes, char* buf) {
+            static const char* units[] = {"B", "kB", "MB", "GB", "TB", "PB"};
+            double v = static_cast<double>(bytes);
+            int u = 0;
+            while (v >= 1000.0 && u + 1 < 6) { v /= 1000.0; ++u; }
+            std::snprintf(buf, 32, u == 0 ? "%.0f %s" : "%.2f %s", v, units[u]);
+        };
+        fmt(est, a);
+        fmt(c->n_qubits <= 29 ? engine_bytes(c->n_qubits) : ~uint64_t{0}, b);
+        raise(QSB_ERR_RESOURCE,
+              "unitary-b200 backend refuses %d qubits (guard %d): estimated memory %llu bytes (%s at 8 bytes per "
+              "complex; engine-accurate %s in HBM)",
+              c->n_qubits, guard, static_cast<unsigned long long>(est), a, b);
+    }
+    for (int s = 0; s + 1 < c->n_steps; ++s)
+        for (int i = c->step_offsets[s]; i < c->step_offsets[s + 1]; ++i)
+            if (c->ops[i].kind == QSB_OP_INSTRUCTION && c->ops[i].instruction == QSB_INSTR_RESET)
+                raise(QSB_ERR_VALIDATION, "reset is only supported in the final step");
+}
+
+void check_op(const qsb_circuit* c, const qsb_op& op) {
+    const int n = c->n_qubits;
+    auto q = [&](int v) {
+        if (v < 0 || v >= n) raise(QSB_ERR_ARGUMENT, "qubit index %d out of range for a %d-qubit circuit", v, n);
+    };
+    switch (op.kind) {
+    case QSB_OP_GATE: q(op.target); break;
+    case QSB_OP_CONTROL:
+        q(op.control);
+        q(op.target);
+        if (op.control == op.target) raise(QSB_ERR_ARGUMENT, "control gate: control and target must differ");
+        break;
+    case QSB_OP_FUNCTION: {
+        if (op.count < 1) raise(QSB_ERR_ARGUMENT, "function must span at least one qubit");
+        q(op.first);
+        if (op.first + op.count > n) raise(QSB_ERR_ARGUMENT, "function range exceeds circuit size");
+        if (op.function < 0 || op.function >= c->n_functions || !c->functions)
+            raise(QSB_ERR_LOOKUP, "registry: no function with index %d", op.function);
+        const qsb_function& f = c->functions[op.function];
+        if (f.dim != (int64_t{1} << op.count))  // unitary_backend.cpp:50-53
+            raise(QSB_ERR_VALIDATION, "function %d no longer matches its registered dimension", op.function);
+        if (!f.re || !f.im) raise(QSB_ERR_ARGUMENT, "function %d has null data", op.function);
+        break;
+    }
+    case QSB_OP_INSTRUCTION: q(op.target); break;
+    default: raise(QSB_ERR_ARGUMENT, "unknown operation kind %d", op.kind);
+    }
+}
+
+// Greedy first-fit (unitary_backend.cpp:63-91): layer index of each op of a step.
+std::vector<int> first_fit(const qsb_circuit* c, int step, int* n_layers) {
+    const int b = c->step_offsets[step], e = c->step_offsets[step + 1];
+    if (e < b) raise(QSB_ERR_ARGUMENT, "step offsets are not monotone");
+    std::vector<int> layer(e - b, -1);
+    std::vector<std::vector<Interval>> layers;
+    for (int i = b; i < e; ++i) {
+        const Interval iv = interval_of(c->ops[i]);
+        int placed = -1;
+        for (size_t l = 0; l < layers.size() && placed < 0; ++l) {
+            bool fits = true;
+            for (const Interval& o : layers[l])
+                if (!(iv.first + iv.span <= o.first || o.first + o.span <= iv.first)) fits = false;
+            if (fits) placed = static_cast<int>(l);
+        }
+        if (placed < 0) {
+            placed = static_cast<int>(layers.size());
+            layers.emplace_back();
+        }
+        layers[placed].push_back(iv);
+        layer[i - b] = placed;
+    }
+    *n_layers = static_cast<int>(layers.size());
+    return layer;
+}
+
+// LayerDesc of one layer: non-identity blocks sorted by first qubit (fill_layer order).
+qsb::LayerDesc build_layer(const qsb_circuit* c, int step, const std::vector<int>& layer_of, int layer) {
+    const int n = c->n_qubits;
+    const int b = c->step_offsets[step];
+    std::vector<int> ops;
+    for (size_t i = 0; i < layer_of.size(); ++i)
+        if (layer_of[i] == layer) ops.push_back(b + static_cast<int>(i));
+    std::sort(ops.begin(), ops.end(),
+              [&](int x, int y) { return interval_of(c->ops[x]).first < interval_of(c->ops[y]).first; });
+    qsb::LayerDesc d;
+    std::memset(&d, 0, sizeof d);
+    uint32_t covered = 0;
+    int nb = 0;
+    for (int i : ops) {
+        const qsb_op& op = c->ops[i];
+        if (op.kind == QSB_OP_INSTRUCTION) continue;  // identity(2) (unitary_backend.cpp:56-57)
+        const Interval iv = interval_of(op);
+        qsb::BlockDesc& blk = d.blocks[nb++];
+        blk.shift = n - iv.first - iv.span;
+        blk.span = iv.span;
+        blk.mask = (iv.span >= 32) ? 0xffffffffu : ((1u << iv.span) - 1u);
+        covered |= blk.mask << blk.shift;
+        if (op.kind == QSB_OP_GATE) {
+            blk.kind = qsb::kBlockGate;
+        } else if (op.kind == QSB_OP_CONTROL) {
+            blk.kind = qsb::kBlockControlled;
+            blk.cmask = 1u << (iv.span - 1 - (op.control - iv.first));
+            blk.tmask = 1u << (iv.span - 1 - (op.target - iv.first));
+        } else {
+            blk.kind = qsb::kBlockTable;
+            blk.t_re = nullptr;  // patched with device pointers at upload
+            blk.t_im = reinterpret_cast<const double*>(static_cast<intptr_t>(op.function));
+        }
+        for (int e = 0; e < 4; ++e) {
+            blk.u_re[e] = op.u_re[e];
+            blk.u_im[e] = op.u_im[e];
+        }
+    }
+    d.nblocks = nb;
+    const uint32_t all = (n >= 32) ? 0xffffffffu : ((1u << n) - 1u);
+    d.idmask = all & ~covered;
+    return d;
+}
+
+Compiled compile(const qsb_circuit* c) {
+    Compiled out;
+    out.n = c->n_qubits;
+    out.N = 1u << c->n_qubits;
+    out.n_steps = c->n_steps;
+    std::vector<char> used(static_cast<size_t>(std::max(c->n_functions, 0)), 0);
+    for (int s = 0; s < c->n_steps; ++s) {
+        for (int i = c->step_offsets[s]; i < c->step_offsets[s + 1]; ++i) {
+            check_op(c, c->ops[i]);
+            if (c->ops[i].kind == QSB_OP_FUNCTION) used[c->ops[i].function] = 1;
+        }
+        int nl = 0;
+        const std::vector<int> layer_of = first_fit(c, s, &nl);
+        for (int l = 0; l < nl; ++l) {
+            out.app.push_back(build_layer(c, s, layer_of, l));
+            out.app_step.push_back(s);
+            out.app_index.push_back(l);
+        }
+    }
+    for (size_t f = 0; f < used.size(); ++f)
+        if (used[f]) out.used_functions.push_back(static_cast<int>(f));
+    return out;
+}
+
+qsb::LayerDesc identity_layer(int n) {
+    qsb::LayerDesc d;
+    std::memset(&d, 0, sizeof d);
+    d.idmask = (1u << n) - 1u;
+    return d;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ handle
+
+struct qsb_handle {
+    int device = 0;
+    int guard = 0;
+    int gemm_mode = QSB_GEMM_AUTO;
+    int flags = 0;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    Buffers cache;
+};
+
+struct qsb_plan {
+    qsb_handle* h = nullptr;
+    Compiled cc;
+    std::vector<qsb::LayerDesc> chain;  // row-form order: chain[0] expanded, chain[1..] multiplied
+    int n_identity = 0;
+    int64_t row_begin = 0, row_count = 0;  // requested shard
+    int64_t eff_begin = 0;                 // computed rows [eff_begin, eff_begin + M)
+    int M = 0;
+    int N = 0;
+    int tile = qsb::kTile32x32;
+    bool small = false;
+    Buffers b;
+    bool borrowed = false;
+    CUtensorMap tmap[2];
+    int final_buf = 0;
+    cudaGraphExec_t graph = nullptr;
+    bool timing = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    bool timed_run = false;
+    qsb_plan_info info{};
+};
+
+namespace {
+
+void upload_tables(qsb_plan* p, const qsb_circuit* c) {
+    size_t total = 0;
+    std::vector<size_t> off(static_cast<size_t>(std::max(c->n_functions, 0)), 0);
+    for (int f : p->cc.used_functions) {
+        off[f] = total;
+        total += 2 * static_cast<size_t>(c->functions[f].dim) * c->functions[f].dim;
+    }
+    if (total == 0) return;
+    p->b.tables.ensure(total * sizeof(double));
+    double* base = p->b.tables.as<double>();
+    for (int f : p->cc.used_functions) {
+        const size_t d2 = static_cast<size_t>(c->functions[f].dim) * c->functions[f].dim;
+        cuda_check(cudaMemcpy(base + off[f], c->functions[f].re, d2 * 8, cudaMemcpyHostToDevice), "upload function");
+        cuda_check(cudaMemcpy(base + off[f] + d2, c->functions[f].im, d2 * 8, cudaMemcpyHostToDevice),
+                   "upload function");
+    }
+    auto patch = [&](qsb::LayerDesc& d) {
+        for (int i = 0; i < d.nblocks; ++i) {
+            qsb::BlockDesc& blk = d.blocks[i];
+            if (blk.kind != qsb::kBlockTable) continue;
+            const int f = static_cast<int>(reinterpret_cast<intptr_t>(blk.t_im));
+            const size_t d2 = static_cast<size_t>(c->functions[f].dim) * c->functions[f].dim;
+            blk.t_re = base + off[f];
+            blk.t_im = base + off[f] + d2;
+        }
+    };
+    for (auto& d : p->cc.app) patch(d);
+}
+
+int pick_tile(int M, int N) {
+    const int sms = 148;
+    if (M % 128 == 0 && N % 64 == 0 && (M / 128) * (N / 64) >= 2 * sms) return qsb::kTile128x64;
+    if (M % 64 == 0 && N % 64 == 0 && (M / 64) * (N / 64) >= sms) return qsb::kTile64x64;
+    if (M % 128 == 0 && N % 64 == 0 && (M / 128) * (N / 64) >= sms) return qsb::kTile128x64;
+    return qsb::kTile32x32;
+}
+
+// Build a plan; the caller holds the handle mutex when borrow_cache is set.
+std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, const qsb_circuit* c, int64_t row_begin, int64_t row_count,
+                                    bool borrow_cache) {
+    validate_circuit_shape(c);
+    check_guard(c, h->guard);
+    auto p = std::make_unique<qsb_plan>();
+    p->h = h;
+    p->cc = compile(c);
+    const int n = c->n_qubits;
+    const int64_t N = int64_t{1} << n;
+    if (row_count < 0 || row_begin < 0 || row_begin + row_count > N)
+        raise(QSB_ERR_ARGUMENT, "row shard [%lld, %lld) outside [0, %lld)", static_cast<long long>(row_begin),
+              static_cast<long long>(row_begin + row_count), static_cast<long long>(N));
+    if (row_count == 0) raise(QSB_ERR_ARGUMENT, "row shard is empty");
+    p->N = static_cast<int>(N);
+    p->row_begin = row_begin;
+    p->row_count = row_count;
+    // Row-form chain: reverse application order; instruction-only layers are exact identities.
+    for (auto it = p->cc.app.rbegin(); it != p->cc.app.rend(); ++it) {
+        if (it->nblocks == 0)
+            ++p->n_identity;
+        else
+            p->chain.push_back(*it);
+    }
+    p->small = N <= 32;
+    int64_t M = row_count;
+    if (!p->small) {
+        // The tiled kernels need at least 32 rows and power-of-two shards; widen
+        // the computed window if needed (the extra rows are discarded).
+        int64_t want = 32;
+        while (want < M) want <<= 1;
+        M = std::min<int64_t>(want, N);
+    } else {
+        M = N;  // the one-CTA kernel computes all rows
+    }
+    p->M = static_cast<int>(M);
+    p->eff_begin = p->small ? 0 : (row_begin / M) * M;
+    if (row_begin + row_count > p->eff_begin + M)
+        raise(QSB_ERR_ARGUMENT, "row shard [%lld, +%lld) is not contained in one aligned window of %lld rows",
+              static_cast<long long>(row_begin), static_cast<long long>(row_count), static_cast<long long>(M));
+    p->tile = p->small ? qsb::kTile32x32 : pick_tile(p->M, p->N);
+
+    DeviceScope ds(h->device);
+    if (borrow_cache) {
+        p->b = std::move(h->cache);
+        p->borrowed = true;
+    }
+    const size_t plane_bytes = static_cast<size_t>(M) * N * 8;
+    p->b.v[0].ensure(2 * plane_bytes);
+    if (!p->small && p->chain.size() > 1) p->b.v[1].ensure(2 * plane_bytes);
+    p->b.psi.ensure(2 * static_cast<size_t>(M) * 8);
+    p->b.x.ensure(2 * static_cast<size_t>(N) * 8);
+    upload_tables(p.get(), c);
+    // re-derive the chain with patched table pointers
+    p->chain.clear();
+    for (auto it = p->cc.app.rbegin(); it != p->cc.app.rend(); ++it)
+        if (it->nblocks != 0) p->chain.push_back(*it);
+    if (p->chain.empty()) p->chain.push_back(identity_layer(n));
+    // psi0 = |0...0> (zero_state, state.cpp:37-47)
+    std::vector<double> x(2 * static_cast<size_t>(N), 0.0);
+    x[0] = 1.0;
+    cuda_check(cudaMemcpy(p->b.x.p, x.data(), x.size() * 8, cudaMemcpyHostToDevice), "upload psi0");
+    if (p->small) {
+        p->b.layers.ensure(sizeof(qsb::LayerDesc) * p->chain.size());
+        cuda_check(cudaMemcpy(p->b.layers.p, p->chain.data(), sizeof(qsb::LayerDesc) * p->chain.size(),
+                              cudaMemcpyHostToDevice),
+                   "upload layers");
+    } else {
+        const int rows = qsb::gemm_tile_rows(p->tile);
+        p->tmap[0] = make_tmap(p->b.v[0].p, p->M, p->N, rows);
+        if (p->b.v[1].p) p->tmap[1] = make_tmap(p->b.v[1].p, p->M, p->N, rows);
+    }
+    const int gemms = p->small ? static_cast<int>(p->chain.size()) - 1 : static_cast<int>(p->chain.size()) - 1;
+    qsb_plan_info& in = p->info;
+    in.n_qubits = n;
+    in.n_steps = c->n_steps;
+    in.n_layers = static_cast<int>(p->cc.app.size());
+    in.n_gemms = gemms;
+    in.n_identity_layers = p->n_identity;
+    in.n_launches = p->small ? 1 : 1 + gemms + 1;
+    in.row_begin = row_begin;
+    in.row_count = row_count;
+    in.gemm_flops = 8.0 * static_cast<double>(p->M) * static_cast<double>(N) * static_cast<double>(N) * gemms;
+    in.expand_bytes = p->small ? 0.0 : 16.0 * static_cast<double>(p->M) * static_cast<double>(N);
+    return p;
+}
+
+void release_plan(std::unique_ptr<qsb_plan>& p) {
+    if (!p) return;
+    DeviceScope ds(p->h->device);
+    if (p->graph) cudaGraphExecDestroy(p->graph);
+    for (auto& e : p->ev)
+        if (e) cudaEventDestroy(e);
+    if (p->borrowed) p->h->cache = std::move(p->b);
+    p.reset();
+}
+
+void enqueue(qsb_plan* p, cudaStream_t s) {
+    const uint32_t rb = static_cast<uint32_t>(p->eff_begin);
+    if (p->small) {
+        cuda_check(qsb::launch_small_circuit(p->b.layers.as<qsb::LayerDesc>(), static_cast<int>(p->chain.size()), rb,
+                                             p->M, p->N, p->b.x.as<double>(), p->b.v[0].as<double>(),
+                                             p->b.psi.as<double>(), s),
+                   "small_circuit_kernel");
+        p->final_buf = 0;
+        return;
+    }
+    const bool ev = p->timing && p->timed_run;
+    if (ev) cuda_check(cudaEventRecord(p->ev[0], s), "event");
+    cuda_check(qsb::launch_expand(p->chain[0], rb, p->M, p->N, p->b.v[0].as<double>(), s), "expand_kernel");
+    if (ev) cuda_check(cudaEventRecord(p->ev[1], s), "event");
+    int cur = 0;
+    for (size_t i = 1; i < p->chain.size(); ++i) {
+        qsb::GemmArgs a{&p->tmap[cur], &p->chain[i], p->b.v[1 - cur].as<double>(), p->M, p->N};
+        cuda_check(qsb::launch_zgemm(a, p->tile, p->h->gemm_mode, s), "zgemm_gen_kernel");
+        cur ^= 1;
+    }
+    if (ev) cuda_check(cudaEventRecord(p->ev[2], s), "event");
+    cuda_check(qsb::launch_matvec(p->b.v[cur].as<double>(), p->M, p->N, p->b.x.as<double>(), p->b.psi.as<double>(), s),
+               "matvec_kernel");
+    if (ev) cuda_check(cudaEventRecord(p->ev[3], s), "event");
+    p->final_buf = cur;
+}
+
+void execute(qsb_plan* p, cudaStream_t s, bool allow_graph) {
+    DeviceScope ds(p->h->device);
+    const bool use_graph = allow_graph && !p->timing && !(p->h->flags & QSB_FLAG_NO_GRAPH);
+    p->timed_run = p->timing;
+    if (p->timing) {
+        for (auto& e : p->ev)
+            if (!e) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    }
+    if (!use_graph) {
+        enqueue(p, s);
+        return;
+    }
+    if (!p->graph) {
+        cudaGraph_t g = nullptr;
+        cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+        try {
+            enqueue(p, s);
+        } catch (...) {
+            cudaStreamEndCapture(s, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        cuda_check(cudaStreamEndCapture(s, &g), "cudaStreamEndCapture");
+        cudaError_t e = cudaGraphInstantiate(&p->graph, g, 0);
+        cudaGraphDestroy(g);
+        cuda_check(e, "cudaGraphInstantiate");
+    }
+    cuda_check(cudaGraphLaunch(p->graph, s), "cudaGraphLaunch");
+}
+
+const double* psi_rows(const qsb_plan* p) { return p->b.psi.as<double>() + (p->row_begin - p->eff_begin); }
+
+}  // namespace
+
+// ------------------------------------------------------------------ C ABI
+
+extern "C" {
+
+int qsb_abi_version(void) { return QSB_ABI_VERSION; }
+
+size_t qsb_last_error(char* buf, size_t len) {
+    if (buf && len) {
+        std::snprintf(buf, len, "%s", g_error.c_str());
+    }
+    return g_error.size();
+}
+
+qsb_status qsb_create(const qsb_options* options, qsb_handle** out) {
+    return guarded([&] {
+        if (!out) raise(QSB_ERR_ARGUMENT, "out is null");
+        *out = nullptr;
+        qsb_options o{0, 0, QSB_GEMM_AUTO, 0};
+        if (options) o = *options;
+        int count = 0;
+        cudaError_t e = cudaGetDeviceCount(&count);
+        if (e != cudaSuccess || count == 0) {
+            cudaGetLastError();
+            raise(QSB_ERR_CUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
+        }
+        if (o.device < 0 || o.device >= count) raise(QSB_ERR_ARGUMENT, "device %d out of range", o.device);
+        auto h = std::make_unique<qsb_handle>();
+        h->device = o.device;
+        h->gemm_mode = o.gemm_mode;
+        h->flags = o.flags;
+        DeviceScope ds(o.device);
+        cudaDeviceProp prop;
+        cuda_check(cudaGetDeviceProperties(&prop, o.device), "cudaGetDeviceProperties");
+        if (prop.major < 10)
+            raise(QSB_ERR_CUDA, "device %d (%s, sm_%d%d) is not sm_100a", o.device, prop.name, prop.major, prop.minor);
+        cuda_check(qsb::configure_kernels(), "configure kernels");
+        // HBM-derived default guard: both V buffers must fit in 92% of device memory.
+        int hbm_guard = 1;
+        for (int n = 1; n <= qsb::kMaxQubits; ++n)
+            if (static_cast<double>(engine_bytes(n)) <= 0.92 * static_cast<double>(prop.totalGlobalMem)) hbm_guard = n;
+        h->guard = o.qubit_guard > 0 ? std::min(o.qubit_guard, qsb::kMaxQubits) : hbm_guard;
+        cuda_check(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        *out = h.release();
+    });
+}
+
+qsb_status qsb_destroy(qsb_handle* h) {
+    return guarded([&] {
+        if (!h) return;
+        {
+            DeviceScope ds(h->device);
+            std::lock_guard<std::mutex> lk(h->mu);
+            if (h->stream) cudaStreamDestroy(h->stream);
+            h->cache = Buffers{};
+        }
+        delete h;
+    });
+}
+
+qsb_status qsb_qubit_guard(const qsb_handle* h, int32_t* guard) {
+    return guarded([&] {
+        if (!h || !guard) raise(QSB_ERR_ARGUMENT, "null argument");
+        *guard = h->guard;
+    });
+}
+
+static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re, const double* psi0_im,
+                     double* psi_re, double* psi_im, double* u_re, double* u_im) {
+    std::lock_guard<std::mutex> lk(h->mu);
+    validate_circuit_shape(c);
+    std::unique_ptr<qsb_plan> p;
+    try {
+        p = make_plan(h, c, 0, int64_t{1} << c->n_qubits, true);
+        DeviceScope ds(h->device);
+        const size_t N = static_cast<size_t>(p->N);
+        if (psi0_re) {
+            cuda_check(cudaMemcpyAsync(p->b.x.p, psi0_re, N * 8, cudaMemcpyHostToDevice, h->stream), "upload psi0");
+            cuda_check(cudaMemcpyAsync(p->b.x.as<double>() + N, psi0_im, N * 8, cudaMemcpyHostToDevice, h->stream),
+                       "upload psi0");
+        }
+        execute(p.get(), h->stream, false);
+        if (psi_re) {
+            cuda_check(cudaMemcpyAsync(psi_re, p->b.psi.p, N * 8, cudaMemcpyDeviceToHost, h->stream), "download psi");
+            cuda_check(cudaMemcpyAsync(psi_im, p->b.psi.as<double>() + N, N * 8, cudaMemcpyDeviceToHost, h->stream),
+                       "download psi");
+        }
+        if (u_re) {
+            const double* v = p->b.v[p->final_buf].as<double>();
+            cuda_check(cudaMemcpyAsync(u_re, v, N * N * 8, cudaMemcpyDeviceToHost, h->stream), "download U");
+            cuda_check(cudaMemcpyAsync(u_im, v + N * N, N * N * 8, cudaMemcpyDeviceToHost, h->stream), "download U");
+        }
+        cuda_check(cudaStreamSynchronize(h->stream), "cudaStreamSynchronize");
+    } catch (...) {
+        release_plan(p);
+        throw;
+    }
+    release_plan(p);
+}
+
+qsb_status qsb_simulate_full_state(qsb_handle* h, const qsb_circuit* c, double* psi_re, double* psi_im) {
+    return guarded([&] {
+        if (!h || !psi_re || !psi_im) raise(QSB_ERR_ARGUMENT, "null argument");
+        run_full(h, c, nullptr, nullptr, psi_re, psi_im, nullptr, nullptr);
+    });
+}
+
+qsb_status qsb_simulate_from_state(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
+                                   const double* psi0_im, double* psi_re, double* psi_im) {
+    return guarded([&] {
+        if (!h || !psi0_re || !psi0_im || !psi_re || !psi_im) raise(QSB_ERR_ARGUMENT, "null argument");
+        run_full(h, c, psi0_re, psi0_im, psi_re, psi_im, nullptr, nullptr);
+    });
+}
+
+qsb_status qsb_build_unitary(qsb_handle* h, const qsb_circuit* c, double* u_re, double* u_im) {
+    return guarded([&] {
+        if (!h || !u_re || !u_im) raise(QSB_ERR_ARGUMENT, "null argument");
+        run_full(h, c, nullptr, nullptr, nullptr, nullptr, u_re, u_im);
+    });
+}
+
+qsb_status qsb_simulate_and_collapse(qsb_handle* h, const qsb_circuit* c, uint64_t seed, uint64_t* basis_index) {
+    return guarded([&] {
+        if (!h || !basis_index) raise(QSB_ERR_ARGUMENT, "null argument");
+        validate_circuit_shape(c);
+        const size_t N = size_t{1} << c->n_qubits;
+        std::vector<double> re(N), im(N), p(N);
+        run_full(h, c, nullptr, nullptr, re.data(), im.data(), nullptr, nullptr);
+        double norm = 0.0;
+        qsb_status st = qsb_probabilities(h, re.data(), im.data(), static_cast<int64_t>(N), p.data(), &norm);
+        if (st != QSB_OK) throw Failure{st, g_error};
+        // collapse (state.cpp:81-98): SplitMix64 draw, sequential inverse CDF.
+        uint64_t state = seed;
+        uint64_t z = (state += 0x9E3779B97F4A7C15ULL);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        z = z ^ (z >> 31);
+        const double u = static_cast<double>(z >> 11) * 0x1.0p-53;
+        double cumulative = 0.0;
+        uint64_t fallback = 0;
+        for (size_t i = 0; i < N; ++i) {
+            if (p[i] > 0.0) fallback = i;
+            cumulative += p[i];
+            if (cumulative > u) {
+                *basis_index = i;
+                return;
+            }
+        }
+        *basis_index = fallback;
+    });
+}
+
+qsb_status qsb_step_layer_count(const qsb_circuit* c, int32_t step, int32_t* layers) {
+    return guarded([&] {
+        validate_circuit_shape(c);
+        if (!layers) raise(QSB_ERR_ARGUMENT, "null argument");
+        if (step < 0 || step >= c->n_steps) raise(QSB_ERR_ARGUMENT, "step %d out of range", step);
+        int nl = 0;
+        first_fit(c, step, &nl);
+        *layers = nl;
+    });
+}
+
+qsb_status qsb_layer_operator(qsb_handle* h, const qsb_circuit* c, int32_t step, int32_t layer, double* re,
+                              double* im) {
+    return guarded([&] {
+        if (!h || !re || !im) raise(QSB_ERR_ARGUMENT, "null argument");
+        std::lock_guard<std::mutex> lk(h->mu);
+        validate_circuit_shape(c);
+        if (c->n_qubits > h->guard) check_guard(c, h->guard);
+        if (step < 0 || step >= c->n_steps) raise(QSB_ERR_ARGUMENT, "step %d out of range", step);
+        Compiled cc = compile(c);
+        int idx = -1;
+        for (size_t i = 0; i < cc.app.size(); ++i)
+            if (cc.app_step[i] == step && cc.app_index[i] == layer) idx = static_cast<int>(i);
+        if (idx < 0) raise(QSB_ERR_ARGUMENT, "layer %d out of range for step %d", layer, step);
+        DeviceScope ds(h->device);
+        const size_t N = size_t{1} << c->n_qubits;
+        qsb_plan tmp;  // for table upload
+        tmp.h = h;
+        tmp.cc = std::move(cc);
+        tmp.b = std::move(h->cache);
+        try {
+            upload_tables(&tmp, c);
+            tmp.b.v[0].ensure(2 * N * N * 8);
+            cuda_check(qsb::launch_expand(tmp.cc.app[idx], 0, static_cast<int>(N), static_cast<int>(N),
+                                          tmp.b.v[0].as<double>(), h->stream),
+                       "expand_kernel");
+            cuda_check(cudaMemcpyAsync(re, tmp.b.v[0].p, N * N * 8, cudaMemcpyDeviceToHost, h->stream), "download");
+            cuda_check(cudaMemcpyAsync(im, tmp.b.v[0].as<double>() + N * N, N * N * 8, cudaMemcpyDeviceToHost,
+                                       h->stream),
+                       "download");
+            cuda_check(cudaStreamSynchronize(h->stream), "cudaStreamSynchronize");
+        } catch (...) {
+            h->cache = std::move(tmp.b);
+            throw;
+        }
+        h->cache = std::move(tmp.b);
+    });
+}
+
+qsb_status qsb_probabilities(qsb_handle* h, const double* psi_re, const double* psi_im, int64_t dim, double* p,
+                             double* norm_squared) {
+    return guarded([&] {
+        if (!h || !psi_re || !psi_im || !p || !norm_squared || dim < 1) raise(QSB_ERR_ARGUMENT, "bad argument");
+        std::lock_guard<std::mutex> lk(h->mu);
+        DeviceScope ds(h->device);
+        Buffers& b = h->cache;
+        const int cap = 4096;
+        b.psi.ensure(2 * static_cast<size_t>(dim) * 8);
+        b.p.ensure(static_cast<size_t>(dim) * 8);
+        b.partial.ensure((cap + 1) * 8);
+        double* psi = b.psi.as<double>();
+        cuda_check(cudaMemcpyAsync(psi, psi_re, dim * 8, cudaMemcpyHostToDevice, h->stream), "upload");
+        cuda_check(cudaMemcpyAsync(psi + dim, psi_im, dim * 8, cudaMemcpyHostToDevice, h->stream), "upload");
+        double* partial = b.partial.as<double>();
+        cuda_check(qsb::launch_probabilities(psi, dim, b.p.as<double>(), partial, cap, partial + cap, h->stream),
+                   "probs_kernel");
+        cuda_check(cudaMemcpyAsync(p, b.p.p, dim * 8, cudaMemcpyDeviceToHost, h->stream), "download");
+        cuda_check(cudaMemcpyAsync(norm_squared, partial + cap, 8, cudaMemcpyDeviceToHost, h->stream), "download");
+        cuda_check(cudaStreamSynchronize(h->stream), "cudaStreamSynchronize");
+    });
+}
+
+qsb_status qsb_plan_create(qsb_handle* h, const qsb_circuit* c, int64_t row_begin, int64_t row_count,
+                           qsb_plan** out) {
+    return guarded([&] {
+        if (!h || !out) raise(QSB_ERR_ARGUMENT, "null argument");
+        *out = nullptr;
+        std::unique_ptr<qsb_plan> p = make_plan(h, c, row_begin, row_count, false);
+        *out = p.release();
+    });
+}
+
+qsb_status qsb_plan_destroy(qsb_plan* plan) {
+    return guarded([&] {
+        std::unique_ptr<qsb_plan> p(plan);
+        release_plan(p);
+    });
+}
+
+qsb_status qsb_plan_get_info(const qsb_plan* plan, qsb_plan_info* info) {
+    return guarded([&] {
+        if (!plan || !info) raise(QSB_ERR_ARGUMENT, "null argument");
+        *info = plan->info;
+    });
+}
+
+qsb_status qsb_plan_set_timing(qsb_plan* plan, int32_t enable) {
+    return guarded([&] {
+        if (!plan) raise(QSB_ERR_ARGUMENT, "null argument");
+        plan->timing = enable != 0;
+    });
+}
+
+qsb_status qsb_plan_execute(qsb_plan* plan, void* stream) {
+    return guarded([&] {
+        if (!plan) raise(QSB_ERR_ARGUMENT, "null argument");
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->h->stream;
+        execute(plan, s, true);
+    });
+}
+
+qsb_status qsb_plan_set_initial_state(qsb_plan* plan, const double* re, const double* im, void* stream) {
+    return guarded([&] {
+        if (!plan || !re || !im) raise(QSB_ERR_ARGUMENT, "null argument");
+        DeviceScope ds(plan->h->device);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->h->stream;
+        const size_t N = static_cast<size_t>(plan->N);
+        cuda_check(cudaMemcpyAsync(plan->b.x.p, re, N * 8, cudaMemcpyDefault, s), "copy psi0");
+        cuda_check(cudaMemcpyAsync(plan->b.x.as<double>() + N, im, N * 8, cudaMemcpyDefault, s), "copy psi0");
+    });
+}
+
+qsb_status qsb_plan_unitary_device(const qsb_plan* plan, const double** re, const double** im) {
+    return guarded([&] {
+        if (!plan || !re || !im) raise(QSB_ERR_ARGUMENT, "null argument");
+        const double* v = plan->b.v[plan->final_buf].as<double>();
+        const size_t plane = static_cast<size_t>(plan->M) * plan->N;
+        const size_t off = static_cast<size_t>(plan->row_begin - plan->eff_begin) * plan->N;
+        *re = v + off;
+        *im = v + plane + off;
+    });
+}
+
+qsb_status qsb_plan_state_device(const qsb_plan* plan, const double** re, const double** im) {
+    return guarded([&] {
+        if (!plan || !re || !im) raise(QSB_ERR_ARGUMENT, "null argument");
+        *re = psi_rows(plan);
+        *im = psi_rows(plan) + plan->M;
+    });
+}
+
+qsb_status qsb_plan_copy_state(const qsb_plan* plan, double* dst_re, double* dst_im, void* stream) {
+    return guarded([&] {
+        if (!plan || !dst_re || !dst_im) raise(QSB_ERR_ARGUMENT, "null argument");
+        DeviceScope ds(plan->h->device);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->h->stream;
+        const size_t bytes = static_cast<size_t>(plan->row_count) * 8;
+        cuda_check(cudaMemcpyAsync(dst_re, psi_rows(plan), bytes, cudaMemcpyDefault, s), "copy psi");
+        cuda_check(cudaMemcpyAsync(dst_im, psi_rows(plan) + plan->M, bytes, cudaMemcpyDefault, s), "copy psi");
+    });
+}
+
+qsb_status qsb_plan_last_timing(qsb_plan* plan, double* total_ms, double* gemm_ms, double* gemm_mean_ms) {
+    return guarded([&] {
+        if (!plan || !total_ms || !gemm_ms || !gemm_mean_ms) raise(QSB_ERR_ARGUMENT, "null argument");
+        if (!plan->timing || !plan->timed_run || !plan->ev[0] || plan->small)
+            raise(QSB_ERR_ARGUMENT, "no timed execute on this plan (qsb_plan_set_timing, tiled path only)");
+        DeviceScope ds(plan->h->device);
+        cuda_check(cudaEventSynchronize(plan->ev[3]), "cudaEventSynchronize");
+        float t = 0, g = 0;
+        cuda_check(cudaEventElapsedTime(&t, plan->ev[0], plan->ev[3]), "cudaEventElapsedTime");
+        cuda_check(cudaEventElapsedTime(&g, plan->ev[1], plan->ev[2]), "cudaEventElapsedTime");
+        *total_ms = t;
+        *gemm_ms = g;
+        *gemm_mean_ms = plan->info.n_gemms > 0 ? g / plan->info.n_gemms : 0.0;
+    });
+}
+
+uint64_t qsb_memory_estimate(int32_t n_qubits, int32_t kind) {
+    // unitary_backend.cpp:156-166 (8 bytes per complex, the paper's accounting)
+    if (n_qubits < 1 || n_qubits > 30) return 0;
+    const uint64_t dim = uint64_t{1} << n_qubits;
+    return kind == 0 ? dim * dim * 8 + dim * 8 : dim * 8;
+}
+
+uint64_t qsb_engine_memory_estimate(int32_t n_qubits, int32_t kind) {
+    // this engine: two 2^n x 2^n complex buffers (V, V') + psi0 + psi, 16 bytes per complex
+    if (n_qubits < 1 || n_qubits > 29) return 0;
+    return kind == 0 ? engine_bytes(n_qubits) : (uint64_t{1} << n_qubits) * 16;
+}
+
+}  // extern "C"

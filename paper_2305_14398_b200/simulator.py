@@ -1,0 +1,275 @@
+"""Simulator plugin interface + the B200 backend, mirroring
+core/include/qsim/simulator.hpp:32-68 and core/src/simulator.cpp:26-82.
+
+``B200UnitarySimulator`` is registered as ``"unitary-b200"``. Every call goes
+through libqsb.so's C ABI (include/qsb.h); nothing here computes amplitudes.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+from typing import Callable, Dict, List, Optional, Tuple
+
+import numpy as np
+
+from . import native
+from .circuit import Circuit, GateRegistry
+from .errors import LookupError_
+
+BACKEND_ID = "unitary-b200"
+
+
+@dataclass
+class StateVector:
+    """StateVector (state.hpp:46-51): amplitudes as re/im planes."""
+
+    n_qubits: int
+    re: np.ndarray
+    im: np.ndarray
+
+    def dimension(self) -> int:
+        return len(self.re)
+
+    @property
+    def amplitudes(self) -> np.ndarray:
+        return self.re + 1j * self.im
+
+
+@dataclass
+class CollapsedState:
+    """CollapsedState (state.hpp:66-72)."""
+
+    n_qubits: int
+    basis_index: int
+
+    def bitstring(self) -> str:
+        return "".join("1" if (self.basis_index >> (self.n_qubits - 1 - q)) & 1 else "0"
+                       for q in range(self.n_qubits))
+
+
+@dataclass
+class SimulatorOptions:
+    """SimulatorOptions (simulator.hpp:53-56)."""
+
+    qubit_guard: Optional[int] = None
+
+
+class Simulator:
+    """Simulator (simulator.hpp:32-51)."""
+
+    def name(self) -> str:
+        raise NotImplementedError
+
+    def qubit_guard(self) -> int:
+        raise NotImplementedError
+
+    def simulate_full_state(self, circuit: Circuit, registry: Optional[GateRegistry] = None) -> StateVector:
+        raise NotImplementedError
+
+    def simulate_and_collapse(self, circuit: Circuit, registry: Optional[GateRegistry],
+                              seed: int) -> CollapsedState:
+        raise NotImplementedError
+
+
+class Plan:
+    """A device-resident compiled circuit for rows [row_begin, row_begin+row_count)
+    of U (qsb_plan_*). Used by the benchmark and the multi-GPU row sharding."""
+
+    def __init__(self, sim: "B200UnitarySimulator", flat: native.FlatCircuit, row_begin: int, row_count: int):
+        self._flat = flat
+        self._sim = sim
+        self._p = ctypes.c_void_p()
+        native.check(native.lib().qsb_plan_create(sim._h, flat.ptr, row_begin, row_count, ctypes.byref(self._p)))
+        self.info = native.QsbPlanInfo()
+        native.check(native.lib().qsb_plan_get_info(self._p, ctypes.byref(self.info)))
+
+    def set_timing(self, enable: bool) -> None:
+        native.check(native.lib().qsb_plan_set_timing(self._p, 1 if enable else 0))
+
+    def set_initial_state(self, re_ptr: int, im_ptr: int, stream: int = 0) -> None:
+        native.check(native.lib().qsb_plan_set_initial_state(self._p, re_ptr, im_ptr, stream or None))
+
+    def execute(self, stream: int = 0) -> None:
+        native.check(native.lib().qsb_plan_execute(self._p, stream or None))
+
+    def copy_state(self, dst_re_ptr: int, dst_im_ptr: int, stream: int = 0) -> None:
+        native.check(native.lib().qsb_plan_copy_state(self._p, dst_re_ptr, dst_im_ptr, stream or None))
+
+    def unitary_device(self) -> Tuple[int, int]:
+        re, im = ctypes.c_void_p(), ctypes.c_void_p()
+        native.check(native.lib().qsb_plan_unitary_device(self._p, ctypes.byref(re), ctypes.byref(im)))
+        return re.value, im.value
+
+    def state_device(self) -> Tuple[int, int]:
+        re, im = ctypes.c_void_p(), ctypes.c_void_p()
+        native.check(native.lib().qsb_plan_state_device(self._p, ctypes.byref(re), ctypes.byref(im)))
+        return re.value, im.value
+
+    def last_timing(self) -> Tuple[float, float, float]:
+        t, g, m = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        native.check(native.lib().qsb_plan_last_timing(self._p, ctypes.byref(t), ctypes.byref(g), ctypes.byref(m)))
+        return t.value, g.value, m.value
+
+    def close(self) -> None:
+        if self._p:
+            native.lib().qsb_plan_destroy(self._p)
+            self._p = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class B200UnitarySimulator(Simulator):
+    """The drop-in backend: Algorithm 1 on B200 (unitary_backend.cpp:194-215)."""
+
+    def __init__(self, qubit_guard: Optional[int] = None, device: int = 0,
+                 gemm_mode: int = native.GEMM_AUTO, flags: int = 0) -> None:
+        L = native.lib()
+        opts = native.QsbOptions(device, int(qubit_guard or 0), gemm_mode, flags)
+        self._h = ctypes.c_void_p()
+        native.check(L.qsb_create(ctypes.byref(opts), ctypes.byref(self._h)))
+        g = ctypes.c_int32()
+        native.check(L.qsb_qubit_guard(self._h, ctypes.byref(g)))
+        self._guard = g.value
+        self.device = device
+
+    def name(self) -> str:
+        return BACKEND_ID
+
+    def qubit_guard(self) -> int:
+        return self._guard
+
+    @staticmethod
+    def _flat(circuit, registry):
+        return circuit if isinstance(circuit, native.FlatCircuit) else native.flatten(circuit, registry)
+
+    def simulate_full_state(self, circuit, registry: Optional[GateRegistry] = None) -> StateVector:
+        flat = self._flat(circuit, registry)
+        N = 1 << flat.n_qubits
+        re = np.empty(N)
+        im = np.empty(N)
+        native.check(native.lib().qsb_simulate_full_state(self._h, flat.ptr, native.dptr(re), native.dptr(im)))
+        return StateVector(flat.n_qubits, re, im)
+
+    def simulate_from_state(self, circuit, registry, psi0_re: np.ndarray, psi0_im: np.ndarray) -> StateVector:
+        flat = self._flat(circuit, registry)
+        N = 1 << flat.n_qubits
+        r0 = np.ascontiguousarray(psi0_re, dtype=np.float64)
+        i0 = np.ascontiguousarray(psi0_im, dtype=np.float64)
+        re = np.empty(N)
+        im = np.empty(N)
+        native.check(native.lib().qsb_simulate_from_state(self._h, flat.ptr, native.dptr(r0), native.dptr(i0),
+                                                          native.dptr(re), native.dptr(im)))
+        return StateVector(flat.n_qubits, re, im)
+
+    def simulate_and_collapse(self, circuit, registry: Optional[GateRegistry], seed: int) -> CollapsedState:
+        flat = self._flat(circuit, registry)
+        idx = ctypes.c_uint64()
+        native.check(native.lib().qsb_simulate_and_collapse(self._h, flat.ptr, ctypes.c_uint64(seed),
+                                                            ctypes.byref(idx)))
+        return CollapsedState(flat.n_qubits, idx.value)
+
+    def build_unitary(self, circuit, registry: Optional[GateRegistry] = None) -> Tuple[np.ndarray, np.ndarray]:
+        flat = self._flat(circuit, registry)
+        N = 1 << flat.n_qubits
+        re = np.empty((N, N))
+        im = np.empty((N, N))
+        native.check(native.lib().qsb_build_unitary(self._h, flat.ptr, native.dptr(re), native.dptr(im)))
+        return re, im
+
+    def layer_operator(self, circuit, registry, step: int, layer: int) -> Tuple[np.ndarray, np.ndarray]:
+        flat = self._flat(circuit, registry)
+        N = 1 << flat.n_qubits
+        re = np.empty((N, N))
+        im = np.empty((N, N))
+        native.check(native.lib().qsb_layer_operator(self._h, flat.ptr, step, layer, native.dptr(re),
+                                                     native.dptr(im)))
+        return re, im
+
+    def probabilities(self, re: np.ndarray, im: np.ndarray) -> Tuple[np.ndarray, float]:
+        re = np.ascontiguousarray(re, dtype=np.float64)
+        im = np.ascontiguousarray(im, dtype=np.float64)
+        p = np.empty(len(re))
+        norm = ctypes.c_double()
+        native.check(native.lib().qsb_probabilities(self._h, native.dptr(re), native.dptr(im), len(re),
+                                                    native.dptr(p), ctypes.byref(norm)))
+        return p, norm.value
+
+    def plan(self, circuit, registry=None, row_begin: int = 0, row_count: Optional[int] = None) -> Plan:
+        flat = self._flat(circuit, registry)
+        if row_count is None:
+            row_count = (1 << flat.n_qubits) - row_begin
+        return Plan(self, flat, row_begin, row_count)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            native.lib().qsb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _CudaArray:
+    """Minimal __cuda_array_interface__ holder for a raw device pointer."""
+
+    def __init__(self, ptr: int, shape, typestr: str = "<f8"):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def torch_view(ptr: int, shape, device: Optional[int] = None):
+    """Zero-copy torch float64 view of device memory owned by a plan (valid until
+    the plan is destroyed or re-executed)."""
+    import torch
+
+    return torch.as_tensor(_CudaArray(ptr, shape), device=f"cuda:{device or 0}")
+
+
+def step_layer_count(circuit, registry, step: int) -> int:
+    flat = circuit if isinstance(circuit, native.FlatCircuit) else native.flatten(circuit, registry)
+    n = ctypes.c_int32()
+    native.check(native.lib().qsb_step_layer_count(flat.ptr, step, ctypes.byref(n)))
+    return n.value
+
+
+# ---- backend registry (simulator.cpp:32-82) ----
+
+SimulatorFactory = Callable[[SimulatorOptions], Simulator]
+_lock = threading.Lock()
+_factories: Dict[str, SimulatorFactory] = {
+    BACKEND_ID: lambda o: B200UnitarySimulator(qubit_guard=o.qubit_guard),
+}
+
+
+def make_simulator(backend_id: str, options: Optional[SimulatorOptions] = None) -> Simulator:
+    with _lock:
+        f = _factories.get(backend_id)
+    if f is None:
+        raise LookupError_(f"unknown backend '{backend_id}'")
+    return f(options or SimulatorOptions())
+
+
+def register_backend(backend_id: str, factory: SimulatorFactory) -> None:
+    with _lock:
+        _factories[backend_id] = factory
+
+
+def backend_names() -> List[str]:
+    with _lock:
+        return sorted(_factories)
+
+
+def memory_estimate(n_qubits: int, kind: int = 0) -> int:
+    return int(native.lib().qsb_memory_estimate(n_qubits, kind))
+
+
+def engine_memory_estimate(n_qubits: int, kind: int = 0) -> int:
+    return int(native.lib().qsb_engine_memory_estimate(n_qubits, kind))

@@ -1,0 +1,185 @@
+"""GPU parity: the B200 path (libqsb.so, through the C ABI) against the golden
+vectors recorded from the reference and against the C oracle.
+
+Bars (BASELINE.json north_star):
+  * operator entries / permutation indexing: bit-exact (==, as the reference's
+    ComplexMatrix::operator==, so -0.0 == +0.0);
+  * amplitudes and U: ||delta||_F / ||ref||_F <= 1e-10.
+"""
+import numpy as np
+import pytest
+
+from conftest import bit_equal, rel_frob
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def _named_cases(golden):
+    return [c for c in golden.cases if not c.split("_")[0] in ("cross", "fsv", "norm", "steps", "par", "det", "comp")]
+
+
+def test_named_circuits_state(golden, sim):
+    worst = 0.0
+    for case in _named_cases(golden):
+        flat = golden.flat(case)
+        out = sim.simulate_full_state(flat)
+        re, im = golden.psi(case)
+        err = rel_frob(out.re, out.im, re, im)
+        worst = max(worst, err)
+        assert err <= TOL, (case, err)
+    print(f"named circuits: worst relative L2 error {worst:.3e}")
+
+
+def test_named_circuits_unitary(golden, sim):
+    for case in _named_cases(golden):
+        u = golden.unitary(case)
+        if u is None:
+            continue
+        ur, ui = sim.build_unitary(golden.flat(case))
+        assert rel_frob(ur, ui, u[0], u[1]) <= TOL, case
+
+
+@pytest.mark.parametrize("suite", ["cross", "fsv", "norm", "steps", "par", "det", "comp"])
+def test_random_suites(golden, sim, suite):
+    worst = 0.0
+    for case in golden.suites[suite]:
+        flat = golden.flat(case)
+        out = sim.simulate_full_state(flat)
+        re, im = golden.psi(case)
+        err = rel_frob(out.re, out.im, re, im)
+        worst = max(worst, err)
+        assert err <= TOL, (case, err)
+        u = golden.unitary(case)
+        if u is not None:
+            ur, ui = sim.build_unitary(flat)
+            assert rel_frob(ur, ui, u[0], u[1]) <= TOL, case
+    print(f"{suite}: worst {worst:.3e}")
+
+
+def test_layer_operators_bit_exact(golden, sim, orc):
+    """K1 expansion == kronecker_fold(fill_layer(layer)) entrywise, and for
+    single-layer steps == the reference's step_unitary."""
+    from paper_2305_14398_b200.simulator import step_layer_count
+
+    checked = 0
+    for case in golden.cases:
+        steps = golden.steps(case)
+        if not steps:
+            continue
+        flat = golden.flat(case)
+        for s, (sr, si) in enumerate(steps):
+            nl = step_layer_count(flat, None, s)
+            for layer in range(nl):
+                gr, gi = sim.layer_operator(flat, None, s, layer)
+                orr, ori = orc.layer_operator(flat, s, layer)
+                assert bit_equal(gr, orr) and bit_equal(gi, ori), (case, s, layer)
+                checked += 1
+            if nl == 1:
+                gr, gi = sim.layer_operator(flat, None, s, 0)
+                assert bit_equal(gr, sr) and bit_equal(gi, si), (case, s)
+    assert checked > 100
+
+
+def test_initial_state(golden, sim):
+    """test_unitary_backend.cpp:143-153: U applied to random states."""
+    for case in golden.suites["comp"]:
+        flat = golden.flat(case)
+        r0, i0 = golden[f"{case}:state_re"], golden[f"{case}:state_im"]
+        out = sim.simulate_from_state(flat, None, r0, i0)
+        ur, ui = golden.unitary(case)
+        u = ur + 1j * ui
+        want = u @ (r0 + 1j * i0)
+        assert rel_frob(out.re, out.im, want.real, want.imag) <= TOL
+        assert abs(np.sum(out.re ** 2 + out.im ** 2) - 1.0) < 1e-9
+
+
+def test_probabilities_and_collapse(golden, sim):
+    for key in ["comp_0", "comp_1"]:
+        re, im = golden[f"{key}:state_re"], golden[f"{key}:state_im"]
+        p, norm = sim.probabilities(re, im)
+        assert bit_equal(p, golden[f"{key}:probs"])  # p_i bit-exact (state.cpp:58-65)
+        assert abs(norm - float(golden[f"{key}:norm"])) < 1e-14
+    flat = golden.flat("bell")
+    for seed, want in enumerate(golden["collapse_bell"]):
+        assert sim.simulate_and_collapse(flat, None, seed).basis_index == int(want)
+    flat = golden.flat("qft5")
+    for seed, want in enumerate(golden["collapse_qft5"][:50]):
+        assert sim.simulate_and_collapse(flat, None, seed).basis_index == int(want)
+
+
+def test_errors_match_reference(sim):
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200.simulator import B200UnitarySimulator
+
+    bad = q.Circuit(2)
+    bad.reset(0).h(0)
+    with pytest.raises(q.ValidationError):
+        sim.simulate_full_state(bad)
+    ok = q.Circuit(2)
+    ok.h(0).reset(0)
+    assert sim.simulate_full_state(ok).dimension() == 4
+    small = B200UnitarySimulator(qubit_guard=3)
+    with pytest.raises(q.ResourceError) as e:
+        small.simulate_full_state(q.Circuit(4))
+    assert "estimated memory 2176 bytes" in str(e.value)  # memory_estimate(4) (unitary_backend.cpp:156-166)
+    assert small.simulate_full_state(q.Circuit(3)).dimension() == 8
+    small.close()
+
+
+def test_hbm_guard(sim):
+    assert sim.qubit_guard() >= 15  # 2 x 16 x 4^15 B = 34 GB fits any B200
+
+
+@pytest.mark.parametrize("name,n", [("qft", 10), ("entangle", 10), ("deutsch-jozsa", 10), ("qft", 11)])
+def test_large_against_oracle_fsv(sim, orc, name, n):
+    """Beyond the dense oracle: psi vs the reference's fsv restatement, and
+    sampled columns of U vs fsv(e_c)."""
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+
+    c, reg = q.make_named_circuit(name, n)
+    flat = native.flatten(c, reg)
+    out = sim.simulate_full_state(flat)
+    re, im = orc.fsv(flat)
+    assert rel_frob(out.re, out.im, re, im) <= TOL
+    ur, ui = sim.build_unitary(flat)
+    rng = np.random.default_rng(7)
+    for col in rng.choice(1 << n, size=4, replace=False):
+        cr, ci = orc.unitary_column(flat, int(col))
+        assert rel_frob(ur[:, col], ui[:, col], cr, ci) <= TOL
+
+
+def test_row_shards_match_full(sim):
+    """Row-block sharding (the multi-GPU decomposition) on one GPU: G virtual
+    shards computed separately reproduce the full U and psi exactly."""
+    import torch
+
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+
+    c, reg = q.make_named_circuit("qft", 9)
+    flat = native.flatten(c, reg)
+    full_re, full_im = sim.build_unitary(flat)
+    N = 1 << 9
+    for G in (2, 4, 8):
+        rows = N // G
+        for r in range(G):
+            plan = sim.plan(flat, None, r * rows, rows)
+            plan.execute()
+            torch.cuda.synchronize()
+            re_p, im_p = plan.unitary_device()
+            got = np.empty((rows, N))
+            gim = np.empty((rows, N))
+            native_copy(re_p, got)
+            native_copy(im_p, gim)
+            assert bit_equal(got, full_re[r * rows:(r + 1) * rows])
+            assert bit_equal(gim, full_im[r * rows:(r + 1) * rows])
+            plan.close()
+
+
+def native_copy(dev_ptr, host):
+    from paper_2305_14398_b200.simulator import torch_view
+
+    host[...] = torch_view(dev_ptr, host.shape).cpu().numpy()
