@@ -1,0 +1,418 @@
+"""Benchmark: unitary-simulation time per circuit on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload qft-12] [--impl ours|reference]
+
+One step = one full circuit through the hot path (Algorithm 1: K1 expansion of
+the first operator, one K2 DMMA GEMM per further layer, K3 application of
+psi0). ``value`` is milliseconds per circuit with the circuit already resident
+on the device (CUDA events on the launching stream, max over ranks); ``e2e`` is
+the same circuit through the public C ABI with host buffers (descriptor H2D and
+psi D2H inside the timed region). For N > 1 (torchrun, one process per GPU) the
+unitary is sharded by row blocks; each rank computes its rows with no
+communication and psi is all-gathered with NCCL.
+
+``--impl reference`` times the reference's own CPU implementation
+(oracle/_ref: the unmodified reference library compiled from its sources) on
+this host's cores over a bounded sample of the same workload and extrapolates
+the per-circuit time (the sample is stated in the JSON line).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "unitary-sim time (ms) per circuit vs qubits; FP64 TC TFLOPS %peak @1/2/4/8 GPU"
+# FP64 tensor (DMMA) peak measured on this pool's B200: register-only
+# mma.sync.m8n8k4.f64 loop over 148 SMs (tools/microbench/fp64_peak.cu,
+# profiles/r01_fp64_peak.txt). MEASURED_PEAKS.json carries no FP64 figure.
+FP64_DMMA_PEAK_TFLOPS = 37.1
+WORKLOADS = {
+    # name: (circuit, qubits) — BASELINE.json configs
+    "qft-4": ("qft", 4),
+    "entangle-10": ("entangle", 10),
+    "dj-11": ("deutsch-jozsa", 11),
+    "qft-12": ("qft", 12),
+    "qft-14": ("qft", 14),
+}
+DEFAULT_WORKLOAD = "qft-12"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--gemm-mode", default="auto", choices=["auto", "4m", "3m"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# --------------------------------------------------------------- CPU baseline
+
+def cpu_sample(workload: str, repeats: int = 1):
+    """Time the reference CPU path on a bounded sample and extrapolate to one
+    circuit. Components:
+      T = sum_steps [fold(step) + GEMM_par(N)] + extra_layers * GEMM_ser(N)
+    where GEMM_* come from the reference's own matmul on a row slab of the
+    accumulate GEMM (linalg.cpp:72-87 accepts rectangular shapes), fold from
+    step_unitary of a single-layer step (unitary_backend.cpp:141-154)."""
+    import oracle
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+
+    name, n = WORKLOADS[workload]
+    N = 1 << n
+    cores = os.cpu_count() or 1
+    c, reg = q.make_named_circuit(name, n)
+    flat = native.flatten(c, reg)
+    orc = oracle.Oracle()
+    n_steps = len(flat.step_offsets) - 1
+    layers = [orc.step_layers(flat, s)[0] for s in range(n_steps)]
+    extra = sum(l - 1 for l in layers)
+    single = next(s for s in range(n_steps) if layers[s] == 1)
+    if oracle.reference_available():
+        ref = oracle.Reference()
+        kind = "reference"
+        prog = ref.named(name, n)
+        if n <= 8:
+            # small sizes: time the whole reference simulate_full_state directly
+            t_full = []
+            for _ in range(max(1, repeats)):
+                ref.L.refsh_set_worker_count(0)
+                t_full.append(ref.L.refsh_time_simulate(prog.h, b"unitary-parallel", n))
+            t_par = min(t_full)
+            ref.L.refsh_set_worker_count(1)
+            t_ser = min(ref.L.refsh_time_simulate(prog.h, b"unitary", n) for _ in range(max(1, repeats)))
+            ref.L.refsh_set_worker_count(0)
+            best = min(t_par, t_ser)
+            return {"value": best * 1e3, "unit": "ms", "cores": cores, "kind": kind,
+                    "sample": f"full reference UnitarySimulator::simulate_full_state of {workload} "
+                              f"(best of unitary / unitary-parallel, {repeats} run(s))"}
+        rows_par = max(cores * 4, 64)
+        rows_ser = 8
+        t_fold, t_par, t_ser = [], [], []
+        for _ in range(max(1, repeats)):
+            ref.L.refsh_set_worker_count(0)  # QSIM_THREADS unset: all host cores
+            t_fold.append(ref.L.refsh_time_step_unitary(prog.h, single))
+            t_par.append(ref.L.refsh_time_matmul(rows_par, N, 1))
+            t_ser.append(ref.L.refsh_time_matmul(rows_ser, N, 0))
+        fold = min(t_fold)
+        gemm_par = min(t_par) * N / rows_par
+        gemm_ser = min(t_ser) * N / rows_ser
+        sample = (f"reference step_unitary(single-layer step) + matmul({rows_par}x{N} . {N}x{N}, Parallel, "
+                  f"{cores} threads) + matmul({rows_ser}x{N} . {N}x{N}, Serial); extrapolated to {n_steps} steps "
+                  f"+ {extra} serial extra-layer GEMMs")
+    else:
+        kind = "port"
+        orc.set_threads(cores)
+        import numpy as np
+
+        rows_par = max(cores * 4, 64)
+        rows_ser = 8
+        a = np.random.default_rng(0).uniform(-1, 1, (rows_par, N)) * (1 + 0.5j)
+        b = np.eye(N, dtype=complex)
+        t0 = time.perf_counter()
+        orc.layer_operator(flat, single, 0)
+        fold = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        orc.matmul(a, b)
+        gemm_par = (time.perf_counter() - t0) * N / rows_par
+        orc.set_threads(1)
+        t0 = time.perf_counter()
+        orc.matmul(a[:rows_ser], b)
+        gemm_ser = (time.perf_counter() - t0) * N / rows_ser
+        sample = "C oracle port (oracle/_ref absent): same components, extrapolated"
+    total = n_steps * (fold + gemm_par) + extra * (fold + gemm_ser)
+    return {"value": total * 1e3, "unit": "ms", "cores": cores, "kind": kind, "sample": sample,
+            "components_s": {"fold": fold, "gemm_parallel": gemm_par, "gemm_serial": gemm_ser,
+                             "steps": n_steps, "extra_layers": extra}}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    name, n = WORKLOADS[args.workload]
+    for _ in range(args.warmup):
+        cpu_sample(args.workload)
+    vals = []
+    t0 = time.perf_counter()
+    last = None
+    for _ in range(args.steps):
+        last = cpu_sample(args.workload)
+        vals.append(last["value"])
+    wall = time.perf_counter() - t0
+    value = statistics.mean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "ms", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "deterministic circuit (synthetic)",
+        "config": {"workload": args.workload, "circuit": name, "qubits": n, "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": "ms", "cores": last["cores"], "kind": last["kind"],
+                         "sample": last["sample"]},
+        "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_bench_{device}.csv")
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9 and parts[1].isdigit():
+                    rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [int(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][2]), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3] not in ("", "[N/A]"))}
+
+
+# --------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+    from paper_2305_14398_b200.sharding import gather_state, row_shard
+    from paper_2305_14398_b200.simulator import B200UnitarySimulator
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    name, n = WORKLOADS[args.workload]
+    N = 1 << n
+    mode = {"auto": native.GEMM_AUTO, "4m": native.GEMM_4M, "3m": native.GEMM_3M}[args.gemm_mode]
+    sim = B200UnitarySimulator(device=local, gemm_mode=mode)
+    c, reg = q.make_named_circuit(name, n)
+    flat = native.flatten(c, reg)
+    begin, count = row_shard(N, world, rank)
+    # A dedicated stream: every launch of the plan, the all-gather and the
+    # timing events share it (the legacy default stream has handle 0).
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    s_ptr = stream.cuda_stream
+    plan = sim.plan(flat, None, begin, count) if count > 0 else None
+    psi_re = torch.empty(N, dtype=torch.float64, device="cuda")
+    psi_im = torch.empty(N, dtype=torch.float64, device="cuda")
+    flush = None
+    u_bytes = 16 * (count or 1) * N
+    if u_bytes < 2 * L2_BYTES:
+        flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    def step():
+        if plan is not None:
+            plan.execute(s_ptr)
+        gather_state(plan, psi_re, psi_im, begin, count, world, s_ptr)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    timed = plan is not None and plan.info.n_gemms > 0 and N > 32
+    if timed:
+        plan.set_timing(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    gemm_ms = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            if flush is not None:
+                flush.zero_()
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+            if timed:
+                _, g_ms, _ = plan.last_timing()
+                gemm_ms.append(g_ms)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    per_step = [a.elapsed_time(b) for a, b in ev]
+    ms = sum(per_step) / len(per_step)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    # ---- roofline of the dominant kernel (K2) ----
+    info = plan.info if plan is not None else None
+    gemm_flops_step = info.gemm_flops if info else 0.0
+    n_gemms = info.n_gemms if info else 0
+    mean_gemm_ms = (sum(gemm_ms) / len(gemm_ms) / n_gemms) if (gemm_ms and n_gemms) else None
+    per_launch_flops = gemm_flops_step / n_gemms if n_gemms else 0.0
+    achieved = per_launch_flops / (mean_gemm_ms * 1e-3) / 1e12 if mean_gemm_ms else None
+    traffic = None
+    prof_json = os.path.join(ROOT, "profiles", "k2_traffic.json")
+    if os.path.exists(prof_json):
+        with open(prof_json) as f:
+            tr = json.load(f).get(args.workload)
+            if tr:
+                traffic = tr.get("dram_bytes_per_launch")
+    chain_tflops = gemm_flops_step / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+    tot = torch.tensor([gemm_flops_step], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tot)
+    job_tflops = float(tot.item()) / (ms_max * 1e-3) / 1e12
+
+    # ---- e2e through the public API with host buffers ----
+    e2e_ms, h2d, d2h = e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr)
+    if plan is not None:
+        plan.close()
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": ms_max, "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "deterministic circuit from make_named_circuit (synthetic, no dataset)",
+            "config": {"workload": args.workload, "circuit": name, "qubits": n, "dimension": N,
+                       "parallelism": f"row-block x{world}" if world > 1 else "1 GPU",
+                       "gemms_per_circuit": n_gemms, "layers": info.n_layers if info else None,
+                       "identity_layers_skipped": info.n_identity_layers if info else None,
+                       "gemm_mode": args.gemm_mode,
+                       "l2": ("inputs larger than L2" if flush is None else "L2 flushed between steps")},
+            "tflops": job_tflops,
+            "fp64_peak_frac": job_tflops / (FP64_DMMA_PEAK_TFLOPS * world),
+            "roofline": {"bound": "tensor", "kernel": "zgemm_gen_kernel (K2)",
+                         "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": (achieved / FP64_DMMA_PEAK_TFLOPS) if achieved else None,
+                         "traffic": traffic,
+                         "algorithmic_flops_per_launch": per_launch_flops,
+                         "mean_launch_ms": mean_gemm_ms,
+                         "peak_source": "measured FP64 DMMA peak (tools/microbench/fp64_peak.cu, "
+                                        "profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no FP64 entry"},
+            "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "qsb_simulate_full_state (C ABI)" if world == 1 else
+                           "qsb_plan_create/execute + NCCL all-gather + D2H"},
+            "gpu_launches": (info.n_launches if info else 0) * args.steps,
+            "clocks": clocks,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_sample(args.workload)
+        print(json.dumps(line), flush=True)
+    sim.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr):
+    """The same circuit through the public API with host buffers: descriptor
+    H2D and psi D2H inside the timed region, every step."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_14398_b200 import native
+    from paper_2305_14398_b200.sharding import gather_state
+
+    h2d = flat.nbytes()
+    d2h = 16 * N
+    steps = max(1, min(args.steps, 3))
+    if world == 1:
+        re = np.empty(N)
+        im = np.empty(N)
+        L = native.lib()
+        native.check(L.qsb_simulate_full_state(sim._h, flat.ptr, native.dptr(re), native.dptr(im)))
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            native.check(L.qsb_simulate_full_state(sim._h, flat.ptr, native.dptr(re), native.dptr(im)))
+            times.append((time.perf_counter() - t0) * 1e3)
+        return sum(times) / len(times), h2d, d2h
+    psi_re = torch.empty(N, dtype=torch.float64, device="cuda")
+    psi_im = torch.empty(N, dtype=torch.float64, device="cuda")
+    host = torch.empty(2, N, dtype=torch.float64, pin_memory=True)
+    times = []
+    for _ in range(steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        plan = sim.plan(flat, None, begin, count) if count > 0 else None
+        if plan is not None:
+            plan.execute(s_ptr)
+        gather_state(plan, psi_re, psi_im, begin, count, world, s_ptr)
+        host[0].copy_(psi_re, non_blocking=True)
+        host[1].copy_(psi_im, non_blocking=True)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) * 1e3
+        if plan is not None:
+            plan.close()
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        times.append(float(t.item()))
+    return sum(times) / len(times), h2d, d2h
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,50 @@
+// b200_unitary_simulator.hpp — the reference-side binding a qsim maintainer adds
+// to make the B200 path a drop-in backend.
+//
+// Implements the reference's plugin interface qsim::Simulator
+// (proj/core/include/qsim/simulator.hpp:32-51) on top of the C ABI in
+// include/qsb.h, and registers it under "unitary-b200" with
+// qsim::register_backend (simulator.cpp:70-73) so run_bench, the CLI and any
+// caller of make_simulator can select it. Circuit, GateRegistry, gate_matrix,
+// StateVector and the error types are the reference's own, unchanged.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include "qsb.h"
+#include "qsim/simulator.hpp"
+
+namespace qsim {
+
+class B200UnitarySimulator final : public Simulator {
+public:
+    /// qubit_guard 0 = derived from HBM capacity (n <= 16 on one B200).
+    explicit B200UnitarySimulator(std::size_t qubit_guard = 0, int device = 0);
+    ~B200UnitarySimulator() override;
+    B200UnitarySimulator(const B200UnitarySimulator&) = delete;
+    B200UnitarySimulator& operator=(const B200UnitarySimulator&) = delete;
+
+    std::string name() const override { return "unitary-b200"; }
+    std::size_t qubit_guard() const override { return guard_; }
+
+    /// Algorithm 1 on the GPU: same contract as UnitarySimulator
+    /// (unitary_backend.cpp:194-215), results within 1e-10 relative.
+    StateVector simulate_full_state(const Circuit& circuit, const GateRegistry& registry) const override;
+
+    /// Inverse-CDF collapse over the GPU-computed probabilities (state.cpp:81-98).
+    CollapsedState simulate_and_collapse(const Circuit& circuit, const GateRegistry& registry,
+                                         std::uint64_t seed) const override;
+
+    /// The accumulated unitary (test::circuit_unitary, test_util.hpp:135-142).
+    ComplexMatrix circuit_unitary(const Circuit& circuit, const GateRegistry& registry) const;
+
+private:
+    qsb_handle* handle_ = nullptr;
+    std::size_t guard_ = 0;
+};
+
+/// register_backend("unitary-b200", ...) honouring SimulatorOptions::qubit_guard.
+void register_b200_backend();
+
+}  // namespace qsim

@@ -29,7 +29,7 @@ def build(reference: bool = True) -> None:
     """Compile the oracle (always) and, when /root/reference exists, oracle/_ref."""
     targets = ["oracle"]
     if reference and os.path.isdir("/root/reference/proj"):
-        targets.append("ref")
+        targets += ["ref", "dropin"]
     subprocess.run(["make", "-s", "-C", HERE, "-j8", *targets], check=True)
 
 

@@ -62,7 +62,7 @@ int launch_probabilities(const double* psi, int64_t dim, double* p, double* part
                          double* norm, void* stream);
 
 // Tile shapes of the K2 GEMM (rows x cols of the output tile).
-enum GemmTile : int { kTile128x64 = 0, kTile64x64 = 1, kTile32x32 = 2 };
+enum GemmTile : int { kTile128x64 = 0, kTile64x64 = 1, kTile32x32 = 2, kTileWs4M = 3, kTileWs3M = 4 };
 int configure_kernels();
 int gemm_tile_rows(int tile);
 int gemm_tile_cols(int tile);

@@ -340,8 +340,267 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN>::THREADS, 1)
     }
 }
 
-int gemm_tile_rows(int tile) { return tile == kTile128x64 ? 128 : tile == kTile64x64 ? 64 : 32; }
-int gemm_tile_cols(int tile) { return tile == kTile32x32 ? 32 : 64; }
+// ----------------------------------------------------------------------------
+// K2 v2: warp-specialised generated-operand complex GEMM (4M or 3M on DMMA)
+// ----------------------------------------------------------------------------
+//
+// 12 warps: warpgroups 0-1 are consumers (8 warps of DMMA), warpgroup 2 is the
+// producer (its first lane issues the TMA of the A tile, all 128 threads
+// generate the B tile of the same stage). Stages are handed over with
+// mbarriers (full: 1 TMA arrival + transaction bytes + 4 producer-warp
+// arrivals; empty: 8 consumer-warp arrivals), so operator generation overlaps
+// the DMMA work instead of stalling it at a block barrier. setmaxnreg moves
+// registers from the producer warpgroup to the consumers.
+//
+// 4M: Cr += Ar*Br + Ai*(-Bi), Ci += Ar*Bi + Ai*Br (warp tile 32x32, CTA 128x64).
+// 3M: T1 += Ar*Br, T2 += Ai*Bi, T3 += (Ar+Ai)*(Br+Bi); Cr = T1 - T2,
+//     Ci = T3 - T1 - T2 (warp tile 32x16, CTA 64x64; the producer writes the
+//     Br+Bi plane, consumers form Ar+Ai in registers).
+
+template <bool THREE_M>
+struct WsCfg {
+    static constexpr int BK = 16;
+    static constexpr int CONSUMER_WARPS = 8;
+    static constexpr int PRODUCER_WARPS = 4;
+    static constexpr int THREADS = 32 * (CONSUMER_WARPS + PRODUCER_WARPS);
+    static constexpr int WT_N = THREE_M ? 16 : 32;   // warp tile columns
+    static constexpr int NT = WT_N / 8;              // m8n8 tiles per warp row
+    static constexpr int CWM = THREE_M ? 2 : 4;      // consumer warps along M
+    static constexpr int CWN = CONSUMER_WARPS / CWM; // consumer warps along N
+    static constexpr int BM = CWM * 32;
+    static constexpr int BN = CWN * WT_N;
+    static constexpr int B_PLANES = THREE_M ? 3 : 2;
+    static constexpr int A_BYTES = 2 * BM * BK * 8;
+    static constexpr int B_BYTES = B_PLANES * BN * BK * 8;
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int STAGES = (200 * 1024) / STAGE;
+    static constexpr int SMEM = 1024 + STAGES * STAGE + 2 * STAGES * 8;
+    static constexpr int PAIRS = 8 * BN / (32 * PRODUCER_WARPS);
+    static constexpr int CONSUMER_REGS = 224;
+    static constexpr int PRODUCER_REGS = 56;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+template <bool THREE_M>
+__global__ void __launch_bounds__(WsCfg<THREE_M>::THREADS, 1)
+    zgemm_ws_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ LayerDesc layer,
+                    double* __restrict__ out, int M, int N) {
+    using C = WsCfg<THREE_M>;
+    constexpr int BM = C::BM, BN = C::BN;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sBase = smem_u32(smem);
+    const uint32_t sFull = sBase + C::STAGES * C::STAGE;
+    const uint32_t sEmpty = sFull + 8 * C::STAGES;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    const int m0 = blockIdx.y * BM;
+    const int n0 = blockIdx.x * BN;
+    const int KT = N / C::BK;
+
+    if (tid == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(sFull + 8 * s, 1 + C::PRODUCER_WARPS);
+            mbar_init(sEmpty + 8 * s, C::CONSUMER_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp >= C::CONSUMER_WARPS) {
+        // ------------------------------ producer warpgroup
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::PRODUCER_REGS));
+        const int ptid = tid - 32 * C::CONSUMER_WARPS;
+        for (int kt = 0; kt < KT; ++kt) {
+            const int s = kt % C::STAGES;
+            if (kt >= C::STAGES) mbar_wait(sEmpty + 8 * s, ((kt / C::STAGES) & 1) ^ 1);
+            const uint32_t stage = sBase + s * C::STAGE;
+            if (ptid == 0) {
+                mbar_expect_tx(sFull + 8 * s, C::A_BYTES);
+                tma_load_3d(stage, &tmA, sFull + 8 * s, kt * C::BK, m0, 0);
+            }
+            const uint32_t bBase = stage + C::A_BYTES;
+#pragma unroll
+            for (int q = 0; q < C::PAIRS; ++q) {
+                const int idx = ptid + q * 32 * C::PRODUCER_WARPS;
+                const int n = idx % BN;
+                const int p = idx / BN;
+                const uint32_t r0 = static_cast<uint32_t>(kt * C::BK + 2 * p);
+                const uint32_t col = static_cast<uint32_t>(n0 + n);
+                double a_r, a_i, b_r, b_i;
+                layer_entry(layer, r0, col, a_r, a_i);
+                layer_entry(layer, r0 + 1, col, b_r, b_i);
+                const uint32_t off = n * 128 + ((p ^ (n & 7)) << 4);
+                sts128(bBase + off, a_r, b_r);
+                sts128(bBase + BN * 128 + off, a_i, b_i);
+                if (THREE_M) sts128(bBase + 2 * BN * 128 + off, __dadd_rn(a_r, a_i), __dadd_rn(b_r, b_i));
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(sFull + 8 * s);
+        }
+        return;
+    }
+
+    // ------------------------------ consumer warpgroups
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::CONSUMER_REGS));
+    const int g = lane >> 2;
+    const int t = lane & 3;
+    const int wm = warp / C::CWN;
+    const int wn = warp % C::CWN;
+    constexpr int NT = C::NT;
+    constexpr int NACC = THREE_M ? 3 : 2;
+    double acc[NACC][4][NT][2];
+#pragma unroll
+    for (int a = 0; a < NACC; ++a)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) acc[a][i][j][0] = acc[a][i][j][1] = 0.0;
+
+    for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % C::STAGES;
+        mbar_wait(sFull + 8 * s, (kt / C::STAGES) & 1);
+        const uint32_t aRe = sBase + s * C::STAGE;
+        const uint32_t aIm = aRe + BM * 128;
+        const uint32_t bRe = aRe + C::A_BYTES;
+        const uint32_t bIm = bRe + BN * 128;
+        const uint32_t bSm = bIm + BN * 128;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t choff = static_cast<uint32_t>(((2 * t + h) ^ g) << 4);
+            double2 ar[4], ai[4], br[NT], bi[NT], bs[NT];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t line = static_cast<uint32_t>(wm * 32 + i * 8 + g) * 128 + choff;
+                ar[i] = lds128(aRe + line);
+                ai[i] = lds128(aIm + line);
+            }
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                const uint32_t line = static_cast<uint32_t>(wn * C::WT_N + j * 8 + g) * 128 + choff;
+                br[j] = lds128(bRe + line);
+                bi[j] = lds128(bIm + line);
+                if (THREE_M) bs[j] = lds128(bSm + line);
+            }
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                double xr[4], xi[4], yr[NT], yi[NT];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    xr[i] = e ? ar[i].y : ar[i].x;
+                    xi[i] = e ? ai[i].y : ai[i].x;
+                }
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    yr[j] = e ? br[j].y : br[j].x;
+                    yi[j] = e ? bi[j].y : bi[j].x;
+                }
+                if (THREE_M) {
+                    double xs[4], ys[NT];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) xs[i] = __dadd_rn(xr[i], xi[i]);
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) ys[j] = e ? bs[j].y : bs[j].x;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < NT; ++j) dmma(acc[0][i][j], xr[i], yr[j]);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < NT; ++j) dmma(acc[1][i][j], xi[i], yi[j]);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < NT; ++j) dmma(acc[2][i][j], xs[i], ys[j]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < NT; ++j) dmma(acc[0][i][j], xr[i], yr[j]);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < NT; ++j) dmma(acc[1][i][j], xr[i], yi[j]);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < NT; ++j) dmma(acc[0][i][j], xi[i], neg(yi[j]));
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < NT; ++j) dmma(acc[1][i][j], xi[i], yr[j]);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(sEmpty + 8 * s);
+    }
+
+    const size_t plane = static_cast<size_t>(M) * N;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = m0 + wm * 32 + i * 8 + g;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            const int col = n0 + wn * C::WT_N + j * 8 + 2 * t;
+            const size_t o = static_cast<size_t>(row) * N + col;
+            double r0, r1, i0, i1;
+            if (THREE_M) {
+                r0 = acc[0][i][j][0] - acc[1][i][j][0];
+                r1 = acc[0][i][j][1] - acc[1][i][j][1];
+                i0 = acc[2][i][j][0] - acc[0][i][j][0] - acc[1][i][j][0];
+                i1 = acc[2][i][j][1] - acc[0][i][j][1] - acc[1][i][j][1];
+            } else {
+                r0 = acc[0][i][j][0];
+                r1 = acc[0][i][j][1];
+                i0 = acc[1][i][j][0];
+                i1 = acc[1][i][j][1];
+            }
+            *reinterpret_cast<double2*>(out + o) = make_double2(r0, r1);
+            *reinterpret_cast<double2*>(out + plane + o) = make_double2(i0, i1);
+        }
+    }
+}
+
+template <bool THREE_M>
+static int configure_ws_t() {
+    return static_cast<int>(cudaFuncSetAttribute(zgemm_ws_kernel<THREE_M>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, WsCfg<THREE_M>::SMEM));
+}
+
+template <bool THREE_M>
+static int launch_ws_t(const GemmArgs& a, void* stream) {
+    using C = WsCfg<THREE_M>;
+    dim3 grid(a.N / C::BN, a.M / C::BM);
+    zgemm_ws_kernel<THREE_M><<<grid, C::THREADS, C::SMEM, static_cast<cudaStream_t>(stream)>>>(
+        *static_cast<const CUtensorMap*>(a.tmap), *a.layer, a.out, a.M, a.N);
+    return static_cast<int>(cudaGetLastError());
+}
+
+int gemm_tile_rows(int tile) {
+    switch (tile) {
+    case kTile128x64: return 128;
+    case kTile64x64: return 64;
+    case kTileWs4M: return WsCfg<false>::BM;
+    case kTileWs3M: return WsCfg<true>::BM;
+    default: return 32;
+    }
+}
+int gemm_tile_cols(int tile) {
+    switch (tile) {
+    case kTile32x32: return 32;
+    case kTileWs4M: return WsCfg<false>::BN;
+    case kTileWs3M: return WsCfg<true>::BN;
+    default: return 64;
+    }
+}
 
 template <int BM, int BN>
 static int configure_zgemm_t() {
@@ -361,6 +620,8 @@ static int launch_zgemm_t(const GemmArgs& a, void* stream) {
 
 int launch_zgemm(const GemmArgs& a, int tile, int /*gemm_mode*/, void* stream) {
     switch (tile) {
+    case kTileWs4M: return launch_ws_t<false>(a, stream);
+    case kTileWs3M: return launch_ws_t<true>(a, stream);
     case kTile128x64: return launch_zgemm_t<128, 64>(a, stream);
     case kTile64x64: return launch_zgemm_t<64, 64>(a, stream);
     default: return launch_zgemm_t<32, 32>(a, stream);
@@ -541,6 +802,8 @@ int configure_kernels() {
     if ((e = configure_zgemm_t<128, 64>())) return e;
     if ((e = configure_zgemm_t<64, 64>())) return e;
     if ((e = configure_zgemm_t<32, 32>())) return e;
+    if ((e = configure_ws_t<false>())) return e;
+    if ((e = configure_ws_t<true>())) return e;
     return static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
 }

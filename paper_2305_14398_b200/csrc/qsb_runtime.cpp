@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -415,11 +416,19 @@ void upload_tables(qsb_plan* p, const qsb_circuit* c) {
     for (auto& d : p->cc.app) patch(d);
 }
 
-int pick_tile(int M, int N) {
+int pick_tile(int M, int N, int gemm_mode) {
     const int sms = 148;
-    if (M % 128 == 0 && N % 64 == 0 && (M / 128) * (N / 64) >= 2 * sms) return qsb::kTile128x64;
+    if (const char* force = std::getenv("QSB_TILE")) {  // debugging / tests: force a tile variant
+        const int t = std::atoi(force);
+        if (t >= 0 && t <= qsb::kTileWs3M && M % qsb::gemm_tile_rows(t) == 0 && N % qsb::gemm_tile_cols(t) == 0)
+            return t;
+    }
+    const bool three = gemm_mode != QSB_GEMM_4M;
+    const int ws = three ? qsb::kTileWs3M : qsb::kTileWs4M;
+    const int wr = qsb::gemm_tile_rows(ws), wc = qsb::gemm_tile_cols(ws);
+    if (M % wr == 0 && N % wc == 0 && (M / wr) * (N / wc) >= 2 * sms) return ws;
     if (M % 64 == 0 && N % 64 == 0 && (M / 64) * (N / 64) >= sms) return qsb::kTile64x64;
-    if (M % 128 == 0 && N % 64 == 0 && (M / 128) * (N / 64) >= sms) return qsb::kTile128x64;
+    if (M % wr == 0 && N % wc == 0 && (M / wr) * (N / wc) >= sms) return ws;
     return qsb::kTile32x32;
 }
 
@@ -463,7 +472,7 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, const qsb_circuit* c, int64_t
     if (row_begin + row_count > p->eff_begin + M)
         raise(QSB_ERR_ARGUMENT, "row shard [%lld, +%lld) is not contained in one aligned window of %lld rows",
               static_cast<long long>(row_begin), static_cast<long long>(row_count), static_cast<long long>(M));
-    p->tile = p->small ? qsb::kTile32x32 : pick_tile(p->M, p->N);
+    p->tile = p->small ? qsb::kTile32x32 : pick_tile(p->M, p->N, h->gemm_mode);
 
     DeviceScope ds(h->device);
     if (borrow_cache) {

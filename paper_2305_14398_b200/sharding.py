@@ -1,0 +1,71 @@
+"""Row-block sharding of the accumulated unitary over G GPUs.
+
+Rank r owns rows [r*B, r*B + B) of U = L_last ... L_first. It computes
+V = L_last[rows, :] and then V <- V * L for every further layer, regenerating
+each operator tile locally from the replicated descriptor — no communication
+during the chain. The only exchange is the final all-gather of the psi row
+slices (16 * B bytes per rank) with NCCL (gloo on CPU for the host tests).
+"""
+from __future__ import annotations
+
+from typing import Tuple
+
+
+def block_rows(N: int, world: int) -> int:
+    """Rows per rank: N / world for power-of-two worlds, else the next power of
+    two >= ceil(N / world) (trailing ranks then own no rows)."""
+    if world < 1:
+        raise ValueError("world size must be >= 1")
+    b = -(-N // world)
+    p = 1
+    while p < b:
+        p <<= 1
+    return min(p, N)
+
+
+def row_shard(N: int, world: int, rank: int) -> Tuple[int, int]:
+    """(row_begin, row_count) of `rank`; row_count may be 0."""
+    b = block_rows(N, world)
+    begin = min(rank * b, N)
+    return begin, max(0, min(b, N - begin))
+
+
+def gather_rows(local_re, local_im, N: int, world: int):
+    """All-gather equal row blocks (padded to block_rows) into full psi planes.
+    Works for CUDA tensors over NCCL and CPU tensors over gloo."""
+    import torch
+    import torch.distributed as dist
+
+    b = block_rows(N, world)
+    local = torch.zeros(2, b, dtype=local_re.dtype, device=local_re.device)
+    n = local_re.numel()
+    if n:
+        local[0, :n].copy_(local_re)
+        local[1, :n].copy_(local_im)
+    if dist.get_backend() == "nccl":
+        out = torch.empty(world, 2, b, dtype=local.dtype, device=local.device)
+        dist.all_gather_into_tensor(out, local)
+    else:
+        parts = [torch.empty_like(local) for _ in range(world)]
+        dist.all_gather(parts, local)
+        out = torch.stack(parts)
+    full = out.permute(1, 0, 2).reshape(2, world * b)[:, :N]
+    return full[0], full[1]
+
+
+def gather_state(plan, psi_re, psi_im, begin: int, count: int, world: int, stream: int = 0) -> None:
+    """Fill psi_re/psi_im (length N, CUDA) with the full state: the local plan's
+    rows, all-gathered across ranks when world > 1."""
+    import torch
+
+    N = psi_re.numel()
+    if world == 1:
+        plan.copy_state(psi_re.data_ptr(), psi_im.data_ptr(), stream)
+        return
+    lr = torch.empty(count, dtype=torch.float64, device=psi_re.device)
+    li = torch.empty(count, dtype=torch.float64, device=psi_re.device)
+    if plan is not None and count:
+        plan.copy_state(lr.data_ptr(), li.data_ptr(), stream)
+    re, im = gather_rows(lr, li, N, world)
+    psi_re.copy_(re)
+    psi_im.copy_(im)

@@ -41,8 +41,19 @@ def test_named_circuits_unitary(golden, sim):
         assert rel_frob(ur, ui, u[0], u[1]) <= TOL, case
 
 
+@pytest.fixture(scope="module", params=["4m", "3m"])
+def sim_mode(request):
+    from paper_2305_14398_b200 import native
+    from paper_2305_14398_b200.simulator import B200UnitarySimulator
+
+    s = B200UnitarySimulator(gemm_mode=native.GEMM_4M if request.param == "4m" else native.GEMM_3M)
+    yield s
+    s.close()
+
+
 @pytest.mark.parametrize("suite", ["cross", "fsv", "norm", "steps", "par", "det", "comp"])
-def test_random_suites(golden, sim, suite):
+def test_random_suites(golden, sim_mode, suite):
+    sim = sim_mode
     worst = 0.0
     for case in golden.suites[suite]:
         flat = golden.flat(case)
@@ -183,3 +194,43 @@ def native_copy(dev_ptr, host):
     from paper_2305_14398_b200.simulator import torch_view
 
     host[...] = torch_view(dev_ptr, host.shape).cpu().numpy()
+
+
+@pytest.mark.parametrize("tile", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("name,n", [("qft", 8), ("deutsch-jozsa", 9), ("entangle", 9)])
+def test_every_gemm_tile_variant(monkeypatch, sim, orc, tile, name, n):
+    """Force each K2 variant (v1 128x64 / 64x64 / 32x32, warp-specialised 4M / 3M)
+    through the QSB_TILE debug switch and check it against the oracle."""
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+
+    monkeypatch.setenv("QSB_TILE", str(tile))
+    c, reg = q.make_named_circuit(name, n)
+    flat = native.flatten(c, reg)
+    ur, ui = sim.build_unitary(flat)
+    orr, ori = orc.circuit_unitary(flat)
+    assert rel_frob(ur, ui, orr, ori) <= TOL
+
+
+@pytest.mark.parametrize("mode", ["4m", "3m"])
+def test_qft12_modes_against_dft_columns(mode, orc):
+    """n = 12 through the production tiles (both arithmetic modes): psi and
+    sampled columns of U against the fsv restatement."""
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+    from paper_2305_14398_b200.simulator import B200UnitarySimulator
+
+    s = B200UnitarySimulator(gemm_mode=native.GEMM_4M if mode == "4m" else native.GEMM_3M)
+    c, reg = q.make_named_circuit("qft", 12)
+    flat = native.flatten(c, reg)
+    ur, ui = s.build_unitary(flat)
+    for col in (0, 1, 777, 4095):
+        cr, ci = orc.unitary_column(flat, col)
+        assert rel_frob(ur[:, col], ui[:, col], cr, ci) <= TOL
+    # QFT == DFT: U[j, k] = exp(2 pi i jk / N) / sqrt(N)
+    N = 1 << 12
+    j = np.arange(N)[:, None]
+    k = np.arange(0, N, 97)[None, :]
+    dft = np.exp(2j * np.pi * ((j * k) % N) / N) / np.sqrt(N)
+    assert rel_frob(ur[:, ::97], ui[:, ::97], dft.real, dft.imag) <= TOL
+    s.close()
