@@ -41,6 +41,8 @@ struct BlockDesc {
 struct LayerDesc {
     uint32_t idmask;    // index bits owned by identity blocks
     int32_t nblocks;    // non-identity blocks, qubit-0-first (fold order)
+    int32_t real;       // every block entry has an exactly-zero imaginary part
+    int32_t pad;
     BlockDesc blocks[kMaxBlocks];
 };
 

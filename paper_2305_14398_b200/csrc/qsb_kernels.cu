@@ -99,6 +99,98 @@ __device__ __forceinline__ void layer_entry(const LayerDesc& d, uint32_t r, uint
     vi = ai;
 }
 
+// Continue the left fold from block `b` with the running value (ar, ai).
+// Real layers multiply real parts only: (a, 0) * (e, 0) = (a*e - 0*0, a*0 + 0*e)
+// = (a*e, +-0), so the real product is bit-identical to the complex one.
+__device__ __forceinline__ void fold_from(const LayerDesc& d, int b, uint32_t r, uint32_t c, double& ar,
+                                          double& ai) {
+    if (d.real) {
+        for (; b < d.nblocks; ++b) {
+            if (ar == 0.0) break;
+            double er, ei;
+            block_entry(d.blocks[b], r, c, er, ei);
+            ar = __dmul_rn(ar, er);
+        }
+        ai = 0.0;
+        return;
+    }
+    for (; b < d.nblocks; ++b) {
+        if (ar == 0.0 && ai == 0.0) break;
+        double er, ei, tr, ti;
+        block_entry(d.blocks[b], r, c, er, ei);
+        cmul_rn(ar, ai, er, ei, tr, ti);
+        ar = tr;
+        ai = ti;
+    }
+}
+
+// Tile-level view of one layer for a BK x BN operator tile whose row and column
+// indices vary only in their low LOWBITS bits: blocks entirely above LOWBITS are
+// constant over the tile and — being the most significant — form a prefix of
+// the fold, so their product P is computed once per tile; identity bits above
+// LOWBITS decide whether the whole tile is zero. Per element only the
+// remaining (low) blocks are folded, continuing from P: the same sequence of
+// roundings as the full fold, hence still bit-exact.
+struct TilePrefix {
+    double pr, pi;  // prefix product (valid if nconst > 0)
+    int nconst;     // blocks in the prefix
+    bool zero;      // whole tile is zero
+};
+
+template <int LOWBITS>
+__device__ __forceinline__ TilePrefix tile_prefix(const LayerDesc& d, uint32_t r0, uint32_t c0) {
+    constexpr uint32_t LOW = (1u << LOWBITS) - 1u;
+    TilePrefix tp{1.0, 0.0, 0, ((r0 ^ c0) & d.idmask & ~LOW) != 0};
+    if (tp.zero) return tp;
+    int b = 0;
+    while (b < d.nblocks && d.blocks[b].shift >= LOWBITS) ++b;
+    tp.nconst = b;
+    if (b > 0) {
+        block_entry(d.blocks[0], r0, c0, tp.pr, tp.pi);
+        double pr = tp.pr, pi = tp.pi;
+        // fold the rest of the prefix
+        for (int k = 1; k < b; ++k) {
+            if (pr == 0.0 && pi == 0.0) break;
+            double er, ei, tr, ti;
+            block_entry(d.blocks[k], r0, c0, er, ei);
+            if (d.real) {
+                pr = __dmul_rn(pr, er);
+                pi = 0.0;
+            } else {
+                cmul_rn(pr, pi, er, ei, tr, ti);
+                pr = tr;
+                pi = ti;
+            }
+        }
+        tp.pr = pr;
+        tp.pi = pi;
+        tp.zero = (pr == 0.0 && pi == 0.0);
+    }
+    return tp;
+}
+
+template <int LOWBITS>
+__device__ __forceinline__ void tile_entry(const LayerDesc& d, const TilePrefix& tp, uint32_t r, uint32_t c,
+                                           double& vr, double& vi) {
+    constexpr uint32_t LOW = (1u << LOWBITS) - 1u;
+    if ((r ^ c) & d.idmask & LOW) {
+        vr = 0.0;
+        vi = 0.0;
+        return;
+    }
+    if (tp.nconst > 0) {
+        vr = tp.pr;
+        vi = tp.pi;
+        fold_from(d, tp.nconst, r, c, vr, vi);
+    } else if (d.nblocks == 0) {
+        vr = 1.0;
+        vi = 0.0;
+    } else {
+        block_entry(d.blocks[0], r, c, vr, vi);
+        fold_from(d, 1, r, c, vr, vi);
+    }
+}
+
 // ----------------------------------------------------------------------------
 // K1: expansion
 // ----------------------------------------------------------------------------
@@ -376,6 +468,8 @@ struct WsCfg {
     static constexpr int STAGES = (200 * 1024) / STAGE;
     static constexpr int SMEM = 1024 + STAGES * STAGE + 2 * STAGES * 8;
     static constexpr int PAIRS = 8 * BN / (32 * PRODUCER_WARPS);
+    static constexpr int LOWBITS = 6;  // log2(BN) >= log2(BK): tile indices vary below this bit
+    static_assert((1 << LOWBITS) == BN, "BN must be 2^LOWBITS");
     static constexpr int CONSUMER_REGS = 224;
     static constexpr int PRODUCER_REGS = 56;
 };
@@ -426,20 +520,27 @@ __global__ void __launch_bounds__(WsCfg<THREE_M>::THREADS, 1)
                 tma_load_3d(stage, &tmA, sFull + 8 * s, kt * C::BK, m0, 0);
             }
             const uint32_t bBase = stage + C::A_BYTES;
+            const TilePrefix tp = tile_prefix<C::LOWBITS>(layer, static_cast<uint32_t>(kt * C::BK),
+                                                          static_cast<uint32_t>(n0));
+            if (tp.zero) {
+                // whole operator tile is zero: clear the B planes of this stage
+                for (int o = ptid * 16; o < C::B_BYTES; o += 16 * 32 * C::PRODUCER_WARPS) sts128(bBase + o, 0.0, 0.0);
+            } else {
 #pragma unroll
-            for (int q = 0; q < C::PAIRS; ++q) {
-                const int idx = ptid + q * 32 * C::PRODUCER_WARPS;
-                const int n = idx % BN;
-                const int p = idx / BN;
-                const uint32_t r0 = static_cast<uint32_t>(kt * C::BK + 2 * p);
-                const uint32_t col = static_cast<uint32_t>(n0 + n);
-                double a_r, a_i, b_r, b_i;
-                layer_entry(layer, r0, col, a_r, a_i);
-                layer_entry(layer, r0 + 1, col, b_r, b_i);
-                const uint32_t off = n * 128 + ((p ^ (n & 7)) << 4);
-                sts128(bBase + off, a_r, b_r);
-                sts128(bBase + BN * 128 + off, a_i, b_i);
-                if (THREE_M) sts128(bBase + 2 * BN * 128 + off, __dadd_rn(a_r, a_i), __dadd_rn(b_r, b_i));
+                for (int q = 0; q < C::PAIRS; ++q) {
+                    const int idx = ptid + q * 32 * C::PRODUCER_WARPS;
+                    const int n = idx % BN;
+                    const int p = idx / BN;
+                    const uint32_t r0 = static_cast<uint32_t>(kt * C::BK + 2 * p);
+                    const uint32_t col = static_cast<uint32_t>(n0 + n);
+                    double a_r, a_i, b_r, b_i;
+                    tile_entry<C::LOWBITS>(layer, tp, r0, col, a_r, a_i);
+                    tile_entry<C::LOWBITS>(layer, tp, r0 + 1, col, b_r, b_i);
+                    const uint32_t off = n * 128 + ((p ^ (n & 7)) << 4);
+                    sts128(bBase + off, a_r, b_r);
+                    sts128(bBase + BN * 128 + off, a_i, b_i);
+                    if (THREE_M) sts128(bBase + 2 * BN * 128 + off, __dadd_rn(a_r, a_i), __dadd_rn(b_r, b_i));
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(sFull + 8 * s);

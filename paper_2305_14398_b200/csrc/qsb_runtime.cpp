@@ -313,6 +313,19 @@ qsb::LayerDesc build_layer(const qsb_circuit* c, int step, const std::vector<int
         }
     }
     d.nblocks = nb;
+    d.real = 1;
+    for (int i = 0; i < nb; ++i) {
+        const qsb::BlockDesc& blk = d.blocks[i];
+        if (blk.kind == qsb::kBlockTable) {
+            const qsb_function& f = c->functions[reinterpret_cast<intptr_t>(blk.t_im)];
+            const size_t d2 = static_cast<size_t>(f.dim) * f.dim;
+            for (size_t e = 0; e < d2 && d.real; ++e)
+                if (f.im[e] != 0.0) d.real = 0;
+        } else {
+            for (int e = 0; e < 4; ++e)
+                if (blk.u_im[e] != 0.0) d.real = 0;
+        }
+    }
     const uint32_t all = (n >= 32) ? 0xffffffffu : ((1u << n) - 1u);
     d.idmask = all & ~covered;
     return d;
@@ -418,7 +431,8 @@ void upload_tables(qsb_plan* p, const qsb_circuit* c) {
 
 int pick_tile(int M, int N, int gemm_mode) {
     const int sms = 148;
-    if (const char* force = std::getenv("QSB_TILE")) {  // debugging / tests: force a tile variant
+    const char* force = std::getenv("QSB_TILE");  // debugging / tests: force a tile variant
+    if (force && *force) {
         const int t = std::atoi(force);
         if (t >= 0 && t <= qsb::kTileWs3M && M % qsb::gemm_tile_rows(t) == 0 && N % qsb::gemm_tile_cols(t) == 0)
             return t;

@@ -234,3 +234,41 @@ def test_qft12_modes_against_dft_columns(mode, orc):
     dft = np.exp(2j * np.pi * ((j * k) % N) / N) / np.sqrt(N)
     assert rel_frob(ur[:, ::97], ui[:, ::97], dft.real, dft.imag) <= TOL
     s.close()
+
+
+@pytest.mark.parametrize("tile", [3, 4])
+def test_random_circuits_through_warp_specialised_tiles(monkeypatch, golden, sim, orc, tile):
+    """The production K2 (warp-specialised, tile-prefix operator generation)
+    on every golden random circuit it can tile (n >= 6), against the reference."""
+    monkeypatch.setenv("QSB_TILE", str(tile))
+    checked = 0
+    for suite in ("cross", "det", "fsv", "norm"):
+        for case in golden.suites[suite]:
+            flat = golden.flat(case)
+            if flat.n_qubits < 6 or (tile == 3 and flat.n_qubits < 7):
+                continue
+            out = sim.simulate_full_state(flat)
+            re, im = golden.psi(case)
+            assert rel_frob(out.re, out.im, re, im) <= TOL, (case, tile)
+            checked += 1
+    assert checked > 40
+
+
+def test_layer_entries_through_tiles_bit_exact(monkeypatch, sim, orc):
+    """Every K2 product here multiplies by a permutation, so the 4M path must
+    reproduce the reference bit-for-bit: U = X(1) CNOT(0,n-1) L with L a mixed
+    single-layer step. Row form: V = X[rows]; V <- V*CNOT; V <- V*L, and V*L
+    picks exactly one generated entry of L per output (1*x + 0*y + ... = x),
+    so K2's tile-prefix operator generation is checked entry by entry."""
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+
+    monkeypatch.setenv("QSB_TILE", "3")
+    for n in (7, 8, 9, 10):
+        c = q.Circuit(n)
+        c.h(1).t(0).cr(0.3, n - 1, 2)   # step 0: one layer, CR spans qubits 2..n-1
+        c.cnot(0, n - 1).x(1)           # step 1: two permutation layers
+        flat = native.flatten(c)
+        ur, ui = sim.build_unitary(flat)
+        orr, ori = orc.circuit_unitary(flat)
+        assert np.array_equal(ur, orr) and np.array_equal(ui, ori), n

@@ -9,7 +9,9 @@ import paper_2305_14398_b200 as q  # noqa: E402
 from paper_2305_14398_b200 import native  # noqa: E402
 from paper_2305_14398_b200.simulator import B200UnitarySimulator  # noqa: E402
 
-sim = B200UnitarySimulator()
+import os
+from paper_2305_14398_b200 import native as _n
+sim = B200UnitarySimulator(gemm_mode={'4m': _n.GEMM_4M, '3m': _n.GEMM_3M}.get(os.environ.get('QSB_GEMM', ''), _n.GEMM_AUTO))
 for spec in sys.argv[1:] or ["qft:10", "qft:12"]:
     name, n = spec.split(":")
     c, reg = q.make_named_circuit(name, int(n))
