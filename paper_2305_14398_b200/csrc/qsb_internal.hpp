@@ -42,7 +42,8 @@ struct LayerDesc {
     uint32_t idmask;    // index bits owned by identity blocks
     int32_t nblocks;    // non-identity blocks, qubit-0-first (fold order)
     int32_t real;       // every block entry has an exactly-zero imaginary part
-    int32_t pad;
+    uint32_t zmask;     // bits on which r and c must agree for a nonzero entry:
+                        // identity bits + every controlled block's bits except its target
     BlockDesc blocks[kMaxBlocks];
 };
 
@@ -64,7 +65,7 @@ int launch_probabilities(const double* psi, int64_t dim, double* p, double* part
                          double* norm, void* stream);
 
 // Tile shapes of the K2 GEMM (rows x cols of the output tile).
-enum GemmTile : int { kTile128x64 = 0, kTile64x64 = 1, kTile32x32 = 2, kTileWs4M = 3, kTileWs3M = 4 };
+enum GemmTile : int { kTile128x64 = 0, kTile64x64 = 1, kTile32x32 = 2, kTileWs4M = 3, kTileWs3M = 4, kTileWs3MA = 5 };
 int configure_kernels();
 int gemm_tile_rows(int tile);
 int gemm_tile_cols(int tile);

@@ -140,7 +140,7 @@ struct TilePrefix {
 template <int LOWBITS>
 __device__ __forceinline__ TilePrefix tile_prefix(const LayerDesc& d, uint32_t r0, uint32_t c0) {
     constexpr uint32_t LOW = (1u << LOWBITS) - 1u;
-    TilePrefix tp{1.0, 0.0, 0, ((r0 ^ c0) & d.idmask & ~LOW) != 0};
+    TilePrefix tp{1.0, 0.0, 0, ((r0 ^ c0) & d.zmask & ~LOW) != 0};
     if (tp.zero) return tp;
     int b = 0;
     while (b < d.nblocks && d.blocks[b].shift >= LOWBITS) ++b;
@@ -188,6 +188,86 @@ __device__ __forceinline__ void tile_entry(const LayerDesc& d, const TilePrefix&
     } else {
         block_entry(d.blocks[0], r, c, vr, vi);
         fold_from(d, 1, r, c, vr, vi);
+    }
+}
+
+// Producer-side batch generator: EB elements per thread, blocks outermost so
+// each block's parameters are loaded once (uniformly) per batch and entries
+// are selected in registers — no divergent constant-bank loads. The running
+// value starts at the tile prefix P (or 1 + 0i when no block is constant:
+// 1*e = e exactly, up to the sign of zero), then multiplies every low block in
+// fold order with separately rounded products: bit-exact with kronecker_fold.
+__device__ __forceinline__ double sel4(int e, double a0, double a1, double a2, double a3) {
+    const double lo = (e & 1) ? a1 : a0;
+    const double hi = (e & 1) ? a3 : a2;
+    return (e & 2) ? hi : lo;
+}
+
+template <int EB, int LOWBITS>
+__device__ __forceinline__ void gen_batch(const LayerDesc& d, const TilePrefix& tp, const uint32_t (&r)[EB],
+                                          const uint32_t (&c)[EB], double (&vr)[EB], double (&vi)[EB]) {
+    constexpr uint32_t LOW = (1u << LOWBITS) - 1u;
+    const bool real = d.real != 0;
+#pragma unroll
+    for (int k = 0; k < EB; ++k) {
+        const bool nz = ((r[k] ^ c[k]) & d.zmask & LOW) == 0;
+        vr[k] = nz ? (tp.nconst > 0 ? tp.pr : 1.0) : 0.0;
+        vi[k] = nz ? (tp.nconst > 0 ? tp.pi : 0.0) : 0.0;
+    }
+    for (int b = tp.nconst; b < d.nblocks; ++b) {
+        const BlockDesc& B = d.blocks[b];
+        const int kind = B.kind, shift = B.shift;
+        const uint32_t mask = B.mask;
+        if (kind == kBlockTable) {
+#pragma unroll
+            for (int k = 0; k < EB; ++k) {
+                const uint32_t rb = (r[k] >> shift) & mask, cb = (c[k] >> shift) & mask;
+                const size_t e = (static_cast<size_t>(rb) << B.span) + cb;
+                const double er = __ldg(B.t_re + e), ei = __ldg(B.t_im + e);
+                double tr, ti;
+                if (real) {
+                    vr[k] = __dmul_rn(vr[k], er);
+                } else {
+                    cmul_rn(vr[k], vi[k], er, ei, tr, ti);
+                    vr[k] = tr;
+                    vi[k] = ti;
+                }
+            }
+            continue;
+        }
+        const double u0 = B.u_re[0], u1 = B.u_re[1], u2 = B.u_re[2], u3 = B.u_re[3];
+        const double w0 = B.u_im[0], w1 = B.u_im[1], w2 = B.u_im[2], w3 = B.u_im[3];
+        const uint32_t cm = B.cmask, tm = B.tmask;
+        const bool controlled = kind == kBlockControlled;
+#pragma unroll
+        for (int k = 0; k < EB; ++k) {
+            const uint32_t rb = (r[k] >> shift) & mask, cb = (c[k] >> shift) & mask;
+            double er, ei;
+            if (controlled) {
+                // controlled_unitary (gates.cpp:94-107)
+                const bool active = (cb & cm) != 0;
+                const bool hit = ((rb ^ cb) & ~tm) == 0;
+                const int e = ((rb & tm) ? 2 : 0) + ((cb & tm) ? 1 : 0);
+                er = active ? (hit ? sel4(e, u0, u1, u2, u3) : 0.0) : (rb == cb ? 1.0 : 0.0);
+                ei = active ? (hit ? sel4(e, w0, w1, w2, w3) : 0.0) : 0.0;
+            } else {
+                const int e = static_cast<int>(rb * 2 + cb);
+                er = sel4(e, u0, u1, u2, u3);
+                ei = sel4(e, w0, w1, w2, w3);
+            }
+            if (real) {
+                vr[k] = __dmul_rn(vr[k], er);
+            } else {
+                double tr, ti;
+                cmul_rn(vr[k], vi[k], er, ei, tr, ti);
+                vr[k] = tr;
+                vi[k] = ti;
+            }
+        }
+    }
+    if (real) {
+#pragma unroll
+        for (int k = 0; k < EB; ++k) vi[k] = 0.0;
     }
 }
 
@@ -449,7 +529,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN>::THREADS, 1)
 //     Ci = T3 - T1 - T2 (warp tile 32x16, CTA 64x64; the producer writes the
 //     Br+Bi plane, consumers form Ar+Ai in registers).
 
-template <bool THREE_M>
+template <bool THREE_M, bool ASUM = false>
 struct WsCfg {
     static constexpr int BK = 16;
     static constexpr int CONSUMER_WARPS = 8;
@@ -462,33 +542,36 @@ struct WsCfg {
     static constexpr int BM = CWM * 32;
     static constexpr int BN = CWN * WT_N;
     static constexpr int B_PLANES = THREE_M ? 3 : 2;
-    static constexpr int A_BYTES = 2 * BM * BK * 8;
+    static constexpr int A_PLANES = (THREE_M && ASUM) ? 3 : 2;  // + Ar+Ai plane written by the producer
+    static constexpr int A_TMA_BYTES = 2 * BM * BK * 8;
+    static constexpr int A_BYTES = A_PLANES * BM * BK * 8;
     static constexpr int B_BYTES = B_PLANES * BN * BK * 8;
     static constexpr int STAGE = A_BYTES + B_BYTES;
     static constexpr int STAGES = (200 * 1024) / STAGE;
-    static constexpr int SMEM = 1024 + STAGES * STAGE + 2 * STAGES * 8;
+    static constexpr int SMEM = 1024 + STAGES * STAGE + 3 * STAGES * 8;
     static constexpr int PAIRS = 8 * BN / (32 * PRODUCER_WARPS);
     static constexpr int LOWBITS = 6;  // log2(BN) >= log2(BK): tile indices vary below this bit
     static_assert((1 << LOWBITS) == BN, "BN must be 2^LOWBITS");
-    static constexpr int CONSUMER_REGS = 224;
-    static constexpr int PRODUCER_REGS = 56;
+    static constexpr int CONSUMER_REGS = 216;
+    static constexpr int PRODUCER_REGS = 72;
 };
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-template <bool THREE_M>
-__global__ void __launch_bounds__(WsCfg<THREE_M>::THREADS, 1)
+template <bool THREE_M, bool ASUM>
+__global__ void __launch_bounds__(WsCfg<THREE_M, ASUM>::THREADS, 1)
     zgemm_ws_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ LayerDesc layer,
                     double* __restrict__ out, int M, int N) {
-    using C = WsCfg<THREE_M>;
+    using C = WsCfg<THREE_M, ASUM>;
     constexpr int BM = C::BM, BN = C::BN;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sBase = smem_u32(smem);
     const uint32_t sFull = sBase + C::STAGES * C::STAGE;
     const uint32_t sEmpty = sFull + 8 * C::STAGES;
+    const uint32_t sFullA = sEmpty + 8 * C::STAGES;  // TMA completion (ASUM only)
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -499,8 +582,9 @@ __global__ void __launch_bounds__(WsCfg<THREE_M>::THREADS, 1)
 
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
-            mbar_init(sFull + 8 * s, 1 + C::PRODUCER_WARPS);
+            mbar_init(sFull + 8 * s, (ASUM ? 0 : 1) + C::PRODUCER_WARPS);
             mbar_init(sEmpty + 8 * s, C::CONSUMER_WARPS);
+            mbar_init(sFullA + 8 * s, 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -515,9 +599,10 @@ __global__ void __launch_bounds__(WsCfg<THREE_M>::THREADS, 1)
             const int s = kt % C::STAGES;
             if (kt >= C::STAGES) mbar_wait(sEmpty + 8 * s, ((kt / C::STAGES) & 1) ^ 1);
             const uint32_t stage = sBase + s * C::STAGE;
+            const uint32_t tma_bar = ASUM ? sFullA + 8 * s : sFull + 8 * s;
             if (ptid == 0) {
-                mbar_expect_tx(sFull + 8 * s, C::A_BYTES);
-                tma_load_3d(stage, &tmA, sFull + 8 * s, kt * C::BK, m0, 0);
+                mbar_expect_tx(tma_bar, C::A_TMA_BYTES);
+                tma_load_3d(stage, &tmA, tma_bar, kt * C::BK, m0, 0);
             }
             const uint32_t bBase = stage + C::A_BYTES;
             const TilePrefix tp = tile_prefix<C::LOWBITS>(layer, static_cast<uint32_t>(kt * C::BK),
@@ -526,20 +611,41 @@ __global__ void __launch_bounds__(WsCfg<THREE_M>::THREADS, 1)
                 // whole operator tile is zero: clear the B planes of this stage
                 for (int o = ptid * 16; o < C::B_BYTES; o += 16 * 32 * C::PRODUCER_WARPS) sts128(bBase + o, 0.0, 0.0);
             } else {
+                constexpr int EB = 4;  // elements per batch = 2 (k, k+1) pairs
 #pragma unroll
-                for (int q = 0; q < C::PAIRS; ++q) {
-                    const int idx = ptid + q * 32 * C::PRODUCER_WARPS;
-                    const int n = idx % BN;
-                    const int p = idx / BN;
-                    const uint32_t r0 = static_cast<uint32_t>(kt * C::BK + 2 * p);
-                    const uint32_t col = static_cast<uint32_t>(n0 + n);
-                    double a_r, a_i, b_r, b_i;
-                    tile_entry<C::LOWBITS>(layer, tp, r0, col, a_r, a_i);
-                    tile_entry<C::LOWBITS>(layer, tp, r0 + 1, col, b_r, b_i);
-                    const uint32_t off = n * 128 + ((p ^ (n & 7)) << 4);
-                    sts128(bBase + off, a_r, b_r);
-                    sts128(bBase + BN * 128 + off, a_i, b_i);
-                    if (THREE_M) sts128(bBase + 2 * BN * 128 + off, __dadd_rn(a_r, a_i), __dadd_rn(b_r, b_i));
+                for (int q0 = 0; q0 < C::PAIRS; q0 += EB / 2) {
+                    uint32_t rr[EB], cc[EB];
+                    int nn[EB / 2], pp[EB / 2];
+#pragma unroll
+                    for (int h = 0; h < EB / 2; ++h) {
+                        const int idx = ptid + (q0 + h) * 32 * C::PRODUCER_WARPS;
+                        nn[h] = idx % BN;
+                        pp[h] = idx / BN;
+                        rr[2 * h] = static_cast<uint32_t>(kt * C::BK + 2 * pp[h]);
+                        rr[2 * h + 1] = rr[2 * h] + 1;
+                        cc[2 * h] = cc[2 * h + 1] = static_cast<uint32_t>(n0 + nn[h]);
+                    }
+                    double vr[EB], vi[EB];
+                    gen_batch<EB, C::LOWBITS>(layer, tp, rr, cc, vr, vi);
+#pragma unroll
+                    for (int h = 0; h < EB / 2; ++h) {
+                        const uint32_t off = nn[h] * 128 + ((pp[h] ^ (nn[h] & 7)) << 4);
+                        sts128(bBase + off, vr[2 * h], vr[2 * h + 1]);
+                        sts128(bBase + BN * 128 + off, vi[2 * h], vi[2 * h + 1]);
+                        if (THREE_M)
+                            sts128(bBase + 2 * BN * 128 + off, __dadd_rn(vr[2 * h], vi[2 * h]),
+                                   __dadd_rn(vr[2 * h + 1], vi[2 * h + 1]));
+                    }
+                }
+            }
+            if (ASUM) {
+                // Ar + Ai plane: same swizzled offsets as the re/im planes (line & 7 is
+                // unchanged because BM is a multiple of 8).
+                mbar_wait(tma_bar, (kt / C::STAGES) & 1);
+                for (int o = ptid * 16; o < BM * 128; o += 16 * 32 * C::PRODUCER_WARPS) {
+                    const double2 x = lds128(stage + o);
+                    const double2 y = lds128(stage + BM * 128 + o);
+                    sts128(stage + 2 * BM * 128 + o, __dadd_rn(x.x, y.x), __dadd_rn(x.y, y.y));
                 }
             }
             __syncwarp();
@@ -567,20 +673,23 @@ __global__ void __launch_bounds__(WsCfg<THREE_M>::THREADS, 1)
     for (int kt = 0; kt < KT; ++kt) {
         const int s = kt % C::STAGES;
         mbar_wait(sFull + 8 * s, (kt / C::STAGES) & 1);
+        if (ASUM) mbar_wait(sFullA + 8 * s, (kt / C::STAGES) & 1);
         const uint32_t aRe = sBase + s * C::STAGE;
         const uint32_t aIm = aRe + BM * 128;
+        const uint32_t aSm = aIm + BM * 128;
         const uint32_t bRe = aRe + C::A_BYTES;
         const uint32_t bIm = bRe + BN * 128;
         const uint32_t bSm = bIm + BN * 128;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const uint32_t choff = static_cast<uint32_t>(((2 * t + h) ^ g) << 4);
-            double2 ar[4], ai[4], br[NT], bi[NT], bs[NT];
+            double2 ar[4], ai[4], as2[4], br[NT], bi[NT], bs[NT];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const uint32_t line = static_cast<uint32_t>(wm * 32 + i * 8 + g) * 128 + choff;
                 ar[i] = lds128(aRe + line);
                 ai[i] = lds128(aIm + line);
+                if (ASUM) as2[i] = lds128(aSm + line);
             }
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
@@ -605,7 +714,7 @@ __global__ void __launch_bounds__(WsCfg<THREE_M>::THREADS, 1)
                 if (THREE_M) {
                     double xs[4], ys[NT];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) xs[i] = __dadd_rn(xr[i], xi[i]);
+                    for (int i = 0; i < 4; ++i) xs[i] = ASUM ? (e ? as2[i].y : as2[i].x) : __dadd_rn(xr[i], xi[i]);
 #pragma unroll
                     for (int j = 0; j < NT; ++j) ys[j] = e ? bs[j].y : bs[j].x;
 #pragma unroll
@@ -670,17 +779,18 @@ __global__ void __launch_bounds__(WsCfg<THREE_M>::THREADS, 1)
     }
 }
 
-template <bool THREE_M>
+template <bool THREE_M, bool ASUM>
 static int configure_ws_t() {
-    return static_cast<int>(cudaFuncSetAttribute(zgemm_ws_kernel<THREE_M>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, WsCfg<THREE_M>::SMEM));
+    return static_cast<int>(cudaFuncSetAttribute(zgemm_ws_kernel<THREE_M, ASUM>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 WsCfg<THREE_M, ASUM>::SMEM));
 }
 
-template <bool THREE_M>
+template <bool THREE_M, bool ASUM>
 static int launch_ws_t(const GemmArgs& a, void* stream) {
-    using C = WsCfg<THREE_M>;
+    using C = WsCfg<THREE_M, ASUM>;
     dim3 grid(a.N / C::BN, a.M / C::BM);
-    zgemm_ws_kernel<THREE_M><<<grid, C::THREADS, C::SMEM, static_cast<cudaStream_t>(stream)>>>(
+    zgemm_ws_kernel<THREE_M, ASUM><<<grid, C::THREADS, C::SMEM, static_cast<cudaStream_t>(stream)>>>(
         *static_cast<const CUtensorMap*>(a.tmap), *a.layer, a.out, a.M, a.N);
     return static_cast<int>(cudaGetLastError());
 }
@@ -691,6 +801,7 @@ int gemm_tile_rows(int tile) {
     case kTile64x64: return 64;
     case kTileWs4M: return WsCfg<false>::BM;
     case kTileWs3M: return WsCfg<true>::BM;
+    case kTileWs3MA: return WsCfg<true, true>::BM;
     default: return 32;
     }
 }
@@ -699,6 +810,7 @@ int gemm_tile_cols(int tile) {
     case kTile32x32: return 32;
     case kTileWs4M: return WsCfg<false>::BN;
     case kTileWs3M: return WsCfg<true>::BN;
+    case kTileWs3MA: return WsCfg<true, true>::BN;
     default: return 64;
     }
 }
@@ -721,8 +833,9 @@ static int launch_zgemm_t(const GemmArgs& a, void* stream) {
 
 int launch_zgemm(const GemmArgs& a, int tile, int /*gemm_mode*/, void* stream) {
     switch (tile) {
-    case kTileWs4M: return launch_ws_t<false>(a, stream);
-    case kTileWs3M: return launch_ws_t<true>(a, stream);
+    case kTileWs4M: return launch_ws_t<false, false>(a, stream);
+    case kTileWs3M: return launch_ws_t<true, false>(a, stream);
+    case kTileWs3MA: return launch_ws_t<true, true>(a, stream);
     case kTile128x64: return launch_zgemm_t<128, 64>(a, stream);
     case kTile64x64: return launch_zgemm_t<64, 64>(a, stream);
     default: return launch_zgemm_t<32, 32>(a, stream);
@@ -903,8 +1016,9 @@ int configure_kernels() {
     if ((e = configure_zgemm_t<128, 64>())) return e;
     if ((e = configure_zgemm_t<64, 64>())) return e;
     if ((e = configure_zgemm_t<32, 32>())) return e;
-    if ((e = configure_ws_t<false>())) return e;
-    if ((e = configure_ws_t<true>())) return e;
+    if ((e = configure_ws_t<false, false>())) return e;
+    if ((e = configure_ws_t<true, false>())) return e;
+    if ((e = configure_ws_t<true, true>())) return e;
     return static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
 }

@@ -328,6 +328,12 @@ qsb::LayerDesc build_layer(const qsb_circuit* c, int step, const std::vector<int
     }
     const uint32_t all = (n >= 32) ? 0xffffffffu : ((1u << n) - 1u);
     d.idmask = all & ~covered;
+    // controlled_unitary (gates.cpp:94-107) entry (rb, cb) is zero unless rb and cb
+    // agree outside the target bit, so those bits join the zero test.
+    d.zmask = d.idmask;
+    for (int i = 0; i < nb; ++i)
+        if (d.blocks[i].kind == qsb::kBlockControlled)
+            d.zmask |= (d.blocks[i].mask & ~d.blocks[i].tmask) << d.blocks[i].shift;
     return d;
 }
 
@@ -359,6 +365,7 @@ qsb::LayerDesc identity_layer(int n) {
     qsb::LayerDesc d;
     std::memset(&d, 0, sizeof d);
     d.idmask = (1u << n) - 1u;
+    d.zmask = d.idmask;
     return d;
 }
 
@@ -434,7 +441,7 @@ int pick_tile(int M, int N, int gemm_mode) {
     const char* force = std::getenv("QSB_TILE");  // debugging / tests: force a tile variant
     if (force && *force) {
         const int t = std::atoi(force);
-        if (t >= 0 && t <= qsb::kTileWs3M && M % qsb::gemm_tile_rows(t) == 0 && N % qsb::gemm_tile_cols(t) == 0)
+        if (t >= 0 && t <= qsb::kTileWs3MA && M % qsb::gemm_tile_rows(t) == 0 && N % qsb::gemm_tile_cols(t) == 0)
             return t;
     }
     const bool three = gemm_mode != QSB_GEMM_4M;

@@ -196,7 +196,7 @@ def native_copy(dev_ptr, host):
     host[...] = torch_view(dev_ptr, host.shape).cpu().numpy()
 
 
-@pytest.mark.parametrize("tile", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("tile", [0, 1, 2, 3, 4, 5])
 @pytest.mark.parametrize("name,n", [("qft", 8), ("deutsch-jozsa", 9), ("entangle", 9)])
 def test_every_gemm_tile_variant(monkeypatch, sim, orc, tile, name, n):
     """Force each K2 variant (v1 128x64 / 64x64 / 32x32, warp-specialised 4M / 3M)
@@ -236,7 +236,7 @@ def test_qft12_modes_against_dft_columns(mode, orc):
     s.close()
 
 
-@pytest.mark.parametrize("tile", [3, 4])
+@pytest.mark.parametrize("tile", [3, 4, 5])
 def test_random_circuits_through_warp_specialised_tiles(monkeypatch, golden, sim, orc, tile):
     """The production K2 (warp-specialised, tile-prefix operator generation)
     on every golden random circuit it can tile (n >= 6), against the reference."""
@@ -245,7 +245,7 @@ def test_random_circuits_through_warp_specialised_tiles(monkeypatch, golden, sim
     for suite in ("cross", "det", "fsv", "norm"):
         for case in golden.suites[suite]:
             flat = golden.flat(case)
-            if flat.n_qubits < 6 or (tile == 3 and flat.n_qubits < 7):
+            if flat.n_qubits < 6 or (tile == 3 and flat.n_qubits < 7):  # tile rows: 4M 128, 3M 64
                 continue
             out = sim.simulate_full_state(flat)
             re, im = golden.psi(case)
