@@ -56,7 +56,9 @@ struct GemmArgs {
     int N;
 };
 
-int launch_expand(const LayerDesc& layer, uint32_t row_begin, int M, int N, double* out, void* stream);
+int launch_expand(const LayerDesc& layer, uint32_t row_begin, int M, int N, double* out, int planes,
+                  void* stream);
+int gemm_tile_planes(int tile);  // planes of the V buffers a tile variant reads/writes (2, or 3 with Vr+Vi)
 int launch_zgemm(const GemmArgs& a, int tile, int gemm_mode, void* stream);
 int launch_small_circuit(const LayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, int N,
                          const double* x, double* v, double* psi, void* stream);
@@ -65,7 +67,7 @@ int launch_probabilities(const double* psi, int64_t dim, double* p, double* part
                          double* norm, void* stream);
 
 // Tile shapes of the K2 GEMM (rows x cols of the output tile).
-enum GemmTile : int { kTile128x64 = 0, kTile64x64 = 1, kTile32x32 = 2, kTileWs4M = 3, kTileWs3M = 4, kTileWs3MA = 5 };
+enum GemmTile : int { kTile128x64 = 0, kTile64x64 = 1, kTile32x32 = 2, kTileWs4M = 3, kTileWs3M = 4, kTileWs3MS = 5 };
 int configure_kernels();
 int gemm_tile_rows(int tile);
 int gemm_tile_cols(int tile);

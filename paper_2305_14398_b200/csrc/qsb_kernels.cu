@@ -277,7 +277,7 @@ __device__ __forceinline__ void gen_batch(const LayerDesc& d, const TilePrefix& 
 
 __global__ void __launch_bounds__(256) expand_kernel(const __grid_constant__ LayerDesc d,
                                                      uint32_t row_begin, int M, int N,
-                                                     double* __restrict__ out) {
+                                                     double* __restrict__ out, int planes) {
     const size_t plane = static_cast<size_t>(M) * N;
     const size_t pairs = plane / 2;
     const uint32_t half_n = static_cast<uint32_t>(N) / 2;
@@ -290,15 +290,18 @@ __global__ void __launch_bounds__(256) expand_kernel(const __grid_constant__ Lay
         layer_entry(d, row_begin + row, col + 1, r1, i1);
         reinterpret_cast<double2*>(out)[p] = make_double2(r0, r1);
         reinterpret_cast<double2*>(out + plane)[p] = make_double2(i0, i1);
+        if (planes == 3)
+            reinterpret_cast<double2*>(out + 2 * plane)[p] = make_double2(__dadd_rn(r0, i0), __dadd_rn(r1, i1));
     }
 }
 
-int launch_expand(const LayerDesc& layer, uint32_t row_begin, int M, int N, double* out, void* stream) {
+int launch_expand(const LayerDesc& layer, uint32_t row_begin, int M, int N, double* out, int planes,
+                  void* stream) {
     const size_t pairs = static_cast<size_t>(M) * N / 2;
     int blocks = static_cast<int>((pairs + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
-    expand_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(layer, row_begin, M, N, out);
+    expand_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(layer, row_begin, M, N, out, planes);
     return static_cast<int>(cudaGetLastError());
 }
 
@@ -529,7 +532,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN>::THREADS, 1)
 //     Ci = T3 - T1 - T2 (warp tile 32x16, CTA 64x64; the producer writes the
 //     Br+Bi plane, consumers form Ar+Ai in registers).
 
-template <bool THREE_M, bool ASUM = false>
+template <bool THREE_M, bool SUMPLANE = false>
 struct WsCfg {
     static constexpr int BK = 16;
     static constexpr int CONSUMER_WARPS = 8;
@@ -542,9 +545,11 @@ struct WsCfg {
     static constexpr int BM = CWM * 32;
     static constexpr int BN = CWN * WT_N;
     static constexpr int B_PLANES = THREE_M ? 3 : 2;
-    static constexpr int A_PLANES = (THREE_M && ASUM) ? 3 : 2;  // + Ar+Ai plane written by the producer
-    static constexpr int A_TMA_BYTES = 2 * BM * BK * 8;
-    static constexpr int A_BYTES = A_PLANES * BM * BK * 8;
+    // SUMPLANE: V carries a third plane Vr+Vi written by the previous GEMM's
+    // epilogue (or K1), so 3M consumers load it instead of adding in registers.
+    static constexpr int A_PLANES = (THREE_M && SUMPLANE) ? 3 : 2;
+    static constexpr int A_TMA_BYTES = A_PLANES * BM * BK * 8;
+    static constexpr int A_BYTES = A_TMA_BYTES;
     static constexpr int B_BYTES = B_PLANES * BN * BK * 8;
     static constexpr int STAGE = A_BYTES + B_BYTES;
     static constexpr int STAGES = (200 * 1024) / STAGE;
@@ -560,18 +565,17 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-template <bool THREE_M, bool ASUM>
-__global__ void __launch_bounds__(WsCfg<THREE_M, ASUM>::THREADS, 1)
+template <bool THREE_M, bool SUMPLANE>
+__global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
     zgemm_ws_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ LayerDesc layer,
                     double* __restrict__ out, int M, int N) {
-    using C = WsCfg<THREE_M, ASUM>;
+    using C = WsCfg<THREE_M, SUMPLANE>;
     constexpr int BM = C::BM, BN = C::BN;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sBase = smem_u32(smem);
     const uint32_t sFull = sBase + C::STAGES * C::STAGE;
     const uint32_t sEmpty = sFull + 8 * C::STAGES;
-    const uint32_t sFullA = sEmpty + 8 * C::STAGES;  // TMA completion (ASUM only)
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -582,9 +586,8 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, ASUM>::THREADS, 1)
 
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
-            mbar_init(sFull + 8 * s, (ASUM ? 0 : 1) + C::PRODUCER_WARPS);
+            mbar_init(sFull + 8 * s, 1 + C::PRODUCER_WARPS);
             mbar_init(sEmpty + 8 * s, C::CONSUMER_WARPS);
-            mbar_init(sFullA + 8 * s, 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -599,7 +602,7 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, ASUM>::THREADS, 1)
             const int s = kt % C::STAGES;
             if (kt >= C::STAGES) mbar_wait(sEmpty + 8 * s, ((kt / C::STAGES) & 1) ^ 1);
             const uint32_t stage = sBase + s * C::STAGE;
-            const uint32_t tma_bar = ASUM ? sFullA + 8 * s : sFull + 8 * s;
+            const uint32_t tma_bar = sFull + 8 * s;
             if (ptid == 0) {
                 mbar_expect_tx(tma_bar, C::A_TMA_BYTES);
                 tma_load_3d(stage, &tmA, tma_bar, kt * C::BK, m0, 0);
@@ -638,16 +641,6 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, ASUM>::THREADS, 1)
                     }
                 }
             }
-            if (ASUM) {
-                // Ar + Ai plane: same swizzled offsets as the re/im planes (line & 7 is
-                // unchanged because BM is a multiple of 8).
-                mbar_wait(tma_bar, (kt / C::STAGES) & 1);
-                for (int o = ptid * 16; o < BM * 128; o += 16 * 32 * C::PRODUCER_WARPS) {
-                    const double2 x = lds128(stage + o);
-                    const double2 y = lds128(stage + BM * 128 + o);
-                    sts128(stage + 2 * BM * 128 + o, __dadd_rn(x.x, y.x), __dadd_rn(x.y, y.y));
-                }
-            }
             __syncwarp();
             if (lane == 0) mbar_arrive(sFull + 8 * s);
         }
@@ -673,7 +666,6 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, ASUM>::THREADS, 1)
     for (int kt = 0; kt < KT; ++kt) {
         const int s = kt % C::STAGES;
         mbar_wait(sFull + 8 * s, (kt / C::STAGES) & 1);
-        if (ASUM) mbar_wait(sFullA + 8 * s, (kt / C::STAGES) & 1);
         const uint32_t aRe = sBase + s * C::STAGE;
         const uint32_t aIm = aRe + BM * 128;
         const uint32_t aSm = aIm + BM * 128;
@@ -689,7 +681,7 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, ASUM>::THREADS, 1)
                 const uint32_t line = static_cast<uint32_t>(wm * 32 + i * 8 + g) * 128 + choff;
                 ar[i] = lds128(aRe + line);
                 ai[i] = lds128(aIm + line);
-                if (ASUM) as2[i] = lds128(aSm + line);
+                if (SUMPLANE) as2[i] = lds128(aSm + line);
             }
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
@@ -714,7 +706,7 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, ASUM>::THREADS, 1)
                 if (THREE_M) {
                     double xs[4], ys[NT];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) xs[i] = ASUM ? (e ? as2[i].y : as2[i].x) : __dadd_rn(xr[i], xi[i]);
+                    for (int i = 0; i < 4; ++i) xs[i] = SUMPLANE ? (e ? as2[i].y : as2[i].x) : __dadd_rn(xr[i], xi[i]);
 #pragma unroll
                     for (int j = 0; j < NT; ++j) ys[j] = e ? bs[j].y : bs[j].x;
 #pragma unroll
@@ -775,22 +767,24 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, ASUM>::THREADS, 1)
             }
             *reinterpret_cast<double2*>(out + o) = make_double2(r0, r1);
             *reinterpret_cast<double2*>(out + plane + o) = make_double2(i0, i1);
+            if (SUMPLANE)
+                *reinterpret_cast<double2*>(out + 2 * plane + o) = make_double2(__dadd_rn(r0, i0), __dadd_rn(r1, i1));
         }
     }
 }
 
-template <bool THREE_M, bool ASUM>
+template <bool THREE_M, bool SUMPLANE>
 static int configure_ws_t() {
-    return static_cast<int>(cudaFuncSetAttribute(zgemm_ws_kernel<THREE_M, ASUM>,
+    return static_cast<int>(cudaFuncSetAttribute(zgemm_ws_kernel<THREE_M, SUMPLANE>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 WsCfg<THREE_M, ASUM>::SMEM));
+                                                 WsCfg<THREE_M, SUMPLANE>::SMEM));
 }
 
-template <bool THREE_M, bool ASUM>
+template <bool THREE_M, bool SUMPLANE>
 static int launch_ws_t(const GemmArgs& a, void* stream) {
-    using C = WsCfg<THREE_M, ASUM>;
+    using C = WsCfg<THREE_M, SUMPLANE>;
     dim3 grid(a.N / C::BN, a.M / C::BM);
-    zgemm_ws_kernel<THREE_M, ASUM><<<grid, C::THREADS, C::SMEM, static_cast<cudaStream_t>(stream)>>>(
+    zgemm_ws_kernel<THREE_M, SUMPLANE><<<grid, C::THREADS, C::SMEM, static_cast<cudaStream_t>(stream)>>>(
         *static_cast<const CUtensorMap*>(a.tmap), *a.layer, a.out, a.M, a.N);
     return static_cast<int>(cudaGetLastError());
 }
@@ -801,16 +795,18 @@ int gemm_tile_rows(int tile) {
     case kTile64x64: return 64;
     case kTileWs4M: return WsCfg<false>::BM;
     case kTileWs3M: return WsCfg<true>::BM;
-    case kTileWs3MA: return WsCfg<true, true>::BM;
+    case kTileWs3MS: return WsCfg<true, true>::BM;
     default: return 32;
     }
 }
+int gemm_tile_planes(int tile) { return tile == kTileWs3MS ? 3 : 2; }
+
 int gemm_tile_cols(int tile) {
     switch (tile) {
     case kTile32x32: return 32;
     case kTileWs4M: return WsCfg<false>::BN;
     case kTileWs3M: return WsCfg<true>::BN;
-    case kTileWs3MA: return WsCfg<true, true>::BN;
+    case kTileWs3MS: return WsCfg<true, true>::BN;
     default: return 64;
     }
 }
@@ -835,7 +831,7 @@ int launch_zgemm(const GemmArgs& a, int tile, int /*gemm_mode*/, void* stream) {
     switch (tile) {
     case kTileWs4M: return launch_ws_t<false, false>(a, stream);
     case kTileWs3M: return launch_ws_t<true, false>(a, stream);
-    case kTileWs3MA: return launch_ws_t<true, true>(a, stream);
+    case kTileWs3MS: return launch_ws_t<true, true>(a, stream);
     case kTile128x64: return launch_zgemm_t<128, 64>(a, stream);
     case kTile64x64: return launch_zgemm_t<64, 64>(a, stream);
     default: return launch_zgemm_t<32, 32>(a, stream);

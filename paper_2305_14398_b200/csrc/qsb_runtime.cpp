@@ -140,14 +140,15 @@ EncodeTiledFn encode_tiled() {
     return fn;
 }
 
-// Tensor map of a [2][M][N] double buffer, box (16, rows, 2), 128-byte swizzle.
-CUtensorMap make_tmap(void* base, int M, int N, int box_rows) {
+// Tensor map of a [planes][M][N] double buffer, box (16, rows, planes), 128-byte swizzle.
+CUtensorMap make_tmap(void* base, int M, int N, int box_rows, int planes) {
     CUtensorMap m;
     EncodeTiledFn fn = encode_tiled();
     if (!fn) raise(QSB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M), 2};
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M),
+                                static_cast<cuuint64_t>(planes)};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(N) * 8, static_cast<cuuint64_t>(M) * N * 8};
-    const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(box_rows), 2};
+    const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(planes)};
     const cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -393,6 +394,7 @@ struct qsb_plan {
     int M = 0;
     int N = 0;
     int tile = qsb::kTile32x32;
+    int planes = 2;  // V buffer planes: re, im (+ re+im for the 3M sum-plane tile)
     bool small = false;
     Buffers b;
     bool borrowed = false;
@@ -441,11 +443,11 @@ int pick_tile(int M, int N, int gemm_mode) {
     const char* force = std::getenv("QSB_TILE");  // debugging / tests: force a tile variant
     if (force && *force) {
         const int t = std::atoi(force);
-        if (t >= 0 && t <= qsb::kTileWs3MA && M % qsb::gemm_tile_rows(t) == 0 && N % qsb::gemm_tile_cols(t) == 0)
+        if (t >= 0 && t <= qsb::kTileWs3MS && M % qsb::gemm_tile_rows(t) == 0 && N % qsb::gemm_tile_cols(t) == 0)
             return t;
     }
     const bool three = gemm_mode != QSB_GEMM_4M;
-    const int ws = three ? qsb::kTileWs3M : qsb::kTileWs4M;
+    const int ws = three ? qsb::kTileWs3MS : qsb::kTileWs4M;
     const int wr = qsb::gemm_tile_rows(ws), wc = qsb::gemm_tile_cols(ws);
     if (M % wr == 0 && N % wc == 0 && (M / wr) * (N / wc) >= 2 * sms) return ws;
     if (M % 64 == 0 && N % 64 == 0 && (M / 64) * (N / 64) >= sms) return qsb::kTile64x64;
@@ -494,6 +496,15 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, const qsb_circuit* c, int64_t
         raise(QSB_ERR_ARGUMENT, "row shard [%lld, +%lld) is not contained in one aligned window of %lld rows",
               static_cast<long long>(row_begin), static_cast<long long>(row_count), static_cast<long long>(M));
     p->tile = p->small ? qsb::kTile32x32 : pick_tile(p->M, p->N, h->gemm_mode);
+    if (p->tile == qsb::kTileWs3MS) {
+        // the sum plane costs 50% more V memory: fall back to in-register sums if it does not fit
+        size_t free_b = 0, total_b = 0;
+        DeviceScope ds0(h->device);
+        cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+        const double need = 2.0 * 3.0 * 8.0 * static_cast<double>(M) * static_cast<double>(N);
+        if (need > 0.9 * static_cast<double>(free_b)) p->tile = qsb::kTileWs3M;
+    }
+    p->planes = p->small ? 2 : qsb::gemm_tile_planes(p->tile);
 
     DeviceScope ds(h->device);
     if (borrow_cache) {
@@ -501,8 +512,8 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, const qsb_circuit* c, int64_t
         p->borrowed = true;
     }
     const size_t plane_bytes = static_cast<size_t>(M) * N * 8;
-    p->b.v[0].ensure(2 * plane_bytes);
-    if (!p->small && p->chain.size() > 1) p->b.v[1].ensure(2 * plane_bytes);
+    p->b.v[0].ensure(p->planes * plane_bytes);
+    if (!p->small && p->chain.size() > 1) p->b.v[1].ensure(p->planes * plane_bytes);
     p->b.psi.ensure(2 * static_cast<size_t>(M) * 8);
     p->b.x.ensure(2 * static_cast<size_t>(N) * 8);
     upload_tables(p.get(), c);
@@ -522,8 +533,8 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, const qsb_circuit* c, int64_t
                    "upload layers");
     } else {
         const int rows = qsb::gemm_tile_rows(p->tile);
-        p->tmap[0] = make_tmap(p->b.v[0].p, p->M, p->N, rows);
-        if (p->b.v[1].p) p->tmap[1] = make_tmap(p->b.v[1].p, p->M, p->N, rows);
+        p->tmap[0] = make_tmap(p->b.v[0].p, p->M, p->N, rows, p->planes);
+        if (p->b.v[1].p) p->tmap[1] = make_tmap(p->b.v[1].p, p->M, p->N, rows, p->planes);
     }
     const int gemms = p->small ? static_cast<int>(p->chain.size()) - 1 : static_cast<int>(p->chain.size()) - 1;
     qsb_plan_info& in = p->info;
@@ -536,7 +547,7 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, const qsb_circuit* c, int64_t
     in.row_begin = row_begin;
     in.row_count = row_count;
     in.gemm_flops = 8.0 * static_cast<double>(p->M) * static_cast<double>(N) * static_cast<double>(N) * gemms;
-    in.expand_bytes = p->small ? 0.0 : 16.0 * static_cast<double>(p->M) * static_cast<double>(N);
+    in.expand_bytes = p->small ? 0.0 : 8.0 * p->planes * static_cast<double>(p->M) * static_cast<double>(N);
     return p;
 }
 
@@ -562,7 +573,8 @@ void enqueue(qsb_plan* p, cudaStream_t s) {
     }
     const bool ev = p->timing && p->timed_run;
     if (ev) cuda_check(cudaEventRecord(p->ev[0], s), "event");
-    cuda_check(qsb::launch_expand(p->chain[0], rb, p->M, p->N, p->b.v[0].as<double>(), s), "expand_kernel");
+    cuda_check(qsb::launch_expand(p->chain[0], rb, p->M, p->N, p->b.v[0].as<double>(), p->planes, s),
+               "expand_kernel");
     if (ev) cuda_check(cudaEventRecord(p->ev[1], s), "event");
     int cur = 0;
     for (size_t i = 1; i < p->chain.size(); ++i) {
@@ -797,7 +809,7 @@ qsb_status qsb_layer_operator(qsb_handle* h, const qsb_circuit* c, int32_t step,
             upload_tables(&tmp, c);
             tmp.b.v[0].ensure(2 * N * N * 8);
             cuda_check(qsb::launch_expand(tmp.cc.app[idx], 0, static_cast<int>(N), static_cast<int>(N),
-                                          tmp.b.v[0].as<double>(), h->stream),
+                                          tmp.b.v[0].as<double>(), 2, h->stream),
                        "expand_kernel");
             cuda_check(cudaMemcpyAsync(re, tmp.b.v[0].p, N * N * 8, cudaMemcpyDeviceToHost, h->stream), "download");
             cuda_check(cudaMemcpyAsync(im, tmp.b.v[0].as<double>() + N * N, N * N * 8, cudaMemcpyDeviceToHost,
