@@ -111,10 +111,13 @@ typedef struct qsb_circuit {
 enum { QSB_GEMM_AUTO = 0, QSB_GEMM_4M = 1, QSB_GEMM_3M = 2 };
 
 typedef struct qsb_options {
-    int32_t device;       /* CUDA device ordinal */
+    int32_t device;       /* CUDA device ordinal (used when n_devices == 0) */
     int32_t qubit_guard;  /* 0 = derive from HBM capacity (simulator.hpp:53-56 override otherwise) */
     int32_t gemm_mode;    /* QSB_GEMM_* */
     int32_t flags;        /* QSB_FLAG_* */
+    int32_t n_devices;    /* > 1: the host-API calls shard U by row blocks over these devices */
+    int32_t reserved;
+    const int32_t* devices; /* n_devices ordinals (repeats allowed: virtual shards on one GPU) */
 } qsb_options;
 
 enum {
@@ -152,7 +155,9 @@ qsb_status qsb_destroy(qsb_handle* handle);
 qsb_status qsb_qubit_guard(const qsb_handle* handle, int32_t* guard);
 
 /* Algorithm 1: psi = U |0...0>, written to host planes of length 2^n.
- * Host in, host out; thread-safe on one handle (internally serialised). */
+ * Host in, host out; thread-safe on one handle (internally serialised). With
+ * n_devices > 1 every device computes its row block of U with no
+ * communication and writes its psi rows straight into the host planes. */
 qsb_status qsb_simulate_full_state(qsb_handle* handle, const qsb_circuit* circuit,
                                    double* psi_re, double* psi_im);
 

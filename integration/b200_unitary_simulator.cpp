@@ -2,8 +2,10 @@
 // qsb_status back onto the qsim::Error hierarchy (errors.hpp:23-56).
 #include "b200_unitary_simulator.hpp"
 
+#include <cstdlib>
 #include <map>
 #include <memory>
+#include <sstream>
 #include <variant>
 #include <vector>
 
@@ -99,8 +101,10 @@ std::unique_ptr<Flat> flatten(const Circuit& circuit, const GateRegistry& regist
 
 }  // namespace
 
-B200UnitarySimulator::B200UnitarySimulator(std::size_t qubit_guard, int device) {
-    qsb_options o{device, static_cast<int32_t>(qubit_guard), QSB_GEMM_AUTO, 0};
+B200UnitarySimulator::B200UnitarySimulator(std::size_t qubit_guard, std::vector<int> devices) {
+    std::vector<int32_t> ids(devices.begin(), devices.end());
+    qsb_options o{ids.empty() ? 0 : ids[0], static_cast<int32_t>(qubit_guard), QSB_GEMM_AUTO, 0,
+                  static_cast<int32_t>(ids.size()), 0, ids.data()};
     check(qsb_create(&o, &handle_));
     int32_t g = 0;
     check(qsb_qubit_guard(handle_, &g));
@@ -132,9 +136,32 @@ ComplexMatrix B200UnitarySimulator::circuit_unitary(const Circuit& circuit, cons
     return u;
 }
 
+namespace {
+std::vector<int> devices_from_env() {
+    const char* env = std::getenv("QSB_DEVICES");
+    std::vector<int> ids;
+    if (!env || !*env) return {0};
+    if (std::string(env) == "all") {
+        // one row block per visible device, probed through the library
+        for (int d = 0; d < 64; ++d) {
+            qsb_options o{d, 0, QSB_GEMM_AUTO, 0, 0, 0, nullptr};
+            qsb_handle* h = nullptr;
+            if (qsb_create(&o, &h) != QSB_OK) break;
+            qsb_destroy(h);
+            ids.push_back(d);
+        }
+        return ids.empty() ? std::vector<int>{0} : ids;
+    }
+    std::stringstream ss(env);
+    std::string tok;
+    while (std::getline(ss, tok, ',')) ids.push_back(std::stoi(tok));
+    return ids.empty() ? std::vector<int>{0} : ids;
+}
+}  // namespace
+
 void register_b200_backend() {
     register_backend("unitary-b200", [](const SimulatorOptions& o) -> std::unique_ptr<Simulator> {
-        return std::make_unique<B200UnitarySimulator>(o.qubit_guard.value_or(0));
+        return std::make_unique<B200UnitarySimulator>(o.qubit_guard.value_or(0), devices_from_env());
     });
 }
 

@@ -11,6 +11,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "qsb.h"
 #include "qsim/simulator.hpp"
@@ -19,8 +20,10 @@ namespace qsim {
 
 class B200UnitarySimulator final : public Simulator {
 public:
-    /// qubit_guard 0 = derived from HBM capacity (n <= 16 on one B200).
-    explicit B200UnitarySimulator(std::size_t qubit_guard = 0, int device = 0);
+    /// qubit_guard 0 = derived from HBM capacity (n <= 16 on one B200, 17 on 4-8).
+    /// devices: more than one shards U by row blocks over them (no communication
+    /// during the product chain; each device writes its psi rows to the result).
+    explicit B200UnitarySimulator(std::size_t qubit_guard = 0, std::vector<int> devices = {0});
     ~B200UnitarySimulator() override;
     B200UnitarySimulator(const B200UnitarySimulator&) = delete;
     B200UnitarySimulator& operator=(const B200UnitarySimulator&) = delete;
@@ -44,7 +47,8 @@ private:
     std::size_t guard_ = 0;
 };
 
-/// register_backend("unitary-b200", ...) honouring SimulatorOptions::qubit_guard.
+/// register_backend("unitary-b200", ...) honouring SimulatorOptions::qubit_guard;
+/// the device list comes from QSB_DEVICES ("0,1,2,3", or "all"; default "0").
 void register_b200_backend();
 
 }  // namespace qsim

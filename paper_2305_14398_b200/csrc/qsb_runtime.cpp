@@ -374,18 +374,25 @@ qsb::LayerDesc identity_layer(int n) {
 
 // ------------------------------------------------------------------ handle
 
-struct qsb_handle {
+// One CUDA device (or one virtual shard on it) driven by a handle.
+struct DeviceCtx {
     int device = 0;
+    cudaStream_t stream = nullptr;
+    Buffers cache;  // reused by the host-API calls
+};
+
+struct qsb_handle {
     int guard = 0;
     int gemm_mode = QSB_GEMM_AUTO;
     int flags = 0;
-    cudaStream_t stream = nullptr;
+    std::vector<std::unique_ptr<DeviceCtx>> devs;
     std::mutex mu;
-    Buffers cache;
+    DeviceCtx& dev0() { return *devs.front(); }
 };
 
 struct qsb_plan {
     qsb_handle* h = nullptr;
+    DeviceCtx* dc = nullptr;
     Compiled cc;
     std::vector<qsb::LayerDesc> chain;  // row-form order: chain[0] expanded, chain[1..] multiplied
     int n_identity = 0;
@@ -456,12 +463,13 @@ int pick_tile(int M, int N, int gemm_mode) {
 }
 
 // Build a plan; the caller holds the handle mutex when borrow_cache is set.
-std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, const qsb_circuit* c, int64_t row_begin, int64_t row_count,
-                                    bool borrow_cache) {
+std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circuit* c, int64_t row_begin,
+                                    int64_t row_count, bool borrow_cache) {
     validate_circuit_shape(c);
     check_guard(c, h->guard);
     auto p = std::make_unique<qsb_plan>();
     p->h = h;
+    p->dc = dc;
     p->cc = compile(c);
     const int n = c->n_qubits;
     const int64_t N = int64_t{1} << n;
@@ -499,16 +507,16 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, const qsb_circuit* c, int64_t
     if (p->tile == qsb::kTileWs3MS) {
         // the sum plane costs 50% more V memory: fall back to in-register sums if it does not fit
         size_t free_b = 0, total_b = 0;
-        DeviceScope ds0(h->device);
+        DeviceScope ds0(dc->device);
         cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
         const double need = 2.0 * 3.0 * 8.0 * static_cast<double>(M) * static_cast<double>(N);
         if (need > 0.9 * static_cast<double>(free_b)) p->tile = qsb::kTileWs3M;
     }
     p->planes = p->small ? 2 : qsb::gemm_tile_planes(p->tile);
 
-    DeviceScope ds(h->device);
+    DeviceScope ds(dc->device);
     if (borrow_cache) {
-        p->b = std::move(h->cache);
+        p->b = std::move(dc->cache);
         p->borrowed = true;
     }
     const size_t plane_bytes = static_cast<size_t>(M) * N * 8;
@@ -553,11 +561,11 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, const qsb_circuit* c, int64_t
 
 void release_plan(std::unique_ptr<qsb_plan>& p) {
     if (!p) return;
-    DeviceScope ds(p->h->device);
+    DeviceScope ds(p->dc->device);
     if (p->graph) cudaGraphExecDestroy(p->graph);
     for (auto& e : p->ev)
         if (e) cudaEventDestroy(e);
-    if (p->borrowed) p->h->cache = std::move(p->b);
+    if (p->borrowed) p->dc->cache = std::move(p->b);
     p.reset();
 }
 
@@ -590,7 +598,7 @@ void enqueue(qsb_plan* p, cudaStream_t s) {
 }
 
 void execute(qsb_plan* p, cudaStream_t s, bool allow_graph) {
-    DeviceScope ds(p->h->device);
+    DeviceScope ds(p->dc->device);
     const bool use_graph = allow_graph && !p->timing && !(p->h->flags & QSB_FLAG_NO_GRAPH);
     p->timed_run = p->timing;
     if (p->timing) {
@@ -640,7 +648,7 @@ qsb_status qsb_create(const qsb_options* options, qsb_handle** out) {
     return guarded([&] {
         if (!out) raise(QSB_ERR_ARGUMENT, "out is null");
         *out = nullptr;
-        qsb_options o{0, 0, QSB_GEMM_AUTO, 0};
+        qsb_options o{0, 0, QSB_GEMM_AUTO, 0, 0, 0, nullptr};
         if (options) o = *options;
         int count = 0;
         cudaError_t e = cudaGetDeviceCount(&count);
@@ -648,23 +656,42 @@ qsb_status qsb_create(const qsb_options* options, qsb_handle** out) {
             cudaGetLastError();
             raise(QSB_ERR_CUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
         }
-        if (o.device < 0 || o.device >= count) raise(QSB_ERR_ARGUMENT, "device %d out of range", o.device);
+        std::vector<int> ids;
+        if (o.n_devices > 0) {
+            if (!o.devices) raise(QSB_ERR_ARGUMENT, "n_devices > 0 but devices is null");
+            ids.assign(o.devices, o.devices + o.n_devices);
+        } else {
+            ids.push_back(o.device);
+        }
         auto h = std::make_unique<qsb_handle>();
-        h->device = o.device;
         h->gemm_mode = o.gemm_mode;
         h->flags = o.flags;
-        DeviceScope ds(o.device);
-        cudaDeviceProp prop;
-        cuda_check(cudaGetDeviceProperties(&prop, o.device), "cudaGetDeviceProperties");
-        if (prop.major < 10)
-            raise(QSB_ERR_CUDA, "device %d (%s, sm_%d%d) is not sm_100a", o.device, prop.name, prop.major, prop.minor);
-        cuda_check(qsb::configure_kernels(), "configure kernels");
-        // HBM-derived default guard: both V buffers must fit in 92% of device memory.
+        double min_mem = 0.0;
+        for (int id : ids) {
+            if (id < 0 || id >= count) raise(QSB_ERR_ARGUMENT, "device %d out of range", id);
+            DeviceScope ds(id);
+            cudaDeviceProp prop;
+            cuda_check(cudaGetDeviceProperties(&prop, id), "cudaGetDeviceProperties");
+            if (prop.major < 10)
+                raise(QSB_ERR_CUDA, "device %d (%s, sm_%d%d) is not sm_100a", id, prop.name, prop.major, prop.minor);
+            cuda_check(qsb::configure_kernels(), "configure kernels");
+            const double mem = static_cast<double>(prop.totalGlobalMem);
+            min_mem = (min_mem == 0.0) ? mem : std::min(min_mem, mem);
+            auto dc = std::make_unique<DeviceCtx>();
+            dc->device = id;
+            cuda_check(cudaStreamCreateWithFlags(&dc->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            h->devs.push_back(std::move(dc));
+        }
+        // HBM-derived default guard: each device's row block of both V buffers
+        // must fit in 92% of its memory (distinct devices share the rows).
+        std::vector<int> distinct(ids);
+        std::sort(distinct.begin(), distinct.end());
+        distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
+        const double share = static_cast<double>(distinct.size());
         int hbm_guard = 1;
         for (int n = 1; n <= qsb::kMaxQubits; ++n)
-            if (static_cast<double>(engine_bytes(n)) <= 0.92 * static_cast<double>(prop.totalGlobalMem)) hbm_guard = n;
+            if (static_cast<double>(engine_bytes(n)) / share <= 0.92 * min_mem) hbm_guard = n;
         h->guard = o.qubit_guard > 0 ? std::min(o.qubit_guard, qsb::kMaxQubits) : hbm_guard;
-        cuda_check(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
         *out = h.release();
     });
 }
@@ -673,10 +700,12 @@ qsb_status qsb_destroy(qsb_handle* h) {
     return guarded([&] {
         if (!h) return;
         {
-            DeviceScope ds(h->device);
             std::lock_guard<std::mutex> lk(h->mu);
-            if (h->stream) cudaStreamDestroy(h->stream);
-            h->cache = Buffers{};
+            for (auto& dc : h->devs) {
+                DeviceScope ds(dc->device);
+                if (dc->stream) cudaStreamDestroy(dc->stream);
+                dc->cache = Buffers{};
+            }
         }
         delete h;
     });
@@ -689,37 +718,65 @@ qsb_status qsb_qubit_guard(const qsb_handle* h, int32_t* guard) {
     });
 }
 
+// Host-API execution: the row blocks of U over the handle's devices (one block
+// when the handle has a single device), each computed with no communication;
+// psi rows and U rows land directly at their offsets in the host planes.
 static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re, const double* psi0_im,
                      double* psi_re, double* psi_im, double* u_re, double* u_im) {
     std::lock_guard<std::mutex> lk(h->mu);
     validate_circuit_shape(c);
-    std::unique_ptr<qsb_plan> p;
+    check_guard(c, h->guard);
+    const int64_t N = int64_t{1} << c->n_qubits;
+    // equal power-of-two row blocks of at least 32 rows (the one-CTA path takes N <= 32 whole)
+    int G = static_cast<int>(h->devs.size());
+    while (G > 1 && (N / G < 32 || N % G != 0)) --G;
+    if (G > 1 && (G & (G - 1)) != 0) {
+        int p2 = 1;
+        while (p2 * 2 <= G) p2 *= 2;
+        G = p2;
+    }
+    const int64_t rows = N / G;
+    std::vector<std::unique_ptr<qsb_plan>> plans(G);
+    auto release_all = [&] {
+        for (auto& p : plans) release_plan(p);
+    };
     try {
-        p = make_plan(h, c, 0, int64_t{1} << c->n_qubits, true);
-        DeviceScope ds(h->device);
-        const size_t N = static_cast<size_t>(p->N);
-        if (psi0_re) {
-            cuda_check(cudaMemcpyAsync(p->b.x.p, psi0_re, N * 8, cudaMemcpyHostToDevice, h->stream), "upload psi0");
-            cuda_check(cudaMemcpyAsync(p->b.x.as<double>() + N, psi0_im, N * 8, cudaMemcpyHostToDevice, h->stream),
-                       "upload psi0");
+        for (int g = 0; g < G; ++g) plans[g] = make_plan(h, h->devs[g].get(), c, g * rows, rows, true);
+        for (int g = 0; g < G; ++g) {
+            qsb_plan* p = plans[g].get();
+            DeviceScope ds(p->dc->device);
+            cudaStream_t s = p->dc->stream;
+            if (psi0_re) {
+                cuda_check(cudaMemcpyAsync(p->b.x.p, psi0_re, N * 8, cudaMemcpyHostToDevice, s), "upload psi0");
+                cuda_check(cudaMemcpyAsync(p->b.x.as<double>() + N, psi0_im, N * 8, cudaMemcpyHostToDevice, s),
+                           "upload psi0");
+            }
+            execute(p, s, false);
+            const int64_t off = p->row_begin - p->eff_begin;
+            if (psi_re) {
+                cuda_check(cudaMemcpyAsync(psi_re + p->row_begin, p->b.psi.as<double>() + off, rows * 8,
+                                           cudaMemcpyDeviceToHost, s), "download psi");
+                cuda_check(cudaMemcpyAsync(psi_im + p->row_begin, p->b.psi.as<double>() + p->M + off, rows * 8,
+                                           cudaMemcpyDeviceToHost, s), "download psi");
+            }
+            if (u_re) {
+                const double* v = p->b.v[p->final_buf].as<double>();
+                const size_t plane = static_cast<size_t>(p->M) * N;
+                cuda_check(cudaMemcpyAsync(u_re + p->row_begin * N, v + off * N, rows * N * 8,
+                                           cudaMemcpyDeviceToHost, s), "download U");
+                cuda_check(cudaMemcpyAsync(u_im + p->row_begin * N, v + plane + off * N, rows * N * 8,
+                                           cudaMemcpyDeviceToHost, s), "download U");
+            }
         }
-        execute(p.get(), h->stream, false);
-        if (psi_re) {
-            cuda_check(cudaMemcpyAsync(psi_re, p->b.psi.p, N * 8, cudaMemcpyDeviceToHost, h->stream), "download psi");
-            cuda_check(cudaMemcpyAsync(psi_im, p->b.psi.as<double>() + N, N * 8, cudaMemcpyDeviceToHost, h->stream),
-                       "download psi");
+        for (int g = 0; g < G; ++g) {
+            DeviceScope ds(plans[g]->dc->device);
+            cuda_check(cudaStreamSynchronize(plans[g]->dc->stream), "cudaStreamSynchronize");
         }
-        if (u_re) {
-            const double* v = p->b.v[p->final_buf].as<double>();
-            cuda_check(cudaMemcpyAsync(u_re, v, N * N * 8, cudaMemcpyDeviceToHost, h->stream), "download U");
-            cuda_check(cudaMemcpyAsync(u_im, v + N * N, N * N * 8, cudaMemcpyDeviceToHost, h->stream), "download U");
-        }
-        cuda_check(cudaStreamSynchronize(h->stream), "cudaStreamSynchronize");
     } catch (...) {
-        release_plan(p);
+        release_all();
         throw;
     }
-    release_plan(p);
+    release_all();
 }
 
 qsb_status qsb_simulate_full_state(qsb_handle* h, const qsb_circuit* c, double* psi_re, double* psi_im) {
@@ -799,28 +856,30 @@ qsb_status qsb_layer_operator(qsb_handle* h, const qsb_circuit* c, int32_t step,
         for (size_t i = 0; i < cc.app.size(); ++i)
             if (cc.app_step[i] == step && cc.app_index[i] == layer) idx = static_cast<int>(i);
         if (idx < 0) raise(QSB_ERR_ARGUMENT, "layer %d out of range for step %d", layer, step);
-        DeviceScope ds(h->device);
+        DeviceCtx& dc = h->dev0();
+        DeviceScope ds(dc.device);
         const size_t N = size_t{1} << c->n_qubits;
         qsb_plan tmp;  // for table upload
         tmp.h = h;
+        tmp.dc = &dc;
         tmp.cc = std::move(cc);
-        tmp.b = std::move(h->cache);
+        tmp.b = std::move(dc.cache);
         try {
             upload_tables(&tmp, c);
             tmp.b.v[0].ensure(2 * N * N * 8);
             cuda_check(qsb::launch_expand(tmp.cc.app[idx], 0, static_cast<int>(N), static_cast<int>(N),
-                                          tmp.b.v[0].as<double>(), 2, h->stream),
+                                          tmp.b.v[0].as<double>(), 2, dc.stream),
                        "expand_kernel");
-            cuda_check(cudaMemcpyAsync(re, tmp.b.v[0].p, N * N * 8, cudaMemcpyDeviceToHost, h->stream), "download");
+            cuda_check(cudaMemcpyAsync(re, tmp.b.v[0].p, N * N * 8, cudaMemcpyDeviceToHost, dc.stream), "download");
             cuda_check(cudaMemcpyAsync(im, tmp.b.v[0].as<double>() + N * N, N * N * 8, cudaMemcpyDeviceToHost,
-                                       h->stream),
+                                       dc.stream),
                        "download");
-            cuda_check(cudaStreamSynchronize(h->stream), "cudaStreamSynchronize");
+            cuda_check(cudaStreamSynchronize(dc.stream), "cudaStreamSynchronize");
         } catch (...) {
-            h->cache = std::move(tmp.b);
+            dc.cache = std::move(tmp.b);
             throw;
         }
-        h->cache = std::move(tmp.b);
+        dc.cache = std::move(tmp.b);
     });
 }
 
@@ -829,21 +888,22 @@ qsb_status qsb_probabilities(qsb_handle* h, const double* psi_re, const double* 
     return guarded([&] {
         if (!h || !psi_re || !psi_im || !p || !norm_squared || dim < 1) raise(QSB_ERR_ARGUMENT, "bad argument");
         std::lock_guard<std::mutex> lk(h->mu);
-        DeviceScope ds(h->device);
-        Buffers& b = h->cache;
+        DeviceCtx& dc = h->dev0();
+        DeviceScope ds(dc.device);
+        Buffers& b = dc.cache;
         const int cap = 4096;
         b.psi.ensure(2 * static_cast<size_t>(dim) * 8);
         b.p.ensure(static_cast<size_t>(dim) * 8);
         b.partial.ensure((cap + 1) * 8);
         double* psi = b.psi.as<double>();
-        cuda_check(cudaMemcpyAsync(psi, psi_re, dim * 8, cudaMemcpyHostToDevice, h->stream), "upload");
-        cuda_check(cudaMemcpyAsync(psi + dim, psi_im, dim * 8, cudaMemcpyHostToDevice, h->stream), "upload");
+        cuda_check(cudaMemcpyAsync(psi, psi_re, dim * 8, cudaMemcpyHostToDevice, dc.stream), "upload");
+        cuda_check(cudaMemcpyAsync(psi + dim, psi_im, dim * 8, cudaMemcpyHostToDevice, dc.stream), "upload");
         double* partial = b.partial.as<double>();
-        cuda_check(qsb::launch_probabilities(psi, dim, b.p.as<double>(), partial, cap, partial + cap, h->stream),
+        cuda_check(qsb::launch_probabilities(psi, dim, b.p.as<double>(), partial, cap, partial + cap, dc.stream),
                    "probs_kernel");
-        cuda_check(cudaMemcpyAsync(p, b.p.p, dim * 8, cudaMemcpyDeviceToHost, h->stream), "download");
-        cuda_check(cudaMemcpyAsync(norm_squared, partial + cap, 8, cudaMemcpyDeviceToHost, h->stream), "download");
-        cuda_check(cudaStreamSynchronize(h->stream), "cudaStreamSynchronize");
+        cuda_check(cudaMemcpyAsync(p, b.p.p, dim * 8, cudaMemcpyDeviceToHost, dc.stream), "download");
+        cuda_check(cudaMemcpyAsync(norm_squared, partial + cap, 8, cudaMemcpyDeviceToHost, dc.stream), "download");
+        cuda_check(cudaStreamSynchronize(dc.stream), "cudaStreamSynchronize");
     });
 }
 
@@ -852,7 +912,7 @@ qsb_status qsb_plan_create(qsb_handle* h, const qsb_circuit* c, int64_t row_begi
     return guarded([&] {
         if (!h || !out) raise(QSB_ERR_ARGUMENT, "null argument");
         *out = nullptr;
-        std::unique_ptr<qsb_plan> p = make_plan(h, c, row_begin, row_count, false);
+        std::unique_ptr<qsb_plan> p = make_plan(h, &h->dev0(), c, row_begin, row_count, false);
         *out = p.release();
     });
 }
@@ -881,7 +941,7 @@ qsb_status qsb_plan_set_timing(qsb_plan* plan, int32_t enable) {
 qsb_status qsb_plan_execute(qsb_plan* plan, void* stream) {
     return guarded([&] {
         if (!plan) raise(QSB_ERR_ARGUMENT, "null argument");
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->h->stream;
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->dc->stream;
         execute(plan, s, true);
     });
 }
@@ -889,8 +949,8 @@ qsb_status qsb_plan_execute(qsb_plan* plan, void* stream) {
 qsb_status qsb_plan_set_initial_state(qsb_plan* plan, const double* re, const double* im, void* stream) {
     return guarded([&] {
         if (!plan || !re || !im) raise(QSB_ERR_ARGUMENT, "null argument");
-        DeviceScope ds(plan->h->device);
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->h->stream;
+        DeviceScope ds(plan->dc->device);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->dc->stream;
         const size_t N = static_cast<size_t>(plan->N);
         cuda_check(cudaMemcpyAsync(plan->b.x.p, re, N * 8, cudaMemcpyDefault, s), "copy psi0");
         cuda_check(cudaMemcpyAsync(plan->b.x.as<double>() + N, im, N * 8, cudaMemcpyDefault, s), "copy psi0");
@@ -919,8 +979,8 @@ qsb_status qsb_plan_state_device(const qsb_plan* plan, const double** re, const 
 qsb_status qsb_plan_copy_state(const qsb_plan* plan, double* dst_re, double* dst_im, void* stream) {
     return guarded([&] {
         if (!plan || !dst_re || !dst_im) raise(QSB_ERR_ARGUMENT, "null argument");
-        DeviceScope ds(plan->h->device);
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->h->stream;
+        DeviceScope ds(plan->dc->device);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->dc->stream;
         const size_t bytes = static_cast<size_t>(plan->row_count) * 8;
         cuda_check(cudaMemcpyAsync(dst_re, psi_rows(plan), bytes, cudaMemcpyDefault, s), "copy psi");
         cuda_check(cudaMemcpyAsync(dst_im, psi_rows(plan) + plan->M, bytes, cudaMemcpyDefault, s), "copy psi");
@@ -932,7 +992,7 @@ qsb_status qsb_plan_last_timing(qsb_plan* plan, double* total_ms, double* gemm_m
         if (!plan || !total_ms || !gemm_ms || !gemm_mean_ms) raise(QSB_ERR_ARGUMENT, "null argument");
         if (!plan->timing || !plan->timed_run || !plan->ev[0] || plan->small)
             raise(QSB_ERR_ARGUMENT, "no timed execute on this plan (qsb_plan_set_timing, tiled path only)");
-        DeviceScope ds(plan->h->device);
+        DeviceScope ds(plan->dc->device);
         cuda_check(cudaEventSynchronize(plan->ev[3]), "cudaEventSynchronize");
         float t = 0, g = 0;
         cuda_check(cudaEventElapsedTime(&t, plan->ev[0], plan->ev[3]), "cudaEventElapsedTime");

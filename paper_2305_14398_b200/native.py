@@ -46,7 +46,9 @@ class QsbCircuit(ctypes.Structure):
 
 class QsbOptions(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("qubit_guard", ctypes.c_int32),
-                ("gemm_mode", ctypes.c_int32), ("flags", ctypes.c_int32)]
+                ("gemm_mode", ctypes.c_int32), ("flags", ctypes.c_int32),
+                ("n_devices", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("devices", ctypes.c_void_p)]
 
 
 class QsbPlanInfo(ctypes.Structure):

@@ -127,9 +127,14 @@ class B200UnitarySimulator(Simulator):
     """The drop-in backend: Algorithm 1 on B200 (unitary_backend.cpp:194-215)."""
 
     def __init__(self, qubit_guard: Optional[int] = None, device: int = 0,
-                 gemm_mode: int = native.GEMM_AUTO, flags: int = 0) -> None:
+                 gemm_mode: int = native.GEMM_AUTO, flags: int = 0, devices: Optional[List[int]] = None) -> None:
         L = native.lib()
-        opts = native.QsbOptions(device, int(qubit_guard or 0), gemm_mode, flags)
+        self._devices = None
+        dev_ptr, n_dev = None, 0
+        if devices:
+            self._devices = (ctypes.c_int32 * len(devices))(*devices)
+            dev_ptr, n_dev = ctypes.cast(self._devices, ctypes.c_void_p).value, len(devices)
+        opts = native.QsbOptions(device, int(qubit_guard or 0), gemm_mode, flags, n_dev, 0, dev_ptr)
         self._h = ctypes.c_void_p()
         native.check(L.qsb_create(ctypes.byref(opts), ctypes.byref(self._h)))
         g = ctypes.c_int32()

@@ -179,6 +179,7 @@ def test_no_cpu_fallback_without_gpu():
 def test_abi_struct_layout():
     assert native.OP_DTYPE.itemsize == 104
     assert ctypes.sizeof(native.QsbCircuit) == 40
+    assert ctypes.sizeof(native.QsbOptions) == 32
     assert ctypes.sizeof(native.QsbFunction) == 24
     assert ctypes.sizeof(native.QsbPlanInfo) == 56
 
