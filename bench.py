@@ -336,7 +336,7 @@ def run_ours(args):
                        "l2": ("inputs larger than L2" if flush is None else "L2 flushed between steps")},
             "tflops": job_tflops,
             "fp64_peak_frac": job_tflops / (FP64_DMMA_PEAK_TFLOPS * world),
-            "roofline": {"bound": "tensor", "kernel": "zgemm_gen_kernel (K2)",
+            "roofline": {"bound": "tensor", "kernel": (native.TILE_NAMES.get(info.gemm_tile, "small_circuit_kernel") + " (K2)") if info else None,
                          "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": (achieved / FP64_DMMA_PEAK_TFLOPS) if achieved else None,
                          "traffic": traffic,

@@ -141,7 +141,13 @@ typedef struct qsb_plan_info {
     int64_t row_count;
     double gemm_flops;         /* 8 * row_count * N^2 per GEMM, summed */
     double expand_bytes;       /* bytes written by the K1 expansion */
+    int32_t gemm_tile;         /* K2 variant: QSB_TILE_* */
+    int32_t v_planes;          /* planes per V buffer (2, or 3 with the 3M sum plane) */
 } qsb_plan_info;
+
+/* K2 variants reported in qsb_plan_info.gemm_tile. */
+enum { QSB_TILE_128x64 = 0, QSB_TILE_64x64 = 1, QSB_TILE_32x32 = 2, QSB_TILE_WS4M = 3, QSB_TILE_WS3M = 4,
+       QSB_TILE_WS3M_SUMPLANE = 5 };
 
 int qsb_abi_version(void);
 

@@ -556,6 +556,8 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     in.row_count = row_count;
     in.gemm_flops = 8.0 * static_cast<double>(p->M) * static_cast<double>(N) * static_cast<double>(N) * gemms;
     in.expand_bytes = p->small ? 0.0 : 8.0 * p->planes * static_cast<double>(p->M) * static_cast<double>(N);
+    in.gemm_tile = p->small ? -1 : p->tile;
+    in.v_planes = p->planes;
     return p;
 }
 

@@ -30,6 +30,8 @@ assert OP_DTYPE.itemsize == 104
 OP_GATE, OP_CONTROL, OP_FUNCTION, OP_INSTRUCTION = 0, 1, 2, 3
 GEMM_AUTO, GEMM_4M, GEMM_3M = 0, 1, 2
 FLAG_NO_GRAPH, FLAG_MATERIALIZE = 1, 2
+TILE_NAMES = {0: "zgemm_gen_kernel<128,64> (4M)", 1: "zgemm_gen_kernel<64,64> (4M)", 2: "zgemm_gen_kernel<32,32> (4M)",
+              3: "zgemm_ws_kernel<4M>", 4: "zgemm_ws_kernel<3M>", 5: "zgemm_ws_kernel<3M, sum plane>"}
 
 
 class QsbFunction(ctypes.Structure):
@@ -57,6 +59,7 @@ class QsbPlanInfo(ctypes.Structure):
         ("n_gemms", ctypes.c_int32), ("n_identity_layers", ctypes.c_int32), ("n_launches", ctypes.c_int32),
         ("row_begin", ctypes.c_int64), ("row_count", ctypes.c_int64),
         ("gemm_flops", ctypes.c_double), ("expand_bytes", ctypes.c_double),
+        ("gemm_tile", ctypes.c_int32), ("v_planes", ctypes.c_int32),
     ]
 
 
