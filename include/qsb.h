@@ -180,6 +180,11 @@ qsb_status qsb_build_unitary(qsb_handle* handle, const qsb_circuit* circuit,
 qsb_status qsb_simulate_and_collapse(qsb_handle* handle, const qsb_circuit* circuit,
                                      uint64_t seed, uint64_t* basis_index);
 
+/* collapse (state.cpp:81-98) of a host state: K4 probabilities on the GPU, then the
+ * reference's sequential inverse-CDF walk with one SplitMix64(seed) draw on the host. */
+qsb_status qsb_collapse(qsb_handle* handle, const double* psi_re, const double* psi_im, int64_t dim,
+                        uint64_t seed, uint64_t* basis_index);
+
 /* Number of layers step `step` factors into (first-fit, unitary_backend.cpp:63-91). */
 qsb_status qsb_step_layer_count(const qsb_circuit* circuit, int32_t step, int32_t* layers);
 
@@ -225,6 +230,71 @@ qsb_status qsb_plan_copy_state(const qsb_plan* plan, double* dst_re, double* dst
  * total, the K2 GEMM chain, and the mean single-GEMM duration (ms). Synchronises. */
 qsb_status qsb_plan_last_timing(qsb_plan* plan, double* total_ms, double* gemm_ms,
                                 double* gemm_mean_ms);
+
+/* ---- state-vector engine: the fsv backend and the structured unitary ----
+ *
+ * One engine evolves a [2][2^n][W] split-plane array by the reference's
+ * full-state-vector operations (fsv_backend.cpp:40-158) in circuit order:
+ * W = 1 is FsvSimulator (one state), W = 2^n columns is the structured unitary
+ * U[:, c] = fsv(e_c) — the same U as the dense path, built with HBM-bound pair
+ * updates instead of dense GEMMs (a different algorithm, reported separately
+ * and never counted against the FP64 tensor roofline). Results are bit-exact
+ * with the reference's fsv backend (up to the sign of zeros). */
+enum { QSB_SV_STATE = 0, QSB_SV_UNITARY = 1 };
+
+typedef struct qsb_sv_plan qsb_sv_plan;
+
+typedef struct qsb_sv_plan_info {
+    int32_t n_qubits;
+    int32_t mode;              /* QSB_SV_* */
+    int32_t n_ops;             /* operations applied (instructions excluded) */
+    int32_t n_passes;          /* launches over the whole array (batches + large functions) */
+    int32_t n_function_passes; /* apply_function blocks too large for a shared-memory slab */
+    int32_t n_launches;        /* kernels per execute, including initialisation */
+    int32_t slab_bits;         /* log2 elements staged per CTA */
+    int32_t max_batch_targets; /* most target bits in one batch */
+    int64_t col_begin;         /* QSB_SV_UNITARY: first column of U computed */
+    int64_t col_count;         /* QSB_SV_UNITARY: columns (power of two); QSB_SV_STATE: 1 */
+    double bytes_per_run;      /* HBM bytes read + written by the passes of one execute */
+} qsb_sv_plan_info;
+
+/* FsvSimulator::qubit_guard (fsv_backend.hpp:47-51): options.qubit_guard, else HBM-derived. */
+qsb_status qsb_fsv_qubit_guard(const qsb_handle* handle, int32_t* guard);
+
+/* FsvSimulator::simulate_full_state (fsv_backend.cpp:135-158): psi = ops |0...0>. */
+qsb_status qsb_fsv_simulate_full_state(qsb_handle* handle, const qsb_circuit* circuit,
+                                       double* psi_re, double* psi_im);
+
+/* Same from an arbitrary state psi0 (host planes, length 2^n); the in-place
+ * apply_gate / apply_control_gate / apply_function sequence of fsv_backend.cpp:59-132. */
+qsb_status qsb_fsv_simulate_from_state(qsb_handle* handle, const qsb_circuit* circuit,
+                                       const double* psi0_re, const double* psi0_im,
+                                       double* psi_re, double* psi_im);
+
+qsb_status qsb_structured_qubit_guard(const qsb_handle* handle, int32_t* guard);
+
+/* U with U[:, c] = fsv(e_c) (host planes, 2^n x 2^n row-major). With
+ * n_devices > 1 the columns are sharded over the devices, no communication. */
+qsb_status qsb_structured_build_unitary(qsb_handle* handle, const qsb_circuit* circuit,
+                                        double* u_re, double* u_im);
+
+/* psi = U e_0 of the structured U (Algorithm 1's final matvec is a column read). */
+qsb_status qsb_structured_simulate_full_state(qsb_handle* handle, const qsb_circuit* circuit,
+                                              double* psi_re, double* psi_im);
+
+/* Device-resident plans (bench, multi-GPU column shards). QSB_SV_UNITARY computes
+ * columns [col_begin, col_begin + col_count) of U (col_count a power of two
+ * dividing 2^n, col_begin a multiple of it); QSB_SV_STATE ignores them. */
+qsb_status qsb_sv_plan_create(qsb_handle* handle, const qsb_circuit* circuit, int32_t mode,
+                              int64_t col_begin, int64_t col_count, qsb_sv_plan** out);
+qsb_status qsb_sv_plan_destroy(qsb_sv_plan* plan);
+qsb_status qsb_sv_plan_get_info(const qsb_sv_plan* plan, qsb_sv_plan_info* info);
+/* QSB_SV_STATE: initial state (host or device planes of length 2^n; default |0...0>), async. */
+qsb_status qsb_sv_plan_set_state(qsb_sv_plan* plan, const double* re, const double* im, void* stream);
+/* Initialise (psi0 or identity columns) and apply every pass on `stream` (NULL = handle stream). Async. */
+qsb_status qsb_sv_plan_execute(qsb_sv_plan* plan, void* stream);
+/* Device planes of the result, [2^n][col_count] row-major (valid until the next execute/destroy). */
+qsb_status qsb_sv_plan_result_device(const qsb_sv_plan* plan, const double** re, const double** im);
 
 /* Reference memory accounting (unitary_backend.cpp:156-179), BackendKind 0 = Unitary, 1 = Fsv. */
 uint64_t qsb_memory_estimate(int32_t n_qubits, int32_t kind);

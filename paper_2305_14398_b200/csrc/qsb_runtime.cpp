@@ -26,103 +26,13 @@
 #include <vector>
 
 #include "../../include/qsb.h"
+#include "qsb_host.hpp"
 #include "qsb_internal.hpp"
+#include "qsb_sv.hpp"
 
 namespace {
 
-thread_local std::string g_error;
-
-struct Failure {
-    qsb_status code;
-    std::string msg;
-};
-
-[[noreturn]] void raise(qsb_status code, const char* fmt, ...) {
-    char buf[768];
-    va_list ap;
-    va_start(ap, fmt);
-    std::vsnprintf(buf, sizeof buf, fmt, ap);
-    va_end(ap);
-    throw Failure{code, buf};
-}
-
-void cuda_check(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) raise(QSB_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
-}
-void cuda_check(int e, const char* what) { cuda_check(static_cast<cudaError_t>(e), what); }
-
-template <typename F>
-qsb_status guarded(F&& f) {
-    try {
-        f();
-        return QSB_OK;
-    } catch (const Failure& e) {
-        g_error = e.msg;
-        return e.code;
-    } catch (const std::bad_alloc&) {
-        g_error = "host allocation failed";
-        return QSB_ERR_RESOURCE;
-    } catch (const std::exception& e) {
-        g_error = e.what();
-        return QSB_ERR_INTERNAL;
-    }
-}
-
-// Restores the caller's current device on scope exit.
-struct DeviceScope {
-    int prev = -1;
-    explicit DeviceScope(int dev) {
-        cudaGetDevice(&prev);
-        if (prev != dev) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
-    }
-    ~DeviceScope() {
-        int cur = -1;
-        cudaGetDevice(&cur);
-        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-    }
-};
-
-struct DevBuf {
-    void* p = nullptr;
-    size_t cap = 0;
-    void ensure(size_t bytes) {
-        if (bytes <= cap) return;
-        release();
-        cudaError_t e = cudaMalloc(&p, bytes);
-        if (e != cudaSuccess) {
-            cudaGetLastError();
-            p = nullptr;
-            raise(QSB_ERR_RESOURCE, "device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
-        }
-        cap = bytes;
-    }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-    }
-    template <typename T>
-    T* as() const { return static_cast<T*>(p); }
-    DevBuf() = default;
-    DevBuf(const DevBuf&) = delete;
-    DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), cap(o.cap) { o.p = nullptr; o.cap = 0; }
-    DevBuf& operator=(DevBuf&& o) noexcept {
-        if (this != &o) { release(); p = o.p; cap = o.cap; o.p = nullptr; o.cap = 0; }
-        return *this;
-    }
-    ~DevBuf() { release(); }
-};
-
-struct Buffers {
-    DevBuf v[2];     // [2][M][N] doubles each: V and V'
-    DevBuf psi;      // [2][M]
-    DevBuf x;        // [2][N] initial state
-    DevBuf layers;   // LayerDesc[] for the one-CTA path
-    DevBuf tables;   // registered function matrices
-    DevBuf p;        // probabilities
-    DevBuf partial;  // reduction partials + norm
-};
+using namespace qsbh;
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -187,66 +97,19 @@ Interval interval_of(const qsb_op& op) {
     return {op.target, 1};
 }
 
-void validate_circuit_shape(const qsb_circuit* c) {
-    if (!c) raise(QSB_ERR_ARGUMENT, "circuit is null");
-    if (c->n_qubits < 1 || c->n_qubits > 30)
-        raise(QSB_ERR_ARGUMENT, "circuit qubit count must be in [1, 30], got %d", c->n_qubits);
-    if (c->n_steps < 0) raise(QSB_ERR_ARGUMENT, "negative step count");
-    if (c->n_steps > 0 && (!c->step_offsets || !c->ops)) raise(QSB_ERR_ARGUMENT, "circuit arrays are null");
-}
-
 // Guard first, then reset placement (unitary_backend.cpp:197-206).
 void check_guard(const qsb_circuit* c, int guard) {
     if (c->n_qubits > guard) {
         const uint64_t est = qsb_memory_estimate(c->n_qubits, 0);
         char a[32], b[32];
-        auto fmt = [](uint64_t bytes, char* buf) {
-            static const char* units[] = {"B", "kB", "MB", "GB", "TB", "PB"};
-            double v = static_cast<double>(bytes);
-            int u = 0;
-            while (v >= 1000.0 && u + 1 < 6) { v /= 1000.0; ++u; }
-            std::snprintf(buf, 32, u == 0 ? "%.0f %s" : "%.2f %s", v, units[u]);
-        };
-        fmt(est, a);
-        fmt(c->n_qubits <= 29 ? engine_bytes(c->n_qubits) : ~uint64_t{0}, b);
+        format_bytes(est, a, sizeof a);
+        format_bytes(c->n_qubits <= 29 ? engine_bytes(c->n_qubits) : ~uint64_t{0}, b, sizeof b);
         raise(QSB_ERR_RESOURCE,
               "unitary-b200 backend refuses %d qubits (guard %d): estimated memory %llu bytes (%s at 8 bytes per "
               "complex; engine-accurate %s in HBM)",
               c->n_qubits, guard, static_cast<unsigned long long>(est), a, b);
     }
-    for (int s = 0; s + 1 < c->n_steps; ++s)
-        for (int i = c->step_offsets[s]; i < c->step_offsets[s + 1]; ++i)
-            if (c->ops[i].kind == QSB_OP_INSTRUCTION && c->ops[i].instruction == QSB_INSTR_RESET)
-                raise(QSB_ERR_VALIDATION, "reset is only supported in the final step");
-}
-
-void check_op(const qsb_circuit* c, const qsb_op& op) {
-    const int n = c->n_qubits;
-    auto q = [&](int v) {
-        if (v < 0 || v >= n) raise(QSB_ERR_ARGUMENT, "qubit index %d out of range for a %d-qubit circuit", v, n);
-    };
-    switch (op.kind) {
-    case QSB_OP_GATE: q(op.target); break;
-    case QSB_OP_CONTROL:
-        q(op.control);
-        q(op.target);
-        if (op.control == op.target) raise(QSB_ERR_ARGUMENT, "control gate: control and target must differ");
-        break;
-    case QSB_OP_FUNCTION: {
-        if (op.count < 1) raise(QSB_ERR_ARGUMENT, "function must span at least one qubit");
-        q(op.first);
-        if (op.first + op.count > n) raise(QSB_ERR_ARGUMENT, "function range exceeds circuit size");
-        if (op.function < 0 || op.function >= c->n_functions || !c->functions)
-            raise(QSB_ERR_LOOKUP, "registry: no function with index %d", op.function);
-        const qsb_function& f = c->functions[op.function];
-        if (f.dim != (int64_t{1} << op.count))  // unitary_backend.cpp:50-53
-            raise(QSB_ERR_VALIDATION, "function %d no longer matches its registered dimension", op.function);
-        if (!f.re || !f.im) raise(QSB_ERR_ARGUMENT, "function %d has null data", op.function);
-        break;
-    }
-    case QSB_OP_INSTRUCTION: q(op.target); break;
-    default: raise(QSB_ERR_ARGUMENT, "unknown operation kind %d", op.kind);
-    }
+    check_reset_placement(c);
 }
 
 // Greedy first-fit (unitary_backend.cpp:63-91): layer index of each op of a step.
@@ -374,22 +237,6 @@ qsb::LayerDesc identity_layer(int n) {
 
 // ------------------------------------------------------------------ handle
 
-// One CUDA device (or one virtual shard on it) driven by a handle.
-struct DeviceCtx {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    Buffers cache;  // reused by the host-API calls
-};
-
-struct qsb_handle {
-    int guard = 0;
-    int gemm_mode = QSB_GEMM_AUTO;
-    int flags = 0;
-    std::vector<std::unique_ptr<DeviceCtx>> devs;
-    std::mutex mu;
-    DeviceCtx& dev0() { return *devs.front(); }
-};
-
 struct qsb_plan {
     qsb_handle* h = nullptr;
     DeviceCtx* dc = nullptr;
@@ -403,7 +250,7 @@ struct qsb_plan {
     int tile = qsb::kTile32x32;
     int planes = 2;  // V buffer planes: re, im (+ re+im for the 3M sum-plane tile)
     bool small = false;
-    Buffers b;
+    qsbh::Buffers b;
     bool borrowed = false;
     CUtensorMap tmap[2];
     int final_buf = 0;
@@ -677,6 +524,7 @@ qsb_status qsb_create(const qsb_options* options, qsb_handle** out) {
             if (prop.major < 10)
                 raise(QSB_ERR_CUDA, "device %d (%s, sm_%d%d) is not sm_100a", id, prop.name, prop.major, prop.minor);
             cuda_check(qsb::configure_kernels(), "configure kernels");
+            cuda_check(qsb::sv_configure(), "configure sv kernels");
             const double mem = static_cast<double>(prop.totalGlobalMem);
             min_mem = (min_mem == 0.0) ? mem : std::min(min_mem, mem);
             auto dc = std::make_unique<DeviceCtx>();
@@ -694,6 +542,15 @@ qsb_status qsb_create(const qsb_options* options, qsb_handle** out) {
         for (int n = 1; n <= qsb::kMaxQubits; ++n)
             if (static_cast<double>(engine_bytes(n)) / share <= 0.92 * min_mem) hbm_guard = n;
         h->guard = o.qubit_guard > 0 ? std::min(o.qubit_guard, qsb::kMaxQubits) : hbm_guard;
+        // structured unitary: one 2^n x 2^n column block per device (+ a second for large
+        // apply_function blocks) — the same budget as the dense path's two V buffers.
+        h->structured_guard = h->guard;
+        // fsv: state + initial state + ping-pong buffer of 16 * 2^n bytes each on one device,
+        // capped at the reference's StateVector limit of 30 qubits (state.cpp:37-47).
+        int fsv_guard = 1;
+        for (int n = 1; n <= 30; ++n)
+            if (3.0 * 16.0 * static_cast<double>(uint64_t{1} << n) <= 0.92 * min_mem) fsv_guard = n;
+        h->fsv_guard = o.qubit_guard > 0 ? std::min(o.qubit_guard, 30) : fsv_guard;
         *out = h.release();
     });
 }
@@ -803,17 +660,16 @@ qsb_status qsb_build_unitary(qsb_handle* h, const qsb_circuit* c, double* u_re, 
     });
 }
 
-qsb_status qsb_simulate_and_collapse(qsb_handle* h, const qsb_circuit* c, uint64_t seed, uint64_t* basis_index) {
+qsb_status qsb_collapse(qsb_handle* h, const double* psi_re, const double* psi_im, int64_t dim, uint64_t seed,
+                        uint64_t* basis_index) {
     return guarded([&] {
-        if (!h || !basis_index) raise(QSB_ERR_ARGUMENT, "null argument");
-        validate_circuit_shape(c);
-        const size_t N = size_t{1} << c->n_qubits;
-        std::vector<double> re(N), im(N), p(N);
-        run_full(h, c, nullptr, nullptr, re.data(), im.data(), nullptr, nullptr);
+        if (!h || !psi_re || !psi_im || !basis_index || dim < 1) raise(QSB_ERR_ARGUMENT, "bad argument");
+        std::vector<double> p(static_cast<size_t>(dim));
         double norm = 0.0;
-        qsb_status st = qsb_probabilities(h, re.data(), im.data(), static_cast<int64_t>(N), p.data(), &norm);
+        qsb_status st = qsb_probabilities(h, psi_re, psi_im, dim, p.data(), &norm);
         if (st != QSB_OK) throw Failure{st, g_error};
-        // collapse (state.cpp:81-98): SplitMix64 draw, sequential inverse CDF.
+        // collapse (state.cpp:81-98): one SplitMix64 draw (state.cpp:26-35), then the
+        // sequential inverse CDF over K4's bit-exact p_i — never a parallel scan.
         uint64_t state = seed;
         uint64_t z = (state += 0x9E3779B97F4A7C15ULL);
         z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -822,15 +678,27 @@ qsb_status qsb_simulate_and_collapse(qsb_handle* h, const qsb_circuit* c, uint64
         const double u = static_cast<double>(z >> 11) * 0x1.0p-53;
         double cumulative = 0.0;
         uint64_t fallback = 0;
-        for (size_t i = 0; i < N; ++i) {
-            if (p[i] > 0.0) fallback = i;
+        for (int64_t i = 0; i < dim; ++i) {
+            if (p[i] > 0.0) fallback = static_cast<uint64_t>(i);
             cumulative += p[i];
             if (cumulative > u) {
-                *basis_index = i;
+                *basis_index = static_cast<uint64_t>(i);
                 return;
             }
         }
         *basis_index = fallback;
+    });
+}
+
+qsb_status qsb_simulate_and_collapse(qsb_handle* h, const qsb_circuit* c, uint64_t seed, uint64_t* basis_index) {
+    return guarded([&] {
+        if (!h || !basis_index) raise(QSB_ERR_ARGUMENT, "null argument");
+        validate_circuit_shape(c);
+        const size_t N = size_t{1} << c->n_qubits;
+        std::vector<double> re(N), im(N);
+        run_full(h, c, nullptr, nullptr, re.data(), im.data(), nullptr, nullptr);
+        qsb_status st = qsb_collapse(h, re.data(), im.data(), static_cast<int64_t>(N), seed, basis_index);
+        if (st != QSB_OK) throw Failure{st, g_error};
     });
 }
 

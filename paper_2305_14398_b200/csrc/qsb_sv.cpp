@@ -1,0 +1,604 @@
+// qsb_sv.cpp — host runtime of the state-vector engine behind the C ABI
+// (include/qsb.h, "state-vector engine"): the fsv backend
+// (FsvSimulator, fsv_backend.cpp:135-158) and the structured unitary
+// (U[:, c] = fsv(e_c) for all columns at once).
+//
+// Responsibilities: validate exactly where the reference's fsv backend does
+// (guard, reset placement, per-operation ranges and function dimensions:
+// fsv_backend.cpp:25-31, 74-79, 86-97, 137-142), translate the circuit into
+// flat-bit operations in application order (steps in order, operations in
+// insertion order, instructions skipped: fsv_backend.cpp:143-156), group them
+// into shared-memory batches, and run the passes on the GPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "../../include/qsb.h"
+#include "qsb_host.hpp"
+#include "qsb_sv.hpp"
+
+using namespace qsbh;
+
+struct qsb_sv_plan {
+    qsb_handle* h = nullptr;
+    DeviceCtx* dc = nullptr;
+    int mode = QSB_SV_STATE;
+    int n = 0, w = 0, m = 0;
+    int64_t col_begin = 0, col_count = 1;
+    struct FnPass {
+        int k, s;
+        const double* t_re;
+        const double* t_im;
+    };
+    enum PassKind { kReg = 0, kSlab = 1, kFn = 2 };
+    struct Pass {
+        int kind;
+        qsb::SvRegBatch reg;  // kReg: gates / controlled gates, elements in registers
+        qsb::SvBatch batch;   // kSlab: small apply_function blocks in shared memory
+        FnPass f;             // kFn: apply_function blocks larger than a slab
+    };
+    std::vector<qsb::SvLocalOp> ops;  // local ops of every batch, contiguous per batch
+    std::vector<Pass> passes;
+    Buffers b;
+    bool borrowed = false;
+    int final_buf = 0;
+    qsb_sv_plan_info info{};
+};
+
+namespace {
+
+// One operation in flat-bit form.
+struct FlatOp {
+    int kind;        // qsb::SvOpKind
+    int cls;         // qsb::SvPairClass
+    int tbit;        // pair: target flat bit; function: flat bit of the block's lsb
+    int cbit;        // pair: control flat bit or -1
+    int k;           // function: qubit count
+    int fn;          // function index
+    double u_re[4], u_im[4];
+};
+
+int classify(const double* ur, const double* ui) {
+    auto zero = [&](int e) { return ur[e] == 0.0 && ui[e] == 0.0; };
+    auto one = [&](int e) { return ur[e] == 1.0 && ui[e] == 0.0; };
+    if (zero(1) && zero(2)) return one(0) ? qsb::kPairDiag1 : qsb::kPairDiag;
+    if (zero(0) && zero(3)) return (one(1) && one(2)) ? qsb::kPairSwap : qsb::kPairAnti;
+    if (ui[0] == 0.0 && ui[1] == 0.0 && ui[2] == 0.0 && ui[3] == 0.0) return qsb::kPairReal;
+    return qsb::kPairGeneral;
+}
+
+int popcount64(uint64_t x) { return __builtin_popcountll(x); }
+
+int slab_bits_default() {
+    const char* e = std::getenv("QSB_SV_SLAB_BITS");  // tuning / tests
+    if (e && *e) {
+        const int v = std::atoi(e);
+        if (v >= 6 && v <= qsb::kSvMaxSlabBits) return v;
+    }
+    return qsb::kSvMaxSlabBits;
+}
+
+void sv_check_guard(const qsb_circuit* c, int guard, const char* backend) {
+    if (c->n_qubits > guard) {
+        raise(QSB_ERR_RESOURCE, "%s backend refuses %d qubits (guard %d)", backend, c->n_qubits, guard);
+    }
+    check_reset_placement(c);
+}
+
+std::vector<FlatOp> flatten_ops(const qsb_circuit* c, int w) {
+    const int n = c->n_qubits;
+    std::vector<FlatOp> out;
+    for (int s = 0; s < c->n_steps; ++s) {
+        if (c->step_offsets[s + 1] < c->step_offsets[s]) raise(QSB_ERR_ARGUMENT, "step offsets are not monotone");
+        for (int i = c->step_offsets[s]; i < c->step_offsets[s + 1]; ++i) {
+            const qsb_op& op = c->ops[i];
+            if (op.kind == QSB_OP_FUNCTION && op.function >= 0 && op.function < c->n_functions && c->functions &&
+                op.count >= 1 && op.count <= 30 && c->functions[op.function].dim != (int64_t{1} << op.count)) {
+                // apply_function's own check (fsv_backend.cpp:90-95)
+                raise(QSB_ERR_VALIDATION, "apply_function: matrix dimension %lld does not match 2^%d",
+                      static_cast<long long>(c->functions[op.function].dim), op.count);
+            }
+            check_op(c, op);
+            if (op.kind == QSB_OP_INSTRUCTION) continue;  // instructions do not change the state
+            FlatOp f{};
+            f.cbit = -1;
+            if (op.kind == QSB_OP_FUNCTION) {
+                f.kind = qsb::kSvFunction;
+                f.k = op.count;
+                f.tbit = w + (n - op.first - op.count);
+                f.fn = op.function;
+            } else {
+                f.kind = qsb::kSvPair;
+                f.tbit = w + (n - 1 - op.target);
+                if (op.kind == QSB_OP_CONTROL) f.cbit = w + (n - 1 - op.control);
+                std::memcpy(f.u_re, op.u_re, sizeof f.u_re);
+                std::memcpy(f.u_im, op.u_im, sizeof f.u_im);
+                f.cls = classify(f.u_re, f.u_im);
+            }
+            out.push_back(f);
+        }
+    }
+    return out;
+}
+
+uint64_t target_bits(const FlatOp& f) {
+    if (f.kind == qsb::kSvPair) return uint64_t{1} << f.tbit;
+    return ((uint64_t{1} << f.k) - 1) << f.tbit;
+}
+
+int reg_k_default() {
+    const char* e = std::getenv("QSB_SV_REG_K");  // tuning / tests
+    if (e && *e) {
+        const int v = std::atoi(e);
+        if (v >= 1 && v <= qsb::kSvRegMaxK) return v;
+    }
+    return qsb::kSvRegMaxK;
+}
+
+// A shared-memory slab batch over ops [i, j) whose target bits are T.
+void push_slab_batch(qsb_sv_plan* p, const std::vector<FlatOp>& flat, size_t i, size_t j, uint64_t T, int L,
+                     const std::vector<const double*>& tre, const std::vector<const double*>& tim) {
+    const int m = p->m;
+    // slab: low run [0, r) plus the targets at or above r, L bits in total
+    int r = L;
+    while (r > 1 && r + popcount64(T & ~((uint64_t{1} << r) - 1)) > L) --r;
+    qsb::SvBatch bt{};
+    bt.L = L;
+    bt.r = r;
+    bt.nhi = 0;
+    int local_of[64];
+    for (int q = 0; q < 64; ++q) local_of[q] = -1;
+    for (int q = 0; q < r; ++q) local_of[q] = q;
+    for (int q = r; q < m; ++q)
+        if ((T >> q) & 1u) {
+            if (bt.nhi >= qsb::kSvMaxHi) raise(QSB_ERR_INTERNAL, "sv batch: too many high slab bits");
+            local_of[q] = r + bt.nhi;
+            bt.hi[bt.nhi++] = q;
+        }
+    if (r + bt.nhi != L) raise(QSB_ERR_INTERNAL, "sv batch: slab of %d bits, expected %d", r + bt.nhi, L);
+    const uint64_t all = (m >= 64) ? ~uint64_t{0} : ((uint64_t{1} << m) - 1);
+    uint64_t slab_mask = (uint64_t{1} << r) - 1;
+    for (int q = 0; q < bt.nhi; ++q) slab_mask |= uint64_t{1} << bt.hi[q];
+    bt.outer_mask = all & ~slab_mask;
+    bt.slabs = int64_t{1} << (m - L);
+    bt.op_begin = static_cast<int>(p->ops.size());
+    bt.op_count = static_cast<int>(j - i);
+    for (size_t q = i; q < j; ++q) {
+        const FlatOp& f = flat[q];
+        qsb::SvLocalOp lo{};
+        lo.kind = f.kind;
+        lo.cls = f.cls;
+        lo.lt = local_of[f.tbit];
+        lo.k = f.k;
+        lo.lc = -1;
+        if (f.kind == qsb::kSvPair && f.cbit >= 0) {
+            if (local_of[f.cbit] >= 0) {
+                lo.lc = local_of[f.cbit];
+                lo.lcmask = 1u << lo.lc;
+            } else {
+                lo.ocmask = uint64_t{1} << f.cbit;
+            }
+        }
+        std::memcpy(lo.u_re, f.u_re, sizeof lo.u_re);
+        std::memcpy(lo.u_im, f.u_im, sizeof lo.u_im);
+        if (f.kind == qsb::kSvFunction) {
+            lo.t_re = tre[f.fn];
+            lo.t_im = tim[f.fn];
+        }
+        if (lo.lt < 0) raise(QSB_ERR_INTERNAL, "sv batch: target outside its slab");
+        p->ops.push_back(lo);
+    }
+    qsb_sv_plan::Pass ps{};
+    ps.kind = qsb_sv_plan::kSlab;
+    ps.batch = bt;
+    p->passes.push_back(ps);
+}
+
+// A register batch over pair ops [i, j) whose target bits are T (|T| <= kSvRegMaxK).
+void push_reg_batch(qsb_sv_plan* p, const std::vector<FlatOp>& flat, size_t i, size_t j, uint64_t T) {
+    qsb::SvRegBatch rb{};
+    rb.K = 0;
+    int index_of[64];
+    for (int q = 0; q < 64; ++q) index_of[q] = -1;
+    for (int q = 0; q < p->m; ++q)
+        if ((T >> q) & 1u) {
+            index_of[q] = rb.K;
+            rb.t[rb.K++] = q;
+        }
+    rb.groups = int64_t{1} << (p->m - rb.K);
+    rb.op_begin = static_cast<int>(p->ops.size());
+    rb.op_count = static_cast<int>(j - i);
+    for (size_t q = i; q < j; ++q) {
+        const FlatOp& f = flat[q];
+        qsb::SvLocalOp lo{};
+        lo.kind = qsb::kSvPair;
+        lo.cls = f.cls;
+        lo.lt = index_of[f.tbit];
+        lo.lc = -1;
+        if (f.cbit >= 0) {
+            if (index_of[f.cbit] >= 0) {
+                lo.lc = index_of[f.cbit];
+                lo.lcmask = 1u << lo.lc;
+            } else {
+                lo.ocmask = uint64_t{1} << f.cbit;
+            }
+        }
+        std::memcpy(lo.u_re, f.u_re, sizeof lo.u_re);
+        std::memcpy(lo.u_im, f.u_im, sizeof lo.u_im);
+        if (lo.lt < 0) raise(QSB_ERR_INTERNAL, "sv register batch: target outside the batch");
+        p->ops.push_back(lo);
+    }
+    qsb_sv_plan::Pass ps{};
+    ps.kind = qsb_sv_plan::kReg;
+    ps.reg = rb;
+    p->passes.push_back(ps);
+}
+
+// Group the ops into passes, in order: runs of gates / controlled gates on at
+// most K distinct targets become register batches; apply_function blocks that
+// fit a shared-memory slab become slab batches (consecutive ones merged); larger
+// blocks get the out-of-place function kernel.
+void build_passes(qsb_sv_plan* p, const std::vector<FlatOp>& flat, const std::vector<const double*>& tre,
+                  const std::vector<const double*>& tim) {
+    const int m = p->m;
+    const int L = std::min(slab_bits_default(), m);
+    const int kmax = (m <= L) ? m : L - 5;
+    const int KR = std::min(reg_k_default(), m);
+    size_t i = 0;
+    int max_targets = 0;
+    while (i < flat.size()) {
+        const FlatOp& f0 = flat[i];
+        if (f0.kind == qsb::kSvFunction && f0.k > kmax) {
+            qsb_sv_plan::Pass ps{};
+            ps.kind = qsb_sv_plan::kFn;
+            ps.f = {f0.k, f0.tbit, tre[f0.fn], tim[f0.fn]};
+            p->passes.push_back(ps);
+            ++p->info.n_function_passes;
+            ++i;
+            continue;
+        }
+        const bool fn_run = f0.kind == qsb::kSvFunction;
+        const int cap = fn_run ? kmax : KR;
+        uint64_t T = 0;
+        size_t j = i;
+        while (j < flat.size()) {
+            const FlatOp& f = flat[j];
+            if ((f.kind == qsb::kSvFunction) != fn_run) break;
+            if (fn_run && f.k > kmax) break;
+            const uint64_t need = T | target_bits(f);
+            if (popcount64(need) > cap) break;
+            T = need;
+            ++j;
+        }
+        max_targets = std::max(max_targets, popcount64(T));
+        if (fn_run)
+            push_slab_batch(p, flat, i, j, T, L, tre, tim);
+        else
+            push_reg_batch(p, flat, i, j, T);
+        i = j;
+    }
+    p->info.slab_bits = L;
+    p->info.max_batch_targets = max_targets;
+}
+
+std::unique_ptr<qsb_sv_plan> make_sv_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circuit* c, int mode,
+                                          int64_t col_begin, int64_t col_count, bool borrow_cache) {
+    validate_circuit_shape(c);
+    if (mode == QSB_SV_STATE)
+        sv_check_guard(c, h->fsv_guard, "fsv-b200");
+    else if (mode == QSB_SV_UNITARY)
+        sv_check_guard(c, h->structured_guard, "unitary-structured-b200");
+    else
+        raise(QSB_ERR_ARGUMENT, "unknown state-vector mode %d", mode);
+    auto p = std::make_unique<qsb_sv_plan>();
+    p->h = h;
+    p->dc = dc;
+    p->mode = mode;
+    p->n = c->n_qubits;
+    const int64_t N = int64_t{1} << p->n;
+    if (mode == QSB_SV_UNITARY) {
+        if (col_count < 1 || (col_count & (col_count - 1)) != 0 || col_count > N || col_begin < 0 ||
+            col_begin % col_count != 0 || col_begin + col_count > N)
+            raise(QSB_ERR_ARGUMENT, "column shard [%lld, +%lld) must be an aligned power-of-two block of [0, %lld)",
+                  static_cast<long long>(col_begin), static_cast<long long>(col_count), static_cast<long long>(N));
+        p->col_begin = col_begin;
+        p->col_count = col_count;
+        int w = 0;
+        while ((int64_t{1} << w) < col_count) ++w;
+        p->w = w;
+    } else {
+        p->col_begin = 0;
+        p->col_count = 1;
+        p->w = 0;
+    }
+    p->m = p->n + p->w;
+    if (p->m > 32) raise(QSB_ERR_RESOURCE, "state-vector array of 2^%d elements exceeds the engine's 32-bit indexing", p->m);
+    const std::vector<FlatOp> flat = flatten_ops(c, p->w);
+
+    DeviceScope ds(dc->device);
+    if (borrow_cache) {
+        p->b = std::move(dc->cache);
+        p->borrowed = true;
+    }
+    // registered matrices used by the circuit, uploaded once per plan
+    std::vector<const double*> tre(static_cast<size_t>(std::max(c->n_functions, 0)), nullptr);
+    std::vector<const double*> tim(tre.size(), nullptr);
+    {
+        std::vector<size_t> off(tre.size(), 0);
+        std::vector<char> used(tre.size(), 0);
+        size_t total = 0;
+        for (const FlatOp& f : flat)
+            if (f.kind == qsb::kSvFunction && !used[f.fn]) {
+                used[f.fn] = 1;
+                off[f.fn] = total;
+                total += 2 * static_cast<size_t>(c->functions[f.fn].dim) * c->functions[f.fn].dim;
+            }
+        if (total > 0) {
+            p->b.tables.ensure(total * sizeof(double));
+            double* base = p->b.tables.as<double>();
+            for (size_t fi = 0; fi < used.size(); ++fi) {
+                if (!used[fi]) continue;
+                const size_t d2 = static_cast<size_t>(c->functions[fi].dim) * c->functions[fi].dim;
+                cuda_check(cudaMemcpy(base + off[fi], c->functions[fi].re, d2 * 8, cudaMemcpyHostToDevice),
+                           "upload function");
+                cuda_check(cudaMemcpy(base + off[fi] + d2, c->functions[fi].im, d2 * 8, cudaMemcpyHostToDevice),
+                           "upload function");
+                tre[fi] = base + off[fi];
+                tim[fi] = base + off[fi] + d2;
+            }
+        }
+    }
+    build_passes(p.get(), flat, tre, tim);
+    const size_t elems = static_cast<size_t>(N) * static_cast<size_t>(p->col_count);
+    p->b.v[0].ensure(2 * elems * sizeof(double));
+    if (p->info.n_function_passes > 0) p->b.v[1].ensure(2 * elems * sizeof(double));
+    if (mode == QSB_SV_STATE) {
+        p->b.x.ensure(2 * elems * sizeof(double));
+        double* x = p->b.x.as<double>();
+        cuda_check(qsb::sv_launch_init_identity(x, x + elems, N, 1, 0, dc->stream), "sv_init_identity");
+        cuda_check(cudaStreamSynchronize(dc->stream), "cudaStreamSynchronize");
+    }
+    if (!p->ops.empty()) {
+        p->b.layers.ensure(p->ops.size() * sizeof(qsb::SvLocalOp));
+        cuda_check(cudaMemcpy(p->b.layers.p, p->ops.data(), p->ops.size() * sizeof(qsb::SvLocalOp),
+                              cudaMemcpyHostToDevice),
+                   "upload ops");
+    }
+    qsb_sv_plan_info& in = p->info;
+    in.n_qubits = p->n;
+    in.mode = mode;
+    in.n_ops = static_cast<int>(flat.size());
+    in.n_passes = static_cast<int>(p->passes.size());
+    in.n_launches = 1 + in.n_passes;
+    in.col_begin = p->col_begin;
+    in.col_count = p->col_count;
+    double bytes = 0.0;
+    for (const auto& ps : p->passes) {
+        bytes += 2.0 * 16.0 * static_cast<double>(elems);  // read + write the whole array
+        if (ps.kind == qsb_sv_plan::kFn) bytes += 16.0 * static_cast<double>(int64_t{1} << (2 * ps.f.k));
+    }
+    in.bytes_per_run = bytes;
+    return p;
+}
+
+void release_sv_plan(std::unique_ptr<qsb_sv_plan>& p) {
+    if (!p) return;
+    if (p->borrowed) {
+        DeviceScope ds(p->dc->device);
+        p->dc->cache = std::move(p->b);
+    }
+    p.reset();
+}
+
+void sv_execute(qsb_sv_plan* p, cudaStream_t s) {
+    DeviceScope ds(p->dc->device);
+    const int64_t R = int64_t{1} << p->n;
+    const size_t elems = static_cast<size_t>(R) * static_cast<size_t>(p->col_count);
+    double* v0 = p->b.v[0].as<double>();
+    if (p->mode == QSB_SV_STATE) {
+        cuda_check(cudaMemcpyAsync(v0, p->b.x.p, 2 * elems * sizeof(double), cudaMemcpyDeviceToDevice, s),
+                   "copy psi0");
+    } else {
+        cuda_check(qsb::sv_launch_init_identity(v0, v0 + elems, R, p->col_count, p->col_begin, s),
+                   "sv_init_identity");
+    }
+    int cur = 0;
+    const qsb::SvLocalOp* ops = p->b.layers.as<qsb::SvLocalOp>();
+    for (const auto& ps : p->passes) {
+        double* v = p->b.v[cur].as<double>();
+        if (ps.kind == qsb_sv_plan::kReg) {
+            cuda_check(qsb::sv_launch_reg(v, v + elems, ops, ps.reg, s), "sv_reg_kernel");
+        } else if (ps.kind == qsb_sv_plan::kSlab) {
+            cuda_check(qsb::sv_launch_batch(v, v + elems, ops, ps.batch, s), "sv_batch_kernel");
+        } else {
+            double* o = p->b.v[1 - cur].as<double>();
+            cuda_check(qsb::sv_launch_function(v, v + elems, o, o + elems, ps.f.t_re, ps.f.t_im, ps.f.k, ps.f.s, p->m,
+                                               s),
+                       "sv_function_kernel");
+            cur ^= 1;
+        }
+    }
+    p->final_buf = cur;
+}
+
+const double* sv_result(const qsb_sv_plan* p) { return p->b.v[p->final_buf].as<double>(); }
+size_t sv_elems(const qsb_sv_plan* p) { return (size_t{1} << p->n) * static_cast<size_t>(p->col_count); }
+
+// Host-API structured unitary: columns sharded over the handle's devices.
+void run_structured(qsb_handle* h, const qsb_circuit* c, double* u_re, double* u_im, double* psi_re,
+                    double* psi_im) {
+    std::lock_guard<std::mutex> lk(h->mu);
+    validate_circuit_shape(c);
+    const int64_t N = int64_t{1} << c->n_qubits;
+    int G = static_cast<int>(h->devs.size());
+    while (G > 1 && (N % G != 0 || (G & (G - 1)) != 0)) --G;
+    const int64_t cols = N / G;
+    std::vector<std::unique_ptr<qsb_sv_plan>> plans(G);
+    auto release_all = [&] {
+        for (auto& p : plans) release_sv_plan(p);
+    };
+    try {
+        for (int g = 0; g < G; ++g)
+            plans[g] = make_sv_plan(h, h->devs[g].get(), c, QSB_SV_UNITARY, g * cols, cols, true);
+        for (int g = 0; g < G; ++g) {
+            qsb_sv_plan* p = plans[g].get();
+            DeviceScope ds(p->dc->device);
+            cudaStream_t s = p->dc->stream;
+            sv_execute(p, s);
+            const double* v = sv_result(p);
+            const size_t elems = sv_elems(p);
+            if (u_re) {
+                cuda_check(cudaMemcpy2DAsync(u_re + p->col_begin, N * 8, v, cols * 8, cols * 8, N,
+                                             cudaMemcpyDeviceToHost, s),
+                           "download U");
+                cuda_check(cudaMemcpy2DAsync(u_im + p->col_begin, N * 8, v + elems, cols * 8, cols * 8, N,
+                                             cudaMemcpyDeviceToHost, s),
+                           "download U");
+            }
+            if (psi_re && p->col_begin == 0) {  // psi = U e_0 = column 0
+                cuda_check(cudaMemcpy2DAsync(psi_re, 8, v, cols * 8, 8, N, cudaMemcpyDeviceToHost, s), "download psi");
+                cuda_check(cudaMemcpy2DAsync(psi_im, 8, v + elems, cols * 8, 8, N, cudaMemcpyDeviceToHost, s),
+                           "download psi");
+            }
+        }
+        for (int g = 0; g < G; ++g) {
+            DeviceScope ds(plans[g]->dc->device);
+            cuda_check(cudaStreamSynchronize(plans[g]->dc->stream), "cudaStreamSynchronize");
+        }
+    } catch (...) {
+        release_all();
+        throw;
+    }
+    release_all();
+}
+
+void run_fsv(qsb_handle* h, const qsb_circuit* c, const double* psi0_re, const double* psi0_im, double* psi_re,
+             double* psi_im) {
+    std::lock_guard<std::mutex> lk(h->mu);
+    DeviceCtx& dc = h->dev0();
+    std::unique_ptr<qsb_sv_plan> p = make_sv_plan(h, &dc, c, QSB_SV_STATE, 0, 1, true);
+    try {
+        DeviceScope ds(dc.device);
+        const size_t N = size_t{1} << c->n_qubits;
+        if (psi0_re) {
+            double* x = p->b.x.as<double>();
+            cuda_check(cudaMemcpyAsync(x, psi0_re, N * 8, cudaMemcpyHostToDevice, dc.stream), "upload psi0");
+            cuda_check(cudaMemcpyAsync(x + N, psi0_im, N * 8, cudaMemcpyHostToDevice, dc.stream), "upload psi0");
+        }
+        sv_execute(p.get(), dc.stream);
+        const double* v = sv_result(p.get());
+        cuda_check(cudaMemcpyAsync(psi_re, v, N * 8, cudaMemcpyDeviceToHost, dc.stream), "download psi");
+        cuda_check(cudaMemcpyAsync(psi_im, v + N, N * 8, cudaMemcpyDeviceToHost, dc.stream), "download psi");
+        cuda_check(cudaStreamSynchronize(dc.stream), "cudaStreamSynchronize");
+    } catch (...) {
+        release_sv_plan(p);
+        throw;
+    }
+    release_sv_plan(p);
+}
+
+}  // namespace
+
+extern "C" {
+
+qsb_status qsb_fsv_qubit_guard(const qsb_handle* h, int32_t* guard) {
+    return guarded([&] {
+        if (!h || !guard) raise(QSB_ERR_ARGUMENT, "null argument");
+        *guard = h->fsv_guard;
+    });
+}
+
+qsb_status qsb_structured_qubit_guard(const qsb_handle* h, int32_t* guard) {
+    return guarded([&] {
+        if (!h || !guard) raise(QSB_ERR_ARGUMENT, "null argument");
+        *guard = h->structured_guard;
+    });
+}
+
+qsb_status qsb_fsv_simulate_full_state(qsb_handle* h, const qsb_circuit* c, double* psi_re, double* psi_im) {
+    return guarded([&] {
+        if (!h || !psi_re || !psi_im) raise(QSB_ERR_ARGUMENT, "null argument");
+        run_fsv(h, c, nullptr, nullptr, psi_re, psi_im);
+    });
+}
+
+qsb_status qsb_fsv_simulate_from_state(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
+                                       const double* psi0_im, double* psi_re, double* psi_im) {
+    return guarded([&] {
+        if (!h || !psi0_re || !psi0_im || !psi_re || !psi_im) raise(QSB_ERR_ARGUMENT, "null argument");
+        run_fsv(h, c, psi0_re, psi0_im, psi_re, psi_im);
+    });
+}
+
+qsb_status qsb_structured_build_unitary(qsb_handle* h, const qsb_circuit* c, double* u_re, double* u_im) {
+    return guarded([&] {
+        if (!h || !u_re || !u_im) raise(QSB_ERR_ARGUMENT, "null argument");
+        run_structured(h, c, u_re, u_im, nullptr, nullptr);
+    });
+}
+
+qsb_status qsb_structured_simulate_full_state(qsb_handle* h, const qsb_circuit* c, double* psi_re,
+                                              double* psi_im) {
+    return guarded([&] {
+        if (!h || !psi_re || !psi_im) raise(QSB_ERR_ARGUMENT, "null argument");
+        run_structured(h, c, nullptr, nullptr, psi_re, psi_im);
+    });
+}
+
+qsb_status qsb_sv_plan_create(qsb_handle* h, const qsb_circuit* c, int32_t mode, int64_t col_begin,
+                              int64_t col_count, qsb_sv_plan** out) {
+    return guarded([&] {
+        if (!h || !out) raise(QSB_ERR_ARGUMENT, "null argument");
+        *out = nullptr;
+        std::unique_ptr<qsb_sv_plan> p = make_sv_plan(h, &h->dev0(), c, mode, col_begin, col_count, false);
+        *out = p.release();
+    });
+}
+
+qsb_status qsb_sv_plan_destroy(qsb_sv_plan* plan) {
+    return guarded([&] {
+        std::unique_ptr<qsb_sv_plan> p(plan);
+        release_sv_plan(p);
+    });
+}
+
+qsb_status qsb_sv_plan_get_info(const qsb_sv_plan* plan, qsb_sv_plan_info* info) {
+    return guarded([&] {
+        if (!plan || !info) raise(QSB_ERR_ARGUMENT, "null argument");
+        *info = plan->info;
+    });
+}
+
+qsb_status qsb_sv_plan_set_state(qsb_sv_plan* plan, const double* re, const double* im, void* stream) {
+    return guarded([&] {
+        if (!plan || !re || !im) raise(QSB_ERR_ARGUMENT, "null argument");
+        if (plan->mode != QSB_SV_STATE) raise(QSB_ERR_ARGUMENT, "set_state needs a QSB_SV_STATE plan");
+        DeviceScope ds(plan->dc->device);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->dc->stream;
+        const size_t N = size_t{1} << plan->n;
+        double* x = plan->b.x.as<double>();
+        cuda_check(cudaMemcpyAsync(x, re, N * 8, cudaMemcpyDefault, s), "copy psi0");
+        cuda_check(cudaMemcpyAsync(x + N, im, N * 8, cudaMemcpyDefault, s), "copy psi0");
+    });
+}
+
+qsb_status qsb_sv_plan_execute(qsb_sv_plan* plan, void* stream) {
+    return guarded([&] {
+        if (!plan) raise(QSB_ERR_ARGUMENT, "null argument");
+        sv_execute(plan, stream ? static_cast<cudaStream_t>(stream) : plan->dc->stream);
+    });
+}
+
+qsb_status qsb_sv_plan_result_device(const qsb_sv_plan* plan, const double** re, const double** im) {
+    return guarded([&] {
+        if (!plan || !re || !im) raise(QSB_ERR_ARGUMENT, "null argument");
+        *re = sv_result(plan);
+        *im = sv_result(plan) + sv_elems(plan);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,438 @@
+// qsb_sv.cu — sm_100a kernels of the state-vector engine (qsb_sv.hpp):
+//
+//   sv_batch_kernel     one batch of gate / controlled-gate / small-function
+//                       operations applied to shared-memory slabs of the
+//                       [2][R][W] array (HBM-bound: one read + one write of the
+//                       array per batch, however many operations it holds).
+//   sv_function_kernel  apply_function for blocks too large for a slab
+//                       (out of place, sequential k-order sums).
+//   sv_init_identity    identity columns / |0...0>.
+//
+// Reference loops replaced (paths relative to /root/reference/proj):
+//   update_pairs (apply_gate, apply_control_gate)  core/src/fsv_backend.cpp:40-82
+//   apply_function                                 core/src/fsv_backend.cpp:84-132
+//   FsvSimulator::simulate_full_state              core/src/fsv_backend.cpp:135-158
+//   zero_state                                     core/src/state.cpp:37-47
+// Every product and sum is rounded separately (__dmul_rn / __dadd_rn /
+// __dsub_rn) in the reference's evaluation order (x86-64, no FMA contraction),
+// so the state matches the reference's fsv backend bit for bit (up to the sign
+// of zeros, which ComplexVector comparisons ignore).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "qsb_sv.hpp"
+
+namespace qsb {
+
+namespace detail {
+
+__device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
+
+// Local slab index j -> flat element index (without the slab's base).
+__device__ __forceinline__ uint64_t local_to_flat(uint32_t j, const SvBatch& b) {
+    const uint32_t lo = j & ((1u << b.r) - 1u);
+    uint32_t hi = j >> b.r;
+    uint64_t f = lo;
+#pragma unroll
+    for (int i = 0; i < kSvMaxHi; ++i) {
+        if (i < b.nhi && ((hi >> i) & 1u)) f |= uint64_t{1} << b.hi[i];
+    }
+    return f;
+}
+
+// Insert bit value v at position p of x.
+__device__ __forceinline__ uint32_t insert_bit(uint32_t x, int p, uint32_t v) {
+    const uint32_t low = x & ((1u << p) - 1u);
+    return ((x >> p) << (p + 1)) | (v << p) | low;
+}
+
+// The pair update of fsv_backend.cpp:52-55 for one class, on values:
+// (a0, a1) -> (a0', a1') with i0 = target bit clear, i1 = target bit set.
+template <int CLS>
+__device__ __forceinline__ void pair_math(const SvLocalOp& op, double& a0r, double& a0i, double& a1r, double& a1i) {
+    if (CLS == kPairSwap) {
+        const double tr = a0r, ti = a0i;
+        a0r = a1r; a0i = a1i;
+        a1r = tr; a1i = ti;
+    } else if (CLS == kPairDiag1) {
+        const double ur = op.u_re[3], ui = op.u_im[3];
+        const double r = ds(dm(ur, a1r), dm(ui, a1i));
+        const double i = da(dm(ur, a1i), dm(ui, a1r));
+        a1r = r; a1i = i;
+    } else if (CLS == kPairDiag) {
+        const double u0r = op.u_re[0], u0i = op.u_im[0], u3r = op.u_re[3], u3i = op.u_im[3];
+        const double r0 = ds(dm(u0r, a0r), dm(u0i, a0i));
+        const double i0 = da(dm(u0r, a0i), dm(u0i, a0r));
+        const double r1 = ds(dm(u3r, a1r), dm(u3i, a1i));
+        const double i1 = da(dm(u3r, a1i), dm(u3i, a1r));
+        a0r = r0; a0i = i0; a1r = r1; a1i = i1;
+    } else if (CLS == kPairAnti) {
+        const double u1r = op.u_re[1], u1i = op.u_im[1], u2r = op.u_re[2], u2i = op.u_im[2];
+        const double r0 = ds(dm(u1r, a1r), dm(u1i, a1i));
+        const double i0 = da(dm(u1r, a1i), dm(u1i, a1r));
+        const double r1 = ds(dm(u2r, a0r), dm(u2i, a0i));
+        const double i1 = da(dm(u2r, a0i), dm(u2i, a0r));
+        a0r = r0; a0i = i0; a1r = r1; a1i = i1;
+    } else if (CLS == kPairReal) {
+        const double u0 = op.u_re[0], u1 = op.u_re[1], u2 = op.u_re[2], u3 = op.u_re[3];
+        const double r0 = da(dm(u0, a0r), dm(u1, a1r));
+        const double i0 = da(dm(u0, a0i), dm(u1, a1i));
+        const double r1 = da(dm(u2, a0r), dm(u3, a1r));
+        const double i1 = da(dm(u2, a0i), dm(u3, a1i));
+        a0r = r0; a0i = i0; a1r = r1; a1i = i1;
+    } else {
+        const double u00r = op.u_re[0], u00i = op.u_im[0], u01r = op.u_re[1], u01i = op.u_im[1];
+        const double u10r = op.u_re[2], u10i = op.u_im[2], u11r = op.u_re[3], u11i = op.u_im[3];
+        // u00r * a0r - u00i * a0i + u01r * a1r - u01i * a1i, left to right
+        const double r0 = ds(da(ds(dm(u00r, a0r), dm(u00i, a0i)), dm(u01r, a1r)), dm(u01i, a1i));
+        const double i0 = da(da(da(dm(u00r, a0i), dm(u00i, a0r)), dm(u01r, a1i)), dm(u01i, a1r));
+        const double r1 = ds(da(ds(dm(u10r, a0r), dm(u10i, a0i)), dm(u11r, a1r)), dm(u11i, a1i));
+        const double i1 = da(da(da(dm(u10r, a0i), dm(u10i, a0r)), dm(u11r, a1i)), dm(u11i, a1r));
+        a0r = r0; a0i = i0; a1r = r1; a1i = i1;
+    }
+}
+
+// The same update on shared-memory elements i0, i1.
+template <int CLS>
+__device__ __forceinline__ void pair_update(const SvLocalOp& op, double* __restrict__ sre, double* __restrict__ sim,
+                                            uint32_t i0, uint32_t i1) {
+    double a0r = sre[i0], a0i = sim[i0], a1r = sre[i1], a1i = sim[i1];
+    pair_math<CLS>(op, a0r, a0i, a1r, a1i);
+    if (CLS != kPairDiag1) {
+        sre[i0] = a0r;
+        sim[i0] = a0i;
+    }
+    sre[i1] = a1r;
+    sim[i1] = a1i;
+}
+
+// Visit exactly the pairs the reference updates: target bit clear, every local
+// control bit set (single control: both bits inserted, lower position first).
+template <int CLS>
+__device__ __forceinline__ void apply_pair(const SvLocalOp& op, double* sre, double* sim, int S) {
+    const int lt = op.lt;
+    if (op.lc < 0) {
+        const int pairs = S >> 1;
+        for (int i = threadIdx.x; i < pairs; i += blockDim.x) {
+            const uint32_t i0 = insert_bit(static_cast<uint32_t>(i), lt, 0u);
+            pair_update<CLS>(op, sre, sim, i0, i0 | (1u << lt));
+        }
+    } else {
+        const int lc = op.lc;
+        const int plo = lt < lc ? lt : lc, phi = lt < lc ? lc : lt;
+        const uint32_t vlo = lt < lc ? 0u : 1u, vhi = lt < lc ? 1u : 0u;
+        const int quads = S >> 2;
+        for (int i = threadIdx.x; i < quads; i += blockDim.x) {
+            const uint32_t i0 = insert_bit(insert_bit(static_cast<uint32_t>(i), plo, vlo), phi, vhi);
+            pair_update<CLS>(op, sre, sim, i0, i0 | (1u << lt));
+        }
+    }
+}
+
+constexpr int kSvMaxPer = (1 << kSvMaxSlabBits) / kSvThreads;
+
+// apply_function on a block inside the slab (fsv_backend.cpp:109-129): for every
+// setting of the other local bits, out[row] = sum_k m[row][k] * in[k], k ascending.
+__device__ __forceinline__ void apply_function_local(const SvLocalOp& op, double* sre, double* sim, int S) {
+    const int blk = 1 << op.k;
+    const int ls = op.lt;
+    const uint32_t bmask = static_cast<uint32_t>(blk - 1) << ls;
+    double outr[kSvMaxPer], outi[kSvMaxPer];
+#pragma unroll
+    for (int q = 0; q < kSvMaxPer; ++q) {
+        const int j = threadIdx.x + q * kSvThreads;
+        if (j < S) {
+            const int row = (j >> ls) & (blk - 1);
+            const uint32_t g = static_cast<uint32_t>(j) & ~bmask;
+            const double* mr = op.t_re + static_cast<size_t>(row) * blk;
+            const double* mi = op.t_im + static_cast<size_t>(row) * blk;
+            double sr = 0.0, si = 0.0;
+            for (int kk = 0; kk < blk; ++kk) {
+                const uint32_t idx = g | (static_cast<uint32_t>(kk) << ls);
+                const double xr = sre[idx], xi = sim[idx];
+                const double m_r = __ldg(mr + kk), m_i = __ldg(mi + kk);
+                sr = da(sr, ds(dm(m_r, xr), dm(m_i, xi)));
+                si = da(si, da(dm(m_r, xi), dm(m_i, xr)));
+            }
+            outr[q] = sr;
+            outi[q] = si;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kSvMaxPer; ++q) {
+        const int j = threadIdx.x + q * kSvThreads;
+        if (j < S) {
+            sre[j] = outr[q];
+            sim[j] = outi[q];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kSvThreads) sv_batch_kernel(double* __restrict__ re, double* __restrict__ im,
+                                                            const SvLocalOp* __restrict__ ops,
+                                                            const __grid_constant__ SvBatch b) {
+    extern __shared__ double sv_smem[];
+    const int S = 1 << b.L;
+    double* sre = sv_smem;
+    double* sim = sv_smem + S;
+    for (int64_t slab = blockIdx.x; slab < b.slabs; slab += gridDim.x) {
+        // base: the slab number deposited into the outer bits
+        uint64_t base = 0, om = b.outer_mask;
+        for (uint64_t sb = static_cast<uint64_t>(slab); om != 0; sb >>= 1) {
+            const uint64_t low = om & (~om + 1);
+            if (sb & 1u) base |= low;
+            om ^= low;
+        }
+        // stage: consecutive local pairs are consecutive flat pairs (r >= 1)
+        for (int j = 2 * threadIdx.x; j < S; j += 2 * blockDim.x) {
+            const uint64_t f = base | local_to_flat(static_cast<uint32_t>(j), b);
+            const double2 vr = *reinterpret_cast<const double2*>(re + f);
+            const double2 vi = *reinterpret_cast<const double2*>(im + f);
+            *reinterpret_cast<double2*>(sre + j) = vr;
+            *reinterpret_cast<double2*>(sim + j) = vi;
+        }
+        __syncthreads();
+        for (int o = 0; o < b.op_count; ++o) {
+            const SvLocalOp& op = ops[b.op_begin + o];
+            if ((base & op.ocmask) != op.ocmask) continue;  // a control outside the slab is clear
+            if (op.kind == kSvFunction) {
+                apply_function_local(op, sre, sim, S);
+            } else {
+                switch (op.cls) {
+                case kPairSwap: apply_pair<kPairSwap>(op, sre, sim, S); break;
+                case kPairDiag1: apply_pair<kPairDiag1>(op, sre, sim, S); break;
+                case kPairDiag: apply_pair<kPairDiag>(op, sre, sim, S); break;
+                case kPairAnti: apply_pair<kPairAnti>(op, sre, sim, S); break;
+                case kPairReal: apply_pair<kPairReal>(op, sre, sim, S); break;
+                default: apply_pair<kPairGeneral>(op, sre, sim, S); break;
+                }
+            }
+            __syncthreads();
+        }
+        for (int j = 2 * threadIdx.x; j < S; j += 2 * blockDim.x) {
+            const uint64_t f = base | local_to_flat(static_cast<uint32_t>(j), b);
+            *reinterpret_cast<double2*>(re + f) = *reinterpret_cast<const double2*>(sre + j);
+            *reinterpret_cast<double2*>(im + f) = *reinterpret_cast<const double2*>(sim + j);
+        }
+        __syncthreads();
+    }
+}
+
+// ---- register batches ----------------------------------------------------
+// Pair (e, e | 1 << TB) of a group held in registers; a control inside the
+// batch's targets is the e-space mask emask (e is a compile-time index, so the
+// predicate never forces a register array into local memory).
+template <int K, int TB, int CLS>
+__device__ __forceinline__ void reg_apply(const SvLocalOp& op, double (&vr)[1 << K], double (&vi)[1 << K],
+                                          uint32_t emask) {
+#pragma unroll
+    for (int e = 0; e < (1 << K); ++e) {
+        if (e & (1 << TB)) continue;
+        if ((static_cast<uint32_t>(e) & emask) != emask) continue;
+        pair_math<CLS>(op, vr[e], vi[e], vr[e | (1 << TB)], vi[e | (1 << TB)]);
+    }
+}
+
+template <int K, int CLS>
+__device__ __forceinline__ void reg_dispatch_tb(const SvLocalOp& op, double (&vr)[1 << K], double (&vi)[1 << K]) {
+    const uint32_t emask = op.lcmask;
+    switch (op.lt) {
+    case 0: reg_apply<K, 0, CLS>(op, vr, vi, emask); break;
+    case 1: if constexpr (K > 1) reg_apply<K, 1, CLS>(op, vr, vi, emask); break;
+    case 2: if constexpr (K > 2) reg_apply<K, 2, CLS>(op, vr, vi, emask); break;
+    case 3: if constexpr (K > 3) reg_apply<K, 3, CLS>(op, vr, vi, emask); break;
+    case 4: if constexpr (K > 4) reg_apply<K, 4, CLS>(op, vr, vi, emask); break;
+    default: break;
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(kSvRegThreads) sv_reg_kernel(double* __restrict__ re, double* __restrict__ im,
+                                                             const SvLocalOp* __restrict__ ops,
+                                                             const __grid_constant__ SvRegBatch b) {
+    constexpr int E = 1 << K;
+    // flat indices fit 32 bits: m <= 32 (host-checked)
+    uint32_t tb[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) tb[i] = 1u << b.t[i];
+    for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < b.groups;
+         g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        // element 0 of the group: the group number with a zero inserted at every
+        // target bit (ascending positions, so each insert is in final coordinates)
+        uint32_t f = static_cast<uint32_t>(g);
+#pragma unroll
+        for (int i = 0; i < K; ++i) f = ((f & ~(tb[i] - 1u)) << 1) | (f & (tb[i] - 1u));
+        double vr[E], vi[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            uint32_t off = f;
+#pragma unroll
+            for (int i = 0; i < K; ++i)
+                if (e & (1 << i)) off |= tb[i];
+            vr[e] = __ldcs(re + off);
+            vi[e] = __ldcs(im + off);
+        }
+#pragma unroll 1
+        for (int o = 0; o < b.op_count; ++o) {
+            const SvLocalOp& op = ops[b.op_begin + o];
+            const uint32_t oc = static_cast<uint32_t>(op.ocmask);
+            if ((f & oc) != oc) continue;  // a control outside the targets is clear
+            switch (op.cls) {
+            case kPairSwap: reg_dispatch_tb<K, kPairSwap>(op, vr, vi); break;
+            case kPairDiag1: reg_dispatch_tb<K, kPairDiag1>(op, vr, vi); break;
+            case kPairDiag: reg_dispatch_tb<K, kPairDiag>(op, vr, vi); break;
+            case kPairAnti: reg_dispatch_tb<K, kPairAnti>(op, vr, vi); break;
+            case kPairReal: reg_dispatch_tb<K, kPairReal>(op, vr, vi); break;
+            default: reg_dispatch_tb<K, kPairGeneral>(op, vr, vi); break;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            uint32_t off = f;
+#pragma unroll
+            for (int i = 0; i < K; ++i)
+                if (e & (1 << i)) off |= tb[i];
+            __stcs(re + off, vr[e]);
+            __stcs(im + off, vi[e]);
+        }
+    }
+}
+
+// out[o][row][i] = sum_kk m[row][kk] * in[o][kk][i]; thread = one inner index i
+// and RT consecutive rows; k-order sequential per output (bit-exact).
+template <int RT>
+__global__ void __launch_bounds__(kSvThreads) sv_function_kernel(const double* __restrict__ in_re,
+                                                               const double* __restrict__ in_im,
+                                                               double* __restrict__ out_re,
+                                                               double* __restrict__ out_im,
+                                                               const double* __restrict__ t_re,
+                                                               const double* __restrict__ t_im, int k, int s,
+                                                               int m, int ti_bits) {
+    const int64_t inner = int64_t{1} << s;
+    const int blk = 1 << k;
+    const int TI = 1 << ti_bits;
+    const int TR = (kSvThreads >> ti_bits) * RT;
+    const int64_t itiles = inner >> ti_bits;
+    const int64_t rtiles = (blk + TR - 1) / TR;
+    const int64_t outer = int64_t{1} << (m - s - k);
+    const int64_t total = itiles * rtiles * outer;
+    const int ti = threadIdx.x & (TI - 1);
+    const int tg = threadIdx.x >> ti_bits;
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+        const int64_t it = t % itiles;
+        const int64_t rest = t / itiles;
+        const int64_t rt = rest % rtiles;
+        const int64_t o = rest / rtiles;
+        const int row0 = static_cast<int>(rt * TR) + tg * RT;
+        if (row0 >= blk) continue;
+        const int64_t i = it * TI + ti;
+        const size_t base = static_cast<size_t>(o) * blk * inner + i;
+        double sr[RT], si[RT];
+#pragma unroll
+        for (int q = 0; q < RT; ++q) sr[q] = si[q] = 0.0;
+        for (int kk = 0; kk < blk; ++kk) {
+            const double xr = in_re[base + static_cast<size_t>(kk) * inner];
+            const double xi = in_im[base + static_cast<size_t>(kk) * inner];
+#pragma unroll
+            for (int q = 0; q < RT; ++q) {
+                const size_t e = static_cast<size_t>(row0 + q) * blk + kk;
+                const double m_r = __ldg(t_re + e), m_i = __ldg(t_im + e);
+                sr[q] = da(sr[q], ds(dm(m_r, xr), dm(m_i, xi)));
+                si[q] = da(si[q], da(dm(m_r, xi), dm(m_i, xr)));
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < RT; ++q) {
+            out_re[base + static_cast<size_t>(row0 + q) * inner] = sr[q];
+            out_im[base + static_cast<size_t>(row0 + q) * inner] = si[q];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kSvThreads) sv_init_identity_kernel(double* __restrict__ re,
+                                                                    double* __restrict__ im, int64_t R,
+                                                                    int64_t W, int64_t col_begin) {
+    const int64_t pairs = R * W / 2;
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < pairs;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t e0 = 2 * p, e1 = e0 + 1;
+        const double v0 = (e0 / W == col_begin + e0 % W) ? 1.0 : 0.0;
+        const double v1 = (e1 / W == col_begin + e1 % W) ? 1.0 : 0.0;
+        reinterpret_cast<double2*>(re)[p] = make_double2(v0, v1);
+        reinterpret_cast<double2*>(im)[p] = make_double2(0.0, 0.0);
+    }
+}
+
+int grid_for(int64_t work, int per_sm) {
+    const int64_t cap = static_cast<int64_t>(148) * per_sm;
+    return static_cast<int>(work < 1 ? 1 : (work < cap ? work : cap));
+}
+
+}  // namespace detail
+
+using namespace detail;
+
+int sv_configure() {
+    return static_cast<int>(cudaFuncSetAttribute(sv_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 2 * (1 << kSvMaxSlabBits) * static_cast<int>(sizeof(double))));
+}
+
+int sv_launch_batch(double* re, double* im, const SvLocalOp* ops, const SvBatch& b, void* stream) {
+    const int smem = 2 * (1 << b.L) * static_cast<int>(sizeof(double));
+    int per_sm = (200 * 1024) / (smem < 4096 ? 4096 : smem);
+    if (per_sm > 8) per_sm = 8;
+    sv_batch_kernel<<<grid_for(b.slabs, per_sm), kSvThreads, smem, static_cast<cudaStream_t>(stream)>>>(re, im, ops,
+                                                                                                     b);
+    return static_cast<int>(cudaGetLastError());
+}
+
+template <int K>
+static int launch_reg_t(double* re, double* im, const SvLocalOp* ops, const SvRegBatch& b, cudaStream_t st) {
+    const int64_t blocks = (b.groups + kSvRegThreads - 1) / kSvRegThreads;
+    sv_reg_kernel<K><<<grid_for(blocks, 12), kSvRegThreads, 0, st>>>(re, im, ops, b);
+    return static_cast<int>(cudaGetLastError());
+}
+
+int sv_launch_reg(double* re, double* im, const SvLocalOp* ops, const SvRegBatch& b, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    switch (b.K) {
+    case 1: return launch_reg_t<1>(re, im, ops, b, st);
+    case 2: return launch_reg_t<2>(re, im, ops, b, st);
+    case 3: return launch_reg_t<3>(re, im, ops, b, st);
+    case 4: return launch_reg_t<4>(re, im, ops, b, st);
+    default: return launch_reg_t<5>(re, im, ops, b, st);
+    }
+}
+
+int sv_launch_function(const double* in_re, const double* in_im, double* out_re, double* out_im,
+                       const double* t_re, const double* t_im, int k, int s, int m, void* stream) {
+    const int ti_bits = s >= 6 ? 6 : s;
+    const int64_t inner = int64_t{1} << s;
+    const int blk = 1 << k;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (ti_bits == 6) {
+        const int TR = (kSvThreads >> 6) * 8;
+        const int64_t work = (inner >> 6) * ((blk + TR - 1) / TR) * (int64_t{1} << (m - s - k));
+        sv_function_kernel<8><<<grid_for(work, 8), kSvThreads, 0, st>>>(in_re, in_im, out_re, out_im, t_re, t_im,
+                                                                        k, s, m, ti_bits);
+    } else {
+        const int TR = kSvThreads >> ti_bits;
+        const int64_t work = (inner >> ti_bits) * ((blk + TR - 1) / TR) * (int64_t{1} << (m - s - k));
+        sv_function_kernel<1><<<grid_for(work, 8), kSvThreads, 0, st>>>(in_re, in_im, out_re, out_im, t_re, t_im,
+                                                                        k, s, m, ti_bits);
+    }
+    return static_cast<int>(cudaGetLastError());
+}
+
+int sv_launch_init_identity(double* re, double* im, int64_t R, int64_t W, int64_t col_begin, void* stream) {
+    const int64_t pairs = R * W / 2;
+    sv_init_identity_kernel<<<grid_for((pairs + kSvThreads - 1) / kSvThreads, 16), kSvThreads, 0,
+                              static_cast<cudaStream_t>(stream)>>>(re, im, R, W, col_begin);
+    return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace qsb

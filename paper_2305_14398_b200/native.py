@@ -63,6 +63,18 @@ class QsbPlanInfo(ctypes.Structure):
     ]
 
 
+SV_STATE, SV_UNITARY = 0, 1
+
+
+class QsbSvPlanInfo(ctypes.Structure):
+    _fields_ = [
+        ("n_qubits", ctypes.c_int32), ("mode", ctypes.c_int32), ("n_ops", ctypes.c_int32),
+        ("n_passes", ctypes.c_int32), ("n_function_passes", ctypes.c_int32), ("n_launches", ctypes.c_int32),
+        ("slab_bits", ctypes.c_int32), ("max_batch_targets", ctypes.c_int32),
+        ("col_begin", ctypes.c_int64), ("col_count", ctypes.c_int64), ("bytes_per_run", ctypes.c_double),
+    ]
+
+
 @dataclass
 class FlatCircuit:
     """A circuit flattened into the ABI's arrays; keeps the numpy storage alive."""
@@ -186,6 +198,19 @@ def lib() -> ctypes.CDLL:
         "qsb_plan_state_device": (ctypes.c_int, [P, P, P]),
         "qsb_plan_copy_state": (ctypes.c_int, [P, P, P, P]),
         "qsb_plan_last_timing": (ctypes.c_int, [P, P, P, P]),
+        "qsb_collapse": (ctypes.c_int, [P, P, P, I64, U64, P]),
+        "qsb_fsv_qubit_guard": (ctypes.c_int, [P, P]),
+        "qsb_fsv_simulate_full_state": (ctypes.c_int, [P, P, P, P]),
+        "qsb_fsv_simulate_from_state": (ctypes.c_int, [P, P, P, P, P, P]),
+        "qsb_structured_qubit_guard": (ctypes.c_int, [P, P]),
+        "qsb_structured_build_unitary": (ctypes.c_int, [P, P, P, P]),
+        "qsb_structured_simulate_full_state": (ctypes.c_int, [P, P, P, P]),
+        "qsb_sv_plan_create": (ctypes.c_int, [P, P, I32, I64, I64, P]),
+        "qsb_sv_plan_destroy": (ctypes.c_int, [P]),
+        "qsb_sv_plan_get_info": (ctypes.c_int, [P, P]),
+        "qsb_sv_plan_set_state": (ctypes.c_int, [P, P, P, P]),
+        "qsb_sv_plan_execute": (ctypes.c_int, [P, P]),
+        "qsb_sv_plan_result_device": (ctypes.c_int, [P, P, P]),
         "qsb_memory_estimate": (U64, [I32, I32]),
         "qsb_engine_memory_estimate": (U64, [I32, I32]),
     }

@@ -18,6 +18,8 @@ from .circuit import Circuit, GateRegistry
 from .errors import LookupError_
 
 BACKEND_ID = "unitary-b200"
+FSV_BACKEND_ID = "fsv-b200"
+STRUCTURED_BACKEND_ID = "unitary-structured-b200"
 
 
 @dataclass
@@ -222,6 +224,170 @@ class B200UnitarySimulator(Simulator):
             pass
 
 
+class SvPlan:
+    """A device-resident state-vector-engine plan (qsb_sv_plan_*): the fsv
+    backend (mode SV_STATE) or columns [col_begin, col_begin+col_count) of the
+    structured unitary (mode SV_UNITARY)."""
+
+    def __init__(self, sim: "_HandleOwner", flat: native.FlatCircuit, mode: int, col_begin: int, col_count: int):
+        self._flat = flat
+        self._sim = sim
+        self._p = ctypes.c_void_p()
+        native.check(native.lib().qsb_sv_plan_create(sim._h, flat.ptr, mode, col_begin, col_count,
+                                                     ctypes.byref(self._p)))
+        self.info = native.QsbSvPlanInfo()
+        native.check(native.lib().qsb_sv_plan_get_info(self._p, ctypes.byref(self.info)))
+
+    def set_state(self, re_ptr: int, im_ptr: int, stream: int = 0) -> None:
+        native.check(native.lib().qsb_sv_plan_set_state(self._p, re_ptr, im_ptr, stream or None))
+
+    def execute(self, stream: int = 0) -> None:
+        native.check(native.lib().qsb_sv_plan_execute(self._p, stream or None))
+
+    def result_device(self) -> Tuple[int, int]:
+        re, im = ctypes.c_void_p(), ctypes.c_void_p()
+        native.check(native.lib().qsb_sv_plan_result_device(self._p, ctypes.byref(re), ctypes.byref(im)))
+        return re.value, im.value
+
+    def close(self) -> None:
+        if self._p:
+            native.lib().qsb_sv_plan_destroy(self._p)
+            self._p = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _HandleOwner(Simulator):
+    """Owns one qsb_handle (qsb_create / qsb_destroy)."""
+
+    def __init__(self, qubit_guard: Optional[int] = None, device: int = 0,
+                 gemm_mode: int = native.GEMM_AUTO, flags: int = 0, devices: Optional[List[int]] = None) -> None:
+        L = native.lib()
+        self._devices = None
+        dev_ptr, n_dev = None, 0
+        if devices:
+            self._devices = (ctypes.c_int32 * len(devices))(*devices)
+            dev_ptr, n_dev = ctypes.cast(self._devices, ctypes.c_void_p).value, len(devices)
+        opts = native.QsbOptions(device, int(qubit_guard or 0), gemm_mode, flags, n_dev, 0, dev_ptr)
+        self._h = ctypes.c_void_p()
+        native.check(L.qsb_create(ctypes.byref(opts), ctypes.byref(self._h)))
+        self.device = device
+
+    @staticmethod
+    def _flat(circuit, registry):
+        return circuit if isinstance(circuit, native.FlatCircuit) else native.flatten(circuit, registry)
+
+    def _guard_of(self, fn) -> int:
+        g = ctypes.c_int32()
+        native.check(fn(self._h, ctypes.byref(g)))
+        return g.value
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            native.lib().qsb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class B200FsvSimulator(_HandleOwner):
+    """FsvSimulator (fsv_backend.hpp:41-58, fsv_backend.cpp:135-158) on B200:
+    every operation applied to the state in circuit order, batched into
+    shared-memory passes. Bit-exact with the reference's fsv backend."""
+
+    def name(self) -> str:
+        return FSV_BACKEND_ID
+
+    def qubit_guard(self) -> int:
+        return self._guard_of(native.lib().qsb_fsv_qubit_guard)
+
+    def simulate_full_state(self, circuit, registry: Optional[GateRegistry] = None) -> StateVector:
+        flat = self._flat(circuit, registry)
+        N = 1 << flat.n_qubits
+        re = np.empty(N)
+        im = np.empty(N)
+        native.check(native.lib().qsb_fsv_simulate_full_state(self._h, flat.ptr, native.dptr(re), native.dptr(im)))
+        return StateVector(flat.n_qubits, re, im)
+
+    def simulate_from_state(self, circuit, registry, psi0_re: np.ndarray, psi0_im: np.ndarray) -> StateVector:
+        flat = self._flat(circuit, registry)
+        N = 1 << flat.n_qubits
+        r0 = np.ascontiguousarray(psi0_re, dtype=np.float64)
+        i0 = np.ascontiguousarray(psi0_im, dtype=np.float64)
+        re = np.empty(N)
+        im = np.empty(N)
+        native.check(native.lib().qsb_fsv_simulate_from_state(self._h, flat.ptr, native.dptr(r0), native.dptr(i0),
+                                                              native.dptr(re), native.dptr(im)))
+        return StateVector(flat.n_qubits, re, im)
+
+    def simulate_and_collapse(self, circuit, registry: Optional[GateRegistry], seed: int) -> CollapsedState:
+        # Simulator::simulate_and_collapse default (simulator.cpp:26-30): full state, then collapse
+        st = self.simulate_full_state(circuit, registry)
+        return CollapsedState(st.n_qubits, _collapse_on(self, st.re, st.im, seed))
+
+    def plan(self, circuit, registry=None) -> SvPlan:
+        return SvPlan(self, self._flat(circuit, registry), native.SV_STATE, 0, 1)
+
+
+class B200StructuredUnitarySimulator(_HandleOwner):
+    """Unitary simulation without dense GEMMs: U[:, c] = fsv(e_c) for every
+    column c, all columns evolved at once by the state-vector engine (columns
+    sharded over devices). A different algorithm from Algorithm 1's dense
+    products — same U within rounding, reported separately."""
+
+    def name(self) -> str:
+        return STRUCTURED_BACKEND_ID
+
+    def qubit_guard(self) -> int:
+        return self._guard_of(native.lib().qsb_structured_qubit_guard)
+
+    def simulate_full_state(self, circuit, registry: Optional[GateRegistry] = None) -> StateVector:
+        flat = self._flat(circuit, registry)
+        N = 1 << flat.n_qubits
+        re = np.empty(N)
+        im = np.empty(N)
+        native.check(native.lib().qsb_structured_simulate_full_state(self._h, flat.ptr, native.dptr(re),
+                                                                     native.dptr(im)))
+        return StateVector(flat.n_qubits, re, im)
+
+    def simulate_and_collapse(self, circuit, registry: Optional[GateRegistry], seed: int) -> CollapsedState:
+        st = self.simulate_full_state(circuit, registry)
+        return CollapsedState(st.n_qubits, _collapse_on(self, st.re, st.im, seed))
+
+    def build_unitary(self, circuit, registry: Optional[GateRegistry] = None) -> Tuple[np.ndarray, np.ndarray]:
+        flat = self._flat(circuit, registry)
+        N = 1 << flat.n_qubits
+        re = np.empty((N, N))
+        im = np.empty((N, N))
+        native.check(native.lib().qsb_structured_build_unitary(self._h, flat.ptr, native.dptr(re), native.dptr(im)))
+        return re, im
+
+    def plan(self, circuit, registry=None, col_begin: int = 0, col_count: Optional[int] = None) -> SvPlan:
+        flat = self._flat(circuit, registry)
+        if col_count is None:
+            col_count = (1 << flat.n_qubits) - col_begin
+        return SvPlan(self, flat, native.SV_UNITARY, col_begin, col_count)
+
+
+def _collapse_on(sim: "_HandleOwner", re: np.ndarray, im: np.ndarray, seed: int) -> int:
+    """collapse (state.cpp:81-98) through qsb_collapse: K4 probabilities on the
+    GPU, sequential inverse-CDF walk in the native runtime."""
+    re = np.ascontiguousarray(re, dtype=np.float64)
+    im = np.ascontiguousarray(im, dtype=np.float64)
+    idx = ctypes.c_uint64()
+    native.check(native.lib().qsb_collapse(sim._h, native.dptr(re), native.dptr(im), len(re), ctypes.c_uint64(seed),
+                                           ctypes.byref(idx)))
+    return idx.value
+
+
 class _CudaArray:
     """Minimal __cuda_array_interface__ holder for a raw device pointer."""
 
@@ -251,6 +417,8 @@ SimulatorFactory = Callable[[SimulatorOptions], Simulator]
 _lock = threading.Lock()
 _factories: Dict[str, SimulatorFactory] = {
     BACKEND_ID: lambda o: B200UnitarySimulator(qubit_guard=o.qubit_guard),
+    FSV_BACKEND_ID: lambda o: B200FsvSimulator(qubit_guard=o.qubit_guard),
+    STRUCTURED_BACKEND_ID: lambda o: B200StructuredUnitarySimulator(qubit_guard=o.qubit_guard),
 }
 
 

@@ -32,7 +32,7 @@ data = {}
 index = {"cases": [], "suites": {}}
 
 
-def put_circuit(key, prog, psi=True, unitary_max_n=6, steps_max_n=0, backend="unitary"):
+def put_circuit(key, prog, psi=True, unitary_max_n=6, steps_max_n=0, backend="unitary", fsv=True):
     n, offs, ops, fns = ref.serialize(prog)
     data[f"{key}:n"] = np.array(n)
     data[f"{key}:offs"] = offs
@@ -45,6 +45,10 @@ def put_circuit(key, prog, psi=True, unitary_max_n=6, steps_max_n=0, backend="un
         re, im = ref.simulate(prog, backend, guard=n)
         data[f"{key}:psi_re"] = re
         data[f"{key}:psi_im"] = im
+    if fsv:  # FsvSimulator::simulate_full_state (fsv_backend.cpp:135-158)
+        re, im = ref.simulate(prog, "fsv", guard=n)
+        data[f"{key}:fsv_re"] = re
+        data[f"{key}:fsv_im"] = im
     if n <= unitary_max_n:
         ur, ui = ref.circuit_unitary(prog)
         data[f"{key}:u_re"] = ur
@@ -156,6 +160,18 @@ for i in range(6):
     keys.append(key)
 L.refsh_rng_free(rng)
 index["suites"]["comp"] = keys
+
+# -- fsv backend beyond one shared-memory slab (2^12 amplitudes): states only -----
+put_circuit("fsvbig_qft13", ref.named("qft", 13), psi=False, unitary_max_n=0)
+put_circuit("fsvbig_entangle14", ref.named("entangle", 14), psi=False, unitary_max_n=0)
+rng = L.refsh_rng_new(4711)
+keys = ["fsvbig_qft13", "fsvbig_entangle14"]
+for i, (n, ops) in enumerate([(13, 60), (13, 120), (14, 90), (15, 40)]):
+    p = oracle.RefProgram(ref, L.refsh_random_circuit(rng, n, ops))
+    put_circuit(f"fsvbig_{i}", p, psi=False, unitary_max_n=0)
+    keys.append(f"fsvbig_{i}")
+L.refsh_rng_free(rng)
+index["suites"]["fsvbig"] = keys
 
 # -- state.cpp: SplitMix64 draws, collapse outcomes, probabilities ---------------
 seeds = np.arange(0, 64, dtype=np.uint64)

@@ -156,3 +156,17 @@ def test_matmul_matches_naive(orc):
     h = orc.gate_matrix(0)
     assert bit_equal(orc.kronecker(h, np.eye(2, dtype=complex)),
                      np.kron(h, np.eye(2)))
+
+
+def test_fsv_restatement_bit_exact_with_reference_fsv(golden, orc):
+    """The C oracle's fsv (fsv_backend.cpp:40-158 restated) reproduces the
+    reference's own FsvSimulator output bit for bit on every recorded circuit,
+    including the multi-slab sizes (n = 13..15)."""
+    checked = 0
+    for case in golden.cases:
+        if not golden.has(f"{case}:fsv_re"):
+            continue
+        re, im = orc.fsv(golden.flat(case))
+        assert bit_equal(re, golden[f"{case}:fsv_re"]) and bit_equal(im, golden[f"{case}:fsv_im"]), case
+        checked += 1
+    assert checked >= 340
