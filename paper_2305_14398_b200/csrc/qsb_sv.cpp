@@ -31,13 +31,12 @@ struct qsb_sv_plan {
     int64_t col_begin = 0, col_count = 1;
     struct FnPass {
         int k, s;
-        const double* t_re;
-        const double* t_im;
+        qsb::SvTable tab;
     };
     enum PassKind { kReg = 0, kSlab = 1, kFn = 2 };
     struct Pass {
         int kind;
-        qsb::SvRegBatch reg;  // kReg: gates / controlled gates, elements in registers
+        std::shared_ptr<qsb::SvRegBatch> reg;  // kReg: gates / controlled gates, elements in registers
         qsb::SvBatch batch;   // kSlab: small apply_function blocks in shared memory
         FnPass f;             // kFn: apply_function blocks larger than a slab
     };
@@ -136,12 +135,12 @@ int reg_k_default() {
         const int v = std::atoi(e);
         if (v >= 1 && v <= qsb::kSvRegMaxK) return v;
     }
-    return qsb::kSvRegMaxK;
+    return qsb::kSvRegDefaultK;
 }
 
 // A shared-memory slab batch over ops [i, j) whose target bits are T.
 void push_slab_batch(qsb_sv_plan* p, const std::vector<FlatOp>& flat, size_t i, size_t j, uint64_t T, int L,
-                     const std::vector<const double*>& tre, const std::vector<const double*>& tim) {
+                     const std::vector<qsb::SvTable>& tabs) {
     const int m = p->m;
     // slab: low run [0, r) plus the targets at or above r, L bits in total
     int r = L;
@@ -185,10 +184,7 @@ void push_slab_batch(qsb_sv_plan* p, const std::vector<FlatOp>& flat, size_t i, 
         }
         std::memcpy(lo.u_re, f.u_re, sizeof lo.u_re);
         std::memcpy(lo.u_im, f.u_im, sizeof lo.u_im);
-        if (f.kind == qsb::kSvFunction) {
-            lo.t_re = tre[f.fn];
-            lo.t_im = tim[f.fn];
-        }
+        if (f.kind == qsb::kSvFunction) lo.tab = tabs[f.fn];
         if (lo.lt < 0) raise(QSB_ERR_INTERNAL, "sv batch: target outside its slab");
         p->ops.push_back(lo);
     }
@@ -198,39 +194,35 @@ void push_slab_batch(qsb_sv_plan* p, const std::vector<FlatOp>& flat, size_t i, 
     p->passes.push_back(ps);
 }
 
-// A register batch over pair ops [i, j) whose target bits are T (|T| <= kSvRegMaxK).
+// A register batch over pair ops [i, j) whose target bits are T (|T| <= kSvRegMaxK,
+// j - i <= kSvRegMaxOps); the ops travel in the launch's parameter space.
 void push_reg_batch(qsb_sv_plan* p, const std::vector<FlatOp>& flat, size_t i, size_t j, uint64_t T) {
-    qsb::SvRegBatch rb{};
-    rb.K = 0;
+    auto rb = std::make_shared<qsb::SvRegBatch>();
+    std::memset(rb.get(), 0, sizeof(qsb::SvRegBatch));
     int index_of[64];
     for (int q = 0; q < 64; ++q) index_of[q] = -1;
     for (int q = 0; q < p->m; ++q)
         if ((T >> q) & 1u) {
-            index_of[q] = rb.K;
-            rb.t[rb.K++] = q;
+            index_of[q] = rb->K;
+            rb->t[rb->K++] = q;
         }
-    rb.groups = int64_t{1} << (p->m - rb.K);
-    rb.op_begin = static_cast<int>(p->ops.size());
-    rb.op_count = static_cast<int>(j - i);
+    rb->groups = int64_t{1} << (p->m - rb->K);
+    if (j - i > static_cast<size_t>(qsb::kSvRegMaxOps)) raise(QSB_ERR_INTERNAL, "sv register batch too long");
+    rb->op_count = static_cast<int>(j - i);
     for (size_t q = i; q < j; ++q) {
         const FlatOp& f = flat[q];
-        qsb::SvLocalOp lo{};
-        lo.kind = qsb::kSvPair;
-        lo.cls = f.cls;
-        lo.lt = index_of[f.tbit];
-        lo.lc = -1;
+        qsb::SvRegOp& o = rb->ops[q - i];
+        o.cls = f.cls;
+        o.tb = index_of[f.tbit];
         if (f.cbit >= 0) {
-            if (index_of[f.cbit] >= 0) {
-                lo.lc = index_of[f.cbit];
-                lo.lcmask = 1u << lo.lc;
-            } else {
-                lo.ocmask = uint64_t{1} << f.cbit;
-            }
+            if (index_of[f.cbit] >= 0)
+                o.emask = 1u << index_of[f.cbit];
+            else
+                o.ocmask = 1u << f.cbit;
         }
-        std::memcpy(lo.u_re, f.u_re, sizeof lo.u_re);
-        std::memcpy(lo.u_im, f.u_im, sizeof lo.u_im);
-        if (lo.lt < 0) raise(QSB_ERR_INTERNAL, "sv register batch: target outside the batch");
-        p->ops.push_back(lo);
+        std::memcpy(o.u_re, f.u_re, sizeof o.u_re);
+        std::memcpy(o.u_im, f.u_im, sizeof o.u_im);
+        if (o.tb < 0) raise(QSB_ERR_INTERNAL, "sv register batch: target outside the batch");
     }
     qsb_sv_plan::Pass ps{};
     ps.kind = qsb_sv_plan::kReg;
@@ -242,11 +234,12 @@ void push_reg_batch(qsb_sv_plan* p, const std::vector<FlatOp>& flat, size_t i, s
 // most K distinct targets become register batches; apply_function blocks that
 // fit a shared-memory slab become slab batches (consecutive ones merged); larger
 // blocks get the out-of-place function kernel.
-void build_passes(qsb_sv_plan* p, const std::vector<FlatOp>& flat, const std::vector<const double*>& tre,
-                  const std::vector<const double*>& tim) {
+void build_passes(qsb_sv_plan* p, const std::vector<FlatOp>& flat, const std::vector<qsb::SvTable>& tabs) {
     const int m = p->m;
     const int L = std::min(slab_bits_default(), m);
-    const int kmax = (m <= L) ? m : L - 5;
+    // blocks of up to 2^6 run inside a slab; larger ones get their own pass
+    // (one thread per output: a 2^k-term sum per element is too long for one CTA)
+    const int kmax = std::min((m <= L) ? m : L - 5, 6);
     const int KR = std::min(reg_k_default(), m);
     size_t i = 0;
     int max_targets = 0;
@@ -255,7 +248,7 @@ void build_passes(qsb_sv_plan* p, const std::vector<FlatOp>& flat, const std::ve
         if (f0.kind == qsb::kSvFunction && f0.k > kmax) {
             qsb_sv_plan::Pass ps{};
             ps.kind = qsb_sv_plan::kFn;
-            ps.f = {f0.k, f0.tbit, tre[f0.fn], tim[f0.fn]};
+            ps.f = {f0.k, f0.tbit, tabs[f0.fn]};
             p->passes.push_back(ps);
             ++p->info.n_function_passes;
             ++i;
@@ -269,6 +262,7 @@ void build_passes(qsb_sv_plan* p, const std::vector<FlatOp>& flat, const std::ve
             const FlatOp& f = flat[j];
             if ((f.kind == qsb::kSvFunction) != fn_run) break;
             if (fn_run && f.k > kmax) break;
+            if (!fn_run && j - i >= static_cast<size_t>(qsb::kSvRegMaxOps)) break;
             const uint64_t need = T | target_bits(f);
             if (popcount64(need) > cap) break;
             T = need;
@@ -276,7 +270,7 @@ void build_passes(qsb_sv_plan* p, const std::vector<FlatOp>& flat, const std::ve
         }
         max_targets = std::max(max_targets, popcount64(T));
         if (fn_run)
-            push_slab_batch(p, flat, i, j, T, L, tre, tim);
+            push_slab_batch(p, flat, i, j, T, L, tabs);
         else
             push_reg_batch(p, flat, i, j, T);
         i = j;
@@ -324,35 +318,59 @@ std::unique_ptr<qsb_sv_plan> make_sv_plan(qsb_handle* h, DeviceCtx* dc, const qs
         p->b = std::move(dc->cache);
         p->borrowed = true;
     }
-    // registered matrices used by the circuit, uploaded once per plan
-    std::vector<const double*> tre(static_cast<size_t>(std::max(c->n_functions, 0)), nullptr);
-    std::vector<const double*> tim(tre.size(), nullptr);
+    // registered matrices used by the circuit, uploaded once per plan as CSR
+    // of their nonzeros (qsb_sv.hpp SvTable)
+    std::vector<qsb::SvTable> tabs(static_cast<size_t>(std::max(c->n_functions, 0)));
     {
-        std::vector<size_t> off(tre.size(), 0);
-        std::vector<char> used(tre.size(), 0);
-        size_t total = 0;
+        std::vector<char> used(tabs.size(), 0);
         for (const FlatOp& f : flat)
-            if (f.kind == qsb::kSvFunction && !used[f.fn]) {
-                used[f.fn] = 1;
-                off[f.fn] = total;
-                total += 2 * static_cast<size_t>(c->functions[f.fn].dim) * c->functions[f.fn].dim;
+            if (f.kind == qsb::kSvFunction) used[f.fn] = 1;
+        struct Csr {
+            std::vector<int32_t> rp, ci;
+            std::vector<double> vr, vi;
+        };
+        std::vector<Csr> csr(tabs.size());
+        size_t bytes = 0;
+        for (size_t fi = 0; fi < used.size(); ++fi) {
+            if (!used[fi]) continue;
+            const qsb_function& fn = c->functions[fi];
+            const int64_t d = fn.dim;
+            Csr& cs = csr[fi];
+            cs.rp.reserve(d + 1);
+            cs.rp.push_back(0);
+            for (int64_t r = 0; r < d; ++r) {
+                for (int64_t k = 0; k < d; ++k) {
+                    const double a = fn.re[r * d + k], b = fn.im[r * d + k];
+                    if (a == 0.0 && b == 0.0) continue;
+                    cs.ci.push_back(static_cast<int32_t>(k));
+                    cs.vr.push_back(a);
+                    cs.vi.push_back(b);
+                }
+                cs.rp.push_back(static_cast<int32_t>(cs.ci.size()));
             }
-        if (total > 0) {
-            p->b.tables.ensure(total * sizeof(double));
-            double* base = p->b.tables.as<double>();
+            bytes += 16 * cs.vr.size() + 4 * (cs.rp.size() + cs.ci.size()) + 64;
+        }
+        if (bytes > 0) {
+            p->b.tables.ensure(bytes);
+            char* base = p->b.tables.as<char>();
+            size_t off = 0;
+            auto put = [&](const void* src, size_t nbytes) {
+                char* dst = base + off;
+                if (nbytes) cuda_check(cudaMemcpy(dst, src, nbytes, cudaMemcpyHostToDevice), "upload function");
+                off += (nbytes + 15) & ~size_t{15};
+                return dst;
+            };
             for (size_t fi = 0; fi < used.size(); ++fi) {
                 if (!used[fi]) continue;
-                const size_t d2 = static_cast<size_t>(c->functions[fi].dim) * c->functions[fi].dim;
-                cuda_check(cudaMemcpy(base + off[fi], c->functions[fi].re, d2 * 8, cudaMemcpyHostToDevice),
-                           "upload function");
-                cuda_check(cudaMemcpy(base + off[fi] + d2, c->functions[fi].im, d2 * 8, cudaMemcpyHostToDevice),
-                           "upload function");
-                tre[fi] = base + off[fi];
-                tim[fi] = base + off[fi] + d2;
+                Csr& cs = csr[fi];
+                tabs[fi].vr = reinterpret_cast<const double*>(put(cs.vr.data(), 8 * cs.vr.size()));
+                tabs[fi].vi = reinterpret_cast<const double*>(put(cs.vi.data(), 8 * cs.vi.size()));
+                tabs[fi].rp = reinterpret_cast<const int32_t*>(put(cs.rp.data(), 4 * cs.rp.size()));
+                tabs[fi].ci = reinterpret_cast<const int32_t*>(put(cs.ci.data(), 4 * cs.ci.size()));
             }
         }
     }
-    build_passes(p.get(), flat, tre, tim);
+    build_passes(p.get(), flat, tabs);
     const size_t elems = static_cast<size_t>(N) * static_cast<size_t>(p->col_count);
     p->b.v[0].ensure(2 * elems * sizeof(double));
     if (p->info.n_function_passes > 0) p->b.v[1].ensure(2 * elems * sizeof(double));
@@ -379,7 +397,7 @@ std::unique_ptr<qsb_sv_plan> make_sv_plan(qsb_handle* h, DeviceCtx* dc, const qs
     double bytes = 0.0;
     for (const auto& ps : p->passes) {
         bytes += 2.0 * 16.0 * static_cast<double>(elems);  // read + write the whole array
-        if (ps.kind == qsb_sv_plan::kFn) bytes += 16.0 * static_cast<double>(int64_t{1} << (2 * ps.f.k));
+        if (ps.kind == qsb_sv_plan::kFn) bytes += 0.0;  // the CSR table is small next to the array
     }
     in.bytes_per_run = bytes;
     return p;
@@ -411,12 +429,12 @@ void sv_execute(qsb_sv_plan* p, cudaStream_t s) {
     for (const auto& ps : p->passes) {
         double* v = p->b.v[cur].as<double>();
         if (ps.kind == qsb_sv_plan::kReg) {
-            cuda_check(qsb::sv_launch_reg(v, v + elems, ops, ps.reg, s), "sv_reg_kernel");
+            cuda_check(qsb::sv_launch_reg(v, v + elems, *ps.reg, s), "sv_reg_kernel");
         } else if (ps.kind == qsb_sv_plan::kSlab) {
             cuda_check(qsb::sv_launch_batch(v, v + elems, ops, ps.batch, s), "sv_batch_kernel");
         } else {
             double* o = p->b.v[1 - cur].as<double>();
-            cuda_check(qsb::sv_launch_function(v, v + elems, o, o + elems, ps.f.t_re, ps.f.t_im, ps.f.k, ps.f.s, p->m,
+            cuda_check(qsb::sv_launch_function(v, v + elems, o, o + elems, ps.f.tab, ps.f.k, ps.f.s, p->m,
                                                s),
                        "sv_function_kernel");
             cur ^= 1;

@@ -51,8 +51,8 @@ __device__ __forceinline__ uint32_t insert_bit(uint32_t x, int p, uint32_t v) {
 
 // The pair update of fsv_backend.cpp:52-55 for one class, on values:
 // (a0, a1) -> (a0', a1') with i0 = target bit clear, i1 = target bit set.
-template <int CLS>
-__device__ __forceinline__ void pair_math(const SvLocalOp& op, double& a0r, double& a0i, double& a1r, double& a1i) {
+template <int CLS, typename Op>
+__device__ __forceinline__ void pair_math(const Op& op, double& a0r, double& a0i, double& a1r, double& a1i) {
     if (CLS == kPairSwap) {
         const double tr = a0r, ti = a0i;
         a0r = a1r; a0i = a1i;
@@ -147,13 +147,11 @@ __device__ __forceinline__ void apply_function_local(const SvLocalOp& op, double
         if (j < S) {
             const int row = (j >> ls) & (blk - 1);
             const uint32_t g = static_cast<uint32_t>(j) & ~bmask;
-            const double* mr = op.t_re + static_cast<size_t>(row) * blk;
-            const double* mi = op.t_im + static_cast<size_t>(row) * blk;
             double sr = 0.0, si = 0.0;
-            for (int kk = 0; kk < blk; ++kk) {
-                const uint32_t idx = g | (static_cast<uint32_t>(kk) << ls);
+            for (int z = __ldg(op.tab.rp + row), ze = __ldg(op.tab.rp + row + 1); z < ze; ++z) {
+                const uint32_t idx = g | (static_cast<uint32_t>(__ldg(op.tab.ci + z)) << ls);
                 const double xr = sre[idx], xi = sim[idx];
-                const double m_r = __ldg(mr + kk), m_i = __ldg(mi + kk);
+                const double m_r = __ldg(op.tab.vr + z), m_i = __ldg(op.tab.vi + z);
                 sr = da(sr, ds(dm(m_r, xr), dm(m_i, xi)));
                 si = da(si, da(dm(m_r, xi), dm(m_i, xr)));
             }
@@ -227,7 +225,7 @@ __global__ void __launch_bounds__(kSvThreads) sv_batch_kernel(double* __restrict
 // batch's targets is the e-space mask emask (e is a compile-time index, so the
 // predicate never forces a register array into local memory).
 template <int K, int TB, int CLS>
-__device__ __forceinline__ void reg_apply(const SvLocalOp& op, double (&vr)[1 << K], double (&vi)[1 << K],
+__device__ __forceinline__ void reg_apply(const SvRegOp& op, double (&vr)[1 << K], double (&vi)[1 << K],
                                           uint32_t emask) {
 #pragma unroll
     for (int e = 0; e < (1 << K); ++e) {
@@ -238,9 +236,9 @@ __device__ __forceinline__ void reg_apply(const SvLocalOp& op, double (&vr)[1 <<
 }
 
 template <int K, int CLS>
-__device__ __forceinline__ void reg_dispatch_tb(const SvLocalOp& op, double (&vr)[1 << K], double (&vi)[1 << K]) {
-    const uint32_t emask = op.lcmask;
-    switch (op.lt) {
+__device__ __forceinline__ void reg_dispatch_tb(const SvRegOp& op, double (&vr)[1 << K], double (&vi)[1 << K]) {
+    const uint32_t emask = op.emask;
+    switch (op.tb) {
     case 0: reg_apply<K, 0, CLS>(op, vr, vi, emask); break;
     case 1: if constexpr (K > 1) reg_apply<K, 1, CLS>(op, vr, vi, emask); break;
     case 2: if constexpr (K > 2) reg_apply<K, 2, CLS>(op, vr, vi, emask); break;
@@ -251,8 +249,7 @@ __device__ __forceinline__ void reg_dispatch_tb(const SvLocalOp& op, double (&vr
 }
 
 template <int K>
-__global__ void __launch_bounds__(kSvRegThreads) sv_reg_kernel(double* __restrict__ re, double* __restrict__ im,
-                                                             const SvLocalOp* __restrict__ ops,
+__global__ void __launch_bounds__(kSvRegThreads, 3) sv_reg_kernel(double* __restrict__ re, double* __restrict__ im,
                                                              const __grid_constant__ SvRegBatch b) {
     constexpr int E = 1 << K;
     // flat indices fit 32 bits: m <= 32 (host-checked)
@@ -278,8 +275,8 @@ __global__ void __launch_bounds__(kSvRegThreads) sv_reg_kernel(double* __restric
         }
 #pragma unroll 1
         for (int o = 0; o < b.op_count; ++o) {
-            const SvLocalOp& op = ops[b.op_begin + o];
-            const uint32_t oc = static_cast<uint32_t>(op.ocmask);
+            const SvRegOp& op = b.ops[o];
+            const uint32_t oc = op.ocmask;
             if ((f & oc) != oc) continue;  // a control outside the targets is clear
             switch (op.cls) {
             case kPairSwap: reg_dispatch_tb<K, kPairSwap>(op, vr, vi); break;
@@ -302,54 +299,33 @@ __global__ void __launch_bounds__(kSvRegThreads) sv_reg_kernel(double* __restric
     }
 }
 
-// out[o][row][i] = sum_kk m[row][kk] * in[o][kk][i]; thread = one inner index i
-// and RT consecutive rows; k-order sequential per output (bit-exact).
-template <int RT>
+// out[o][row][i] = sum_kk m[row][kk] * in[o][kk][i] over the nonzeros of row
+// `row` in ascending kk (bit-exact with the dense sequential sum); one thread
+// per output, consecutive threads on consecutive inner indices i (coalesced).
 __global__ void __launch_bounds__(kSvThreads) sv_function_kernel(const double* __restrict__ in_re,
                                                                const double* __restrict__ in_im,
                                                                double* __restrict__ out_re,
-                                                               double* __restrict__ out_im,
-                                                               const double* __restrict__ t_re,
-                                                               const double* __restrict__ t_im, int k, int s,
-                                                               int m, int ti_bits) {
+                                                               double* __restrict__ out_im, const SvTable tab,
+                                                               int k, int s, int m) {
     const int64_t inner = int64_t{1} << s;
-    const int blk = 1 << k;
-    const int TI = 1 << ti_bits;
-    const int TR = (kSvThreads >> ti_bits) * RT;
-    const int64_t itiles = inner >> ti_bits;
-    const int64_t rtiles = (blk + TR - 1) / TR;
-    const int64_t outer = int64_t{1} << (m - s - k);
-    const int64_t total = itiles * rtiles * outer;
-    const int ti = threadIdx.x & (TI - 1);
-    const int tg = threadIdx.x >> ti_bits;
-    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-        const int64_t it = t % itiles;
-        const int64_t rest = t / itiles;
-        const int64_t rt = rest % rtiles;
-        const int64_t o = rest / rtiles;
-        const int row0 = static_cast<int>(rt * TR) + tg * RT;
-        if (row0 >= blk) continue;
-        const int64_t i = it * TI + ti;
-        const size_t base = static_cast<size_t>(o) * blk * inner + i;
-        double sr[RT], si[RT];
-#pragma unroll
-        for (int q = 0; q < RT; ++q) sr[q] = si[q] = 0.0;
-        for (int kk = 0; kk < blk; ++kk) {
-            const double xr = in_re[base + static_cast<size_t>(kk) * inner];
-            const double xi = in_im[base + static_cast<size_t>(kk) * inner];
-#pragma unroll
-            for (int q = 0; q < RT; ++q) {
-                const size_t e = static_cast<size_t>(row0 + q) * blk + kk;
-                const double m_r = __ldg(t_re + e), m_i = __ldg(t_im + e);
-                sr[q] = da(sr[q], ds(dm(m_r, xr), dm(m_i, xi)));
-                si[q] = da(si[q], da(dm(m_r, xi), dm(m_i, xr)));
-            }
+    const int64_t blk = int64_t{1} << k;
+    const int64_t total = int64_t{1} << m;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = e & (inner - 1);
+        const int64_t row = (e >> s) & (blk - 1);
+        const int64_t base = e - (row << s);  // element with the block bits cleared
+        double sr = 0.0, si = 0.0;
+        for (int z = __ldg(tab.rp + row), ze = __ldg(tab.rp + row + 1); z < ze; ++z) {
+            const int64_t x = base + (static_cast<int64_t>(__ldg(tab.ci + z)) << s);
+            const double xr = in_re[x], xi = in_im[x];
+            const double m_r = __ldg(tab.vr + z), m_i = __ldg(tab.vi + z);
+            sr = da(sr, ds(dm(m_r, xr), dm(m_i, xi)));
+            si = da(si, da(dm(m_r, xi), dm(m_i, xr)));
         }
-#pragma unroll
-        for (int q = 0; q < RT; ++q) {
-            out_re[base + static_cast<size_t>(row0 + q) * inner] = sr[q];
-            out_im[base + static_cast<size_t>(row0 + q) * inner] = si[q];
-        }
+        out_re[e] = sr;
+        out_im[e] = si;
+        (void)i;
     }
 }
 
@@ -391,40 +367,28 @@ int sv_launch_batch(double* re, double* im, const SvLocalOp* ops, const SvBatch&
 }
 
 template <int K>
-static int launch_reg_t(double* re, double* im, const SvLocalOp* ops, const SvRegBatch& b, cudaStream_t st) {
+static int launch_reg_t(double* re, double* im, const SvRegBatch& b, cudaStream_t st) {
     const int64_t blocks = (b.groups + kSvRegThreads - 1) / kSvRegThreads;
-    sv_reg_kernel<K><<<grid_for(blocks, 12), kSvRegThreads, 0, st>>>(re, im, ops, b);
+    sv_reg_kernel<K><<<grid_for(blocks, 12), kSvRegThreads, 0, st>>>(re, im, b);
     return static_cast<int>(cudaGetLastError());
 }
 
-int sv_launch_reg(double* re, double* im, const SvLocalOp* ops, const SvRegBatch& b, void* stream) {
+int sv_launch_reg(double* re, double* im, const SvRegBatch& b, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (b.K) {
-    case 1: return launch_reg_t<1>(re, im, ops, b, st);
-    case 2: return launch_reg_t<2>(re, im, ops, b, st);
-    case 3: return launch_reg_t<3>(re, im, ops, b, st);
-    case 4: return launch_reg_t<4>(re, im, ops, b, st);
-    default: return launch_reg_t<5>(re, im, ops, b, st);
+    case 1: return launch_reg_t<1>(re, im, b, st);
+    case 2: return launch_reg_t<2>(re, im, b, st);
+    case 3: return launch_reg_t<3>(re, im, b, st);
+    case 4: return launch_reg_t<4>(re, im, b, st);
+    default: return launch_reg_t<5>(re, im, b, st);
     }
 }
 
 int sv_launch_function(const double* in_re, const double* in_im, double* out_re, double* out_im,
-                       const double* t_re, const double* t_im, int k, int s, int m, void* stream) {
-    const int ti_bits = s >= 6 ? 6 : s;
-    const int64_t inner = int64_t{1} << s;
-    const int blk = 1 << k;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (ti_bits == 6) {
-        const int TR = (kSvThreads >> 6) * 8;
-        const int64_t work = (inner >> 6) * ((blk + TR - 1) / TR) * (int64_t{1} << (m - s - k));
-        sv_function_kernel<8><<<grid_for(work, 8), kSvThreads, 0, st>>>(in_re, in_im, out_re, out_im, t_re, t_im,
-                                                                        k, s, m, ti_bits);
-    } else {
-        const int TR = kSvThreads >> ti_bits;
-        const int64_t work = (inner >> ti_bits) * ((blk + TR - 1) / TR) * (int64_t{1} << (m - s - k));
-        sv_function_kernel<1><<<grid_for(work, 8), kSvThreads, 0, st>>>(in_re, in_im, out_re, out_im, t_re, t_im,
-                                                                        k, s, m, ti_bits);
-    }
+                       const SvTable& tab, int k, int s, int m, void* stream) {
+    const int64_t total = int64_t{1} << m;
+    sv_function_kernel<<<grid_for((total + kSvThreads - 1) / kSvThreads, 8), kSvThreads, 0,
+                         static_cast<cudaStream_t>(stream)>>>(in_re, in_im, out_re, out_im, tab, k, s, m);
     return static_cast<int>(cudaGetLastError());
 }
 

@@ -44,6 +44,18 @@ enum SvPairClass : int32_t {
     kPairSwap = 5      // u = X: exchange the pair
 };
 
+// A registered matrix as its nonzero entries, row by row with ascending
+// columns (CSR). apply_function's sums run k = 0..2^k-1 in order
+// (fsv_backend.cpp:119-126); a term whose matrix entry is an exact zero adds a
+// signed zero, so summing only the nonzeros in the same order gives the same
+// value (DJ oracles are permutations: one term per row instead of 2^k).
+struct SvTable {
+    const int32_t* rp;  // 2^k + 1 row pointers
+    const int32_t* ci;  // column of each nonzero
+    const double* vr;   // nonzero values
+    const double* vi;
+};
+
 // One operation, translated into the local index space of its batch's slab.
 struct SvLocalOp {
     int32_t kind;     // SvOpKind
@@ -55,8 +67,7 @@ struct SvLocalOp {
     uint64_t ocmask;  // control bits outside the slab (flat positions): the op applies iff all are set
     double u_re[4];
     double u_im[4];
-    const double* t_re;  // function: 2^k x 2^k row-major planes on the device
-    const double* t_im;
+    SvTable tab;      // function: the registered matrix on the device
 };
 
 // One batch launch.
@@ -77,29 +88,40 @@ struct SvBatch {
 // elements that differ only in the K target bits), loads them straight from
 // HBM into registers, applies every operation of the batch, and stores them:
 // one read + one write of the array per batch, no shared memory, no barriers.
-// Ops of a register batch use SvLocalOp with lt = index of the target within
-// t[], lcmask = control bits inside t[] (e-space), ocmask = control bits
-// outside t[] (flat; tested on the group's element 0).
+// The operations travel in the kernel's parameter space (constant bank:
+// uniform, no global-load latency per operation).
 constexpr int kSvRegMaxK = 5;
+constexpr int kSvRegDefaultK = 4;  // 2^4 complex per thread: no spills at 168 registers
 constexpr int kSvRegThreads = 128;
+constexpr int kSvRegMaxOps = 192;  // 192 x 80 B: the launch stays under the 32 KB parameter limit
+
+struct SvRegOp {
+    int32_t cls;      // SvPairClass
+    int32_t tb;       // index of the target within t[]
+    uint32_t emask;   // control inside t[] (e-space bit), or 0
+    uint32_t ocmask;  // control outside t[] (flat bit, tested on the group's element 0), or 0
+    double u_re[4];
+    double u_im[4];
+};
 
 struct SvRegBatch {
-    int32_t op_begin;
     int32_t op_count;
     int32_t K;
     int32_t t[kSvRegMaxK];  // flat target bits, ascending
+    int32_t pad;
     int64_t groups;         // 2^(m - K)
+    SvRegOp ops[kSvRegMaxOps];
 };
 
 // Launch wrappers (qsb_sv.cu); return cudaError_t as int.
-int sv_launch_reg(double* re, double* im, const SvLocalOp* ops, const SvRegBatch& b, void* stream);
+int sv_launch_reg(double* re, double* im, const SvRegBatch& b, void* stream);
 int sv_configure();
 int sv_launch_batch(double* re, double* im, const SvLocalOp* ops, const SvBatch& b, void* stream);
 // out[o][row][i] = sum_kk m[row][kk] * in[o][kk][i] for a 2^k block at flat bit s
 // of an m-bit array (apply_function, fsv_backend.cpp:84-132, for blocks too
 // large for one slab). Out of place.
 int sv_launch_function(const double* in_re, const double* in_im, double* out_re, double* out_im,
-                       const double* t_re, const double* t_im, int k, int s, int m, void* stream);
+                       const SvTable& tab, int k, int s, int m, void* stream);
 // re[i * W + c] = (i == col_begin + c), im = 0: identity columns (W = 1, col_begin = 0: |0...0>).
 int sv_launch_init_identity(double* re, double* im, int64_t R, int64_t W, int64_t col_begin, void* stream);
 
