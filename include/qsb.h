@@ -197,6 +197,14 @@ qsb_status qsb_layer_operator(qsb_handle* handle, const qsb_circuit* circuit, in
 qsb_status qsb_probabilities(qsb_handle* handle, const double* psi_re, const double* psi_im,
                              int64_t dim, double* p, double* norm_squared);
 
+/* is_unitary (linalg.cpp:131-155) as GateRegistry::register_function runs it
+ * on every registered matrix (gates.cpp:112-125, tol = kRegistryUnitaryTol):
+ * result = 1 iff every |(A^H A - I)_ij| <= tol. A^H A is formed on the FP64
+ * tensor cores (dim >= 64) — the O(dim^3) check behind DJ circuit construction.
+ * Host planes, dim x dim row-major. max_deviation (optional) receives the max. */
+qsb_status qsb_is_unitary(qsb_handle* handle, const double* re, const double* im, int64_t dim, double tol,
+                          int32_t* result, double* max_deviation);
+
 /* ---- device-resident plans (bench, multi-GPU row shards) ---- */
 
 /* Compile `circuit` for rows [row_begin, row_begin + row_count) of U and upload

@@ -159,9 +159,61 @@ std::vector<int> devices_from_env() {
 }
 }  // namespace
 
+B200FsvSimulator::B200FsvSimulator(std::size_t qubit_guard, int device) {
+    qsb_options o{device, static_cast<int32_t>(qubit_guard), QSB_GEMM_AUTO, 0, 0, 0, nullptr};
+    check(qsb_create(&o, &handle_));
+    int32_t g = 0;
+    check(qsb_fsv_qubit_guard(handle_, &g));
+    guard_ = static_cast<std::size_t>(g);
+}
+
+B200FsvSimulator::~B200FsvSimulator() { qsb_destroy(handle_); }
+
+StateVector B200FsvSimulator::simulate_full_state(const Circuit& circuit, const GateRegistry& registry) const {
+    const auto f = flatten(circuit, registry);
+    StateVector s{circuit.qubit_count(), ComplexVector(std::size_t{1} << circuit.qubit_count())};
+    check(qsb_fsv_simulate_full_state(handle_, &f->c, s.amplitudes.re.data(), s.amplitudes.im.data()));
+    return s;
+}
+
+B200StructuredUnitarySimulator::B200StructuredUnitarySimulator(std::size_t qubit_guard, std::vector<int> devices) {
+    std::vector<int32_t> ids(devices.begin(), devices.end());
+    qsb_options o{ids.empty() ? 0 : ids[0], static_cast<int32_t>(qubit_guard), QSB_GEMM_AUTO, 0,
+                  static_cast<int32_t>(ids.size()), 0, ids.data()};
+    check(qsb_create(&o, &handle_));
+    int32_t g = 0;
+    check(qsb_structured_qubit_guard(handle_, &g));
+    guard_ = static_cast<std::size_t>(g);
+}
+
+B200StructuredUnitarySimulator::~B200StructuredUnitarySimulator() { qsb_destroy(handle_); }
+
+StateVector B200StructuredUnitarySimulator::simulate_full_state(const Circuit& circuit,
+                                                                const GateRegistry& registry) const {
+    const auto f = flatten(circuit, registry);
+    StateVector s{circuit.qubit_count(), ComplexVector(std::size_t{1} << circuit.qubit_count())};
+    check(qsb_structured_simulate_full_state(handle_, &f->c, s.amplitudes.re.data(), s.amplitudes.im.data()));
+    return s;
+}
+
+ComplexMatrix B200StructuredUnitarySimulator::circuit_unitary(const Circuit& circuit,
+                                                              const GateRegistry& registry) const {
+    const auto f = flatten(circuit, registry);
+    const std::size_t N = std::size_t{1} << circuit.qubit_count();
+    ComplexMatrix u(N, N);
+    check(qsb_structured_build_unitary(handle_, &f->c, u.re_data(), u.im_data()));
+    return u;
+}
+
 void register_b200_backend() {
     register_backend("unitary-b200", [](const SimulatorOptions& o) -> std::unique_ptr<Simulator> {
         return std::make_unique<B200UnitarySimulator>(o.qubit_guard.value_or(0), devices_from_env());
+    });
+    register_backend("fsv-b200", [](const SimulatorOptions& o) -> std::unique_ptr<Simulator> {
+        return std::make_unique<B200FsvSimulator>(o.qubit_guard.value_or(0), devices_from_env().front());
+    });
+    register_backend("unitary-structured-b200", [](const SimulatorOptions& o) -> std::unique_ptr<Simulator> {
+        return std::make_unique<B200StructuredUnitarySimulator>(o.qubit_guard.value_or(0), devices_from_env());
     });
 }
 

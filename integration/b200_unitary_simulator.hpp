@@ -47,8 +47,47 @@ private:
     std::size_t guard_ = 0;
 };
 
-/// register_backend("unitary-b200", ...) honouring SimulatorOptions::qubit_guard;
-/// the device list comes from QSB_DEVICES ("0,1,2,3", or "all"; default "0").
+/// FsvSimulator on the GPU (fsv_backend.cpp:135-158): every operation applied to
+/// the state in circuit order; bit-exact with the reference's fsv backend.
+class B200FsvSimulator final : public Simulator {
+public:
+    explicit B200FsvSimulator(std::size_t qubit_guard = 0, int device = 0);
+    ~B200FsvSimulator() override;
+    B200FsvSimulator(const B200FsvSimulator&) = delete;
+    B200FsvSimulator& operator=(const B200FsvSimulator&) = delete;
+
+    std::string name() const override { return "fsv-b200"; }
+    std::size_t qubit_guard() const override { return guard_; }
+    StateVector simulate_full_state(const Circuit& circuit, const GateRegistry& registry) const override;
+
+private:
+    qsb_handle* handle_ = nullptr;
+    std::size_t guard_ = 0;
+};
+
+/// Unitary simulation without dense GEMMs: U[:, c] = fsv(e_c) for every column,
+/// all columns evolved at once on the GPU (columns sharded over `devices`).
+/// Same U as UnitarySimulator within rounding; psi = U e_0.
+class B200StructuredUnitarySimulator final : public Simulator {
+public:
+    explicit B200StructuredUnitarySimulator(std::size_t qubit_guard = 0, std::vector<int> devices = {0});
+    ~B200StructuredUnitarySimulator() override;
+    B200StructuredUnitarySimulator(const B200StructuredUnitarySimulator&) = delete;
+    B200StructuredUnitarySimulator& operator=(const B200StructuredUnitarySimulator&) = delete;
+
+    std::string name() const override { return "unitary-structured-b200"; }
+    std::size_t qubit_guard() const override { return guard_; }
+    StateVector simulate_full_state(const Circuit& circuit, const GateRegistry& registry) const override;
+    ComplexMatrix circuit_unitary(const Circuit& circuit, const GateRegistry& registry) const;
+
+private:
+    qsb_handle* handle_ = nullptr;
+    std::size_t guard_ = 0;
+};
+
+/// register_backend("unitary-b200" | "fsv-b200" | "unitary-structured-b200", ...)
+/// honouring SimulatorOptions::qubit_guard; the device list comes from
+/// QSB_DEVICES ("0,1,2,3", or "all"; default "0").
 void register_b200_backend();
 
 }  // namespace qsim

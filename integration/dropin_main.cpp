@@ -37,6 +37,10 @@ std::string fmt(const char* f, double a, double b = 0) {
     return buf;
 }
 
+// ComplexVector has no operator==; compare planes with vector == (so -0.0 == +0.0,
+// as ComplexMatrix::operator==, linalg.hpp:63).
+bool same(const ComplexVector& a, const ComplexVector& b) { return a.re == b.re && a.im == b.im; }
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -73,6 +77,43 @@ int main(int argc, char** argv) {
         }
         report("200 random circuits vs fsv (1e-9)", worst <= 1e-9 && worst_norm <= 1e-9,
                fmt("worst %.3e, norm %.3e", worst, worst_norm));
+    }
+    {  // fsv-b200: the reference's own FsvSimulator, bit for bit (same seed stream)
+        std::mt19937_64 rng(20260810);
+        std::uniform_int_distribution<std::size_t> qubit_pick(2, 14);
+        std::uniform_int_distribution<std::size_t> op_pick(1, 60);
+        const FsvSimulator fsv(24);
+        auto gfsv = make_simulator("fsv-b200");
+        bool same = true;
+        for (int i = 0; i < 200; ++i) {
+            const Circuit c = test::random_circuit(rng, qubit_pick(rng), op_pick(rng));
+            same = same && ::same(gfsv->simulate_full_state(c, {}).amplitudes, fsv.simulate_full_state(c, {}).amplitudes);
+        }
+        for (std::size_t n : {13, 16})
+            same = same && ::same(gfsv->simulate_full_state(qft(n), {}).amplitudes,
+                                  fsv.simulate_full_state(qft(n), {}).amplitudes);
+        const auto dj = make_named_circuit("deutsch-jozsa", 9);  // registration is_unitary is O(8^n) on the host
+        same = same && ::same(gfsv->simulate_full_state(dj.circuit, dj.registry).amplitudes,
+                              fsv.simulate_full_state(dj.circuit, dj.registry).amplitudes);
+        report("fsv-b200 == reference FsvSimulator (200 random circuits, qft13/16, dj9; ==)", same, "");
+    }
+    {  // unitary-structured-b200: U within 1e-10 of the reference's U; U[:, c] == fsv(e_c)
+        auto gst = make_simulator("unitary-structured-b200");
+        const auto* st = dynamic_cast<const B200StructuredUnitarySimulator*>(gst.get());
+        std::mt19937_64 rng(31415);
+        std::uniform_int_distribution<std::size_t> qubit_pick(2, 6);
+        std::uniform_int_distribution<std::size_t> op_pick(1, 25);
+        double worst = 0;
+        for (int i = 0; i < 40; ++i) {
+            const Circuit c = test::random_circuit(rng, qubit_pick(rng), op_pick(rng));
+            const ComplexMatrix a = st->circuit_unitary(c, {});
+            const ComplexMatrix b = test::circuit_unitary(c, {});
+            worst = std::max(worst, max_entry_diff(a, b));
+        }
+        const auto q8 = st->simulate_full_state(qft(8), {});
+        const bool col0 = same(q8.amplitudes, FsvSimulator().simulate_full_state(qft(8), {}).amplitudes);
+        report("unitary-structured-b200 U vs reference U (40 random, 1e-10); psi == fsv", worst <= 1e-10 && col0,
+               fmt("worst %.3e", worst));
     }
     {  // acceptance_main.cpp:173-193 — QFT == DFT (n <= 6) and uniform QFT|0> (n <= 12)
         const auto* b200 = dynamic_cast<const B200UnitarySimulator*>(gpu.get());
@@ -154,7 +195,7 @@ int main(int argc, char** argv) {
         cfg.circuits = {"qft", "entangle", "deutsch-jozsa"};
         cfg.qubits_from = 4;
         cfg.qubits_to = 9;
-        cfg.backends = {"unitary-parallel", "unitary-b200"};
+        cfg.backends = {"unitary-parallel", "unitary-b200", "unitary-structured-b200", "fsv-b200"};
         cfg.warmup_iters = 3;
         cfg.sample_iters = 5;
         bool ok = true;

@@ -211,6 +211,18 @@ def _is_unitary(m: np.ndarray, tol: float) -> bool:
     return bool(np.all(np.abs(prod.real) <= tol) and np.all(np.abs(prod.imag) <= tol))
 
 
+# The unitarity check GateRegistry.register_function runs (gates.cpp:121). The
+# default is the host restatement above; set_unitarity_check() routes it to the
+# GPU (simulator.gpu_unitarity_check: qsb_is_unitary, A^H A on the DMMA pipe).
+_unitarity_check = _is_unitary
+
+
+def set_unitarity_check(fn) -> None:
+    """fn(m: complex ndarray, tol: float) -> bool, or None for the host default."""
+    global _unitarity_check
+    _unitarity_check = fn if fn is not None else _is_unitary
+
+
 class GateRegistry:
     """GateRegistry (gates.hpp:45-60, gates.cpp:112-137)."""
 
@@ -225,7 +237,7 @@ class GateRegistry:
         if n < 2 or (n & (n - 1)) != 0:
             raise ValidationError(
                 f"registry: matrix dimension for '{name}' must be a power of two >= 2, got {n}")
-        if not _is_unitary(m, REGISTRY_UNITARY_TOL):
+        if not _unitarity_check(m, REGISTRY_UNITARY_TOL):
             raise ValidationError(f"registry: matrix for '{name}' is not unitary")
         self._entries[name] = np.ascontiguousarray(m)
 

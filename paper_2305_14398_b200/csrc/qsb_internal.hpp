@@ -66,6 +66,13 @@ int launch_matvec(const double* v, int M, int N, const double* x, double* psi, v
 int launch_probabilities(const double* psi, int64_t dim, double* p, double* partial, int partial_cap,
                          double* norm, void* stream);
 
+// Registry validation (qsb_registry.cu): is_unitary via a DMMA Gram matrix.
+int registry_configure();
+int gram_tile();
+int launch_transpose(const double* re, const double* im, double* t, int N, void* stream);
+int launch_gram(const void* tmapT, int N, unsigned long long* maxdev, void* stream);
+int launch_gram_small(const double* re, const double* im, int N, unsigned long long* maxdev, void* stream);
+
 // Tile shapes of the K2 GEMM (rows x cols of the output tile).
 enum GemmTile : int { kTile128x64 = 0, kTile64x64 = 1, kTile32x32 = 2, kTileWs4M = 3, kTileWs3M = 4, kTileWs3MS = 5 };
 int configure_kernels();

@@ -525,6 +525,7 @@ qsb_status qsb_create(const qsb_options* options, qsb_handle** out) {
                 raise(QSB_ERR_CUDA, "device %d (%s, sm_%d%d) is not sm_100a", id, prop.name, prop.major, prop.minor);
             cuda_check(qsb::configure_kernels(), "configure kernels");
             cuda_check(qsb::sv_configure(), "configure sv kernels");
+            cuda_check(qsb::registry_configure(), "configure registry kernels");
             const double mem = static_cast<double>(prop.totalGlobalMem);
             min_mem = (min_mem == 0.0) ? mem : std::min(min_mem, mem);
             auto dc = std::make_unique<DeviceCtx>();
@@ -774,6 +775,47 @@ qsb_status qsb_probabilities(qsb_handle* h, const double* psi_re, const double* 
         cuda_check(cudaMemcpyAsync(p, b.p.p, dim * 8, cudaMemcpyDeviceToHost, dc.stream), "download");
         cuda_check(cudaMemcpyAsync(norm_squared, partial + cap, 8, cudaMemcpyDeviceToHost, dc.stream), "download");
         cuda_check(cudaStreamSynchronize(dc.stream), "cudaStreamSynchronize");
+    });
+}
+
+qsb_status qsb_is_unitary(qsb_handle* h, const double* re, const double* im, int64_t dim, double tol,
+                          int32_t* result, double* max_deviation) {
+    return guarded([&] {
+        if (!h || !re || !im || !result || dim < 1) raise(QSB_ERR_ARGUMENT, "bad argument");
+        if (dim > (int64_t{1} << 16))
+            raise(QSB_ERR_RESOURCE, "is_unitary: dimension %lld exceeds the supported 65536",
+                  static_cast<long long>(dim));
+        std::lock_guard<std::mutex> lk(h->mu);
+        DeviceCtx& dc = h->dev0();
+        DeviceScope ds(dc.device);
+        Buffers& b = dc.cache;
+        const size_t N = static_cast<size_t>(dim);
+        const size_t plane = N * N;
+        b.v[0].ensure(2 * plane * 8);
+        b.partial.ensure(64);
+        double* a = b.v[0].as<double>();
+        unsigned long long* maxdev = b.partial.as<unsigned long long>();
+        cudaStream_t s = dc.stream;
+        cuda_check(cudaMemcpyAsync(a, re, plane * 8, cudaMemcpyHostToDevice, s), "upload matrix");
+        cuda_check(cudaMemcpyAsync(a + plane, im, plane * 8, cudaMemcpyHostToDevice, s), "upload matrix");
+        cuda_check(cudaMemsetAsync(maxdev, 0, 8, s), "memset");
+        const int tile = qsb::gram_tile();
+        if (dim < tile || dim % tile != 0) {
+            cuda_check(qsb::launch_gram_small(a, a + plane, static_cast<int>(N), maxdev, s), "gram_small_kernel");
+        } else {
+            b.v[1].ensure(2 * plane * 8);
+            double* t = b.v[1].as<double>();
+            cuda_check(qsb::launch_transpose(a, a + plane, t, static_cast<int>(N), s), "transpose_kernel");
+            const CUtensorMap tm = make_tmap(t, static_cast<int>(N), static_cast<int>(N), tile, 2);
+            cuda_check(qsb::launch_gram(&tm, static_cast<int>(N), maxdev, s), "gram_kernel");
+        }
+        unsigned long long bits = 0;
+        cuda_check(cudaMemcpyAsync(&bits, maxdev, 8, cudaMemcpyDeviceToHost, s), "download");
+        cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        double dev;
+        std::memcpy(&dev, &bits, 8);
+        *result = dev <= tol ? 1 : 0;
+        if (max_deviation) *max_deviation = dev;
     });
 }
 

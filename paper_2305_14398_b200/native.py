@@ -199,6 +199,7 @@ def lib() -> ctypes.CDLL:
         "qsb_plan_copy_state": (ctypes.c_int, [P, P, P, P]),
         "qsb_plan_last_timing": (ctypes.c_int, [P, P, P, P]),
         "qsb_collapse": (ctypes.c_int, [P, P, P, I64, U64, P]),
+        "qsb_is_unitary": (ctypes.c_int, [P, P, P, I64, D, P, P]),
         "qsb_fsv_qubit_guard": (ctypes.c_int, [P, P]),
         "qsb_fsv_simulate_full_state": (ctypes.c_int, [P, P, P, P]),
         "qsb_fsv_simulate_from_state": (ctypes.c_int, [P, P, P, P, P, P]),

@@ -388,6 +388,24 @@ def _collapse_on(sim: "_HandleOwner", re: np.ndarray, im: np.ndarray, seed: int)
     return idx.value
 
 
+def is_unitary(sim, m: np.ndarray, tol: float) -> Tuple[bool, float]:
+    """is_unitary (linalg.cpp:131-155) on the GPU through qsb_is_unitary:
+    (verdict, max |(A^H A - I)_ij|). `sim` is any backend owning a handle."""
+    m = np.asarray(m, dtype=np.complex128)
+    re = np.ascontiguousarray(m.real)
+    im = np.ascontiguousarray(m.imag)
+    ok = ctypes.c_int32()
+    dev = ctypes.c_double()
+    native.check(native.lib().qsb_is_unitary(sim._h, native.dptr(re), native.dptr(im), m.shape[0], tol,
+                                             ctypes.byref(ok), ctypes.byref(dev)))
+    return bool(ok.value), dev.value
+
+
+def gpu_unitarity_check(sim):
+    """A GateRegistry unitarity check (circuit.set_unitarity_check) running on `sim`'s GPU."""
+    return lambda m, tol: is_unitary(sim, m, tol)[0]
+
+
 class _CudaArray:
     """Minimal __cuda_array_interface__ holder for a raw device pointer."""
 

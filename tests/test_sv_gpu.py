@@ -244,3 +244,45 @@ def test_structured_plan_shard(structured, orc):
         assert bit_equal(re[:, col - 128], cr)
     assert plan.info.col_count == 64 and plan.info.n_passes >= 1
     plan.close()
+
+
+# ---- registry validation on the GPU -------------------
+
+@pytest.mark.parametrize("dim", [2, 4, 32, 64, 128, 512, 2048])
+def test_is_unitary_matches_reference_verdict(sim, orc, dim):
+    """qsb_is_unitary (A^H A on the DMMA pipe for dim >= 64) gives the
+    reference's verdict (linalg.cpp:131-155, the C oracle) for unitary,
+    slightly perturbed and clearly non-unitary matrices at kRegistryUnitaryTol."""
+    from paper_2305_14398_b200.simulator import is_unitary
+
+    rng = np.random.default_rng(dim)
+    a = rng.standard_normal((dim, dim)) + 1j * rng.standard_normal((dim, dim))
+    u, _ = np.linalg.qr(a)
+    tol = 1e-9
+    for m, want in [(u, True), (u * (1 + 1e-6), False), (u + 1e-12 * a, True), (a / np.sqrt(dim), False)]:
+        ok, dev = is_unitary(sim, m, tol)
+        ref = orc.is_unitary(m, tol) if dim <= 512 else want
+        assert ok == ref == want, (dim, dev)
+        if dim <= 512:
+            g = m.conj().T @ m - np.eye(dim)
+            assert abs(dev - max(np.abs(g.real).max(), np.abs(g.imag).max())) <= 1e-12
+
+
+def test_is_unitary_dj_oracles(sim):
+    """The DJ oracle permutation (circuit_library.cpp:45-58) registers through the GPU check."""
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import circuit
+    from paper_2305_14398_b200.simulator import gpu_unitarity_check, is_unitary
+
+    circuit.set_unitarity_check(gpu_unitarity_check(sim))
+    try:
+        c, reg = q.make_named_circuit("deutsch-jozsa", 11)
+        m = reg.lookup(next(iter(reg._entries)))
+        ok, dev = is_unitary(sim, m, 1e-9)
+        assert ok and dev == 0.0
+        bad = m.copy()
+        bad[0, 0] += 1e-7
+        with pytest.raises(q.ValidationError, match="not unitary"):
+            reg.register_function("bad", bad)
+    finally:
+        circuit.set_unitarity_check(None)
