@@ -205,6 +205,20 @@ ComplexMatrix B200StructuredUnitarySimulator::circuit_unitary(const Circuit& cir
     return u;
 }
 
+bool b200_is_unitary(const ComplexMatrix& m, double tol) {
+    if (m.rows() != m.cols())  // the reference's ShapeError (linalg.cpp:132-135)
+        throw ShapeError("is_unitary: matrix is " + std::to_string(m.rows()) + "x" + std::to_string(m.cols()));
+    static qsb_handle* handle = [] {
+        qsb_options o{0, 0, QSB_GEMM_AUTO, 0, 0, 0, nullptr};
+        qsb_handle* h = nullptr;
+        check(qsb_create(&o, &h));
+        return h;
+    }();
+    int32_t ok = 0;
+    check(qsb_is_unitary(handle, m.re_data(), m.im_data(), static_cast<int64_t>(m.rows()), tol, &ok, nullptr));
+    return ok != 0;
+}
+
 void register_b200_backend() {
     register_backend("unitary-b200", [](const SimulatorOptions& o) -> std::unique_ptr<Simulator> {
         return std::make_unique<B200UnitarySimulator>(o.qubit_guard.value_or(0), devices_from_env());

@@ -85,6 +85,11 @@ private:
     std::size_t guard_ = 0;
 };
 
+/// is_unitary (linalg.cpp:131-155) on the GPU (qsb_is_unitary: A^H A on the
+/// FP64 tensor cores), through a process-wide handle on device 0. The
+/// replacement for the check in GateRegistry::register_function (gates.cpp:121).
+bool b200_is_unitary(const ComplexMatrix& m, double tol);
+
 /// register_backend("unitary-b200" | "fsv-b200" | "unitary-structured-b200", ...)
 /// honouring SimulatorOptions::qubit_guard; the device list comes from
 /// QSB_DEVICES ("0,1,2,3", or "all"; default "0").

@@ -115,6 +115,25 @@ int main(int argc, char** argv) {
         report("unitary-structured-b200 U vs reference U (40 random, 1e-10); psi == fsv", worst <= 1e-10 && col0,
                fmt("worst %.3e", worst));
     }
+    {  // registry validation on the GPU: same verdicts as the reference's is_unitary
+        std::mt19937_64 rng(555);
+        std::normal_distribution<double> nd;
+        bool ok = true;
+        for (std::size_t n : {1, 3, 6, 8}) {
+            const std::size_t d = std::size_t{1} << n;
+            ComplexMatrix perm(d, d), noisy(d, d);
+            for (std::size_t i = 0; i < d; ++i) perm.re((i * 5 + 3) % d, i) = 1.0;  // a permutation
+            for (std::size_t i = 0; i < d; ++i)
+                for (std::size_t j = 0; j < d; ++j) {
+                    noisy.re(i, j) = perm.re(i, j) + 1e-7 * nd(rng);
+                    noisy.im(i, j) = 1e-7 * nd(rng);
+                }
+            ok = ok && b200_is_unitary(perm, kRegistryUnitaryTol) == is_unitary(perm, kRegistryUnitaryTol) &&
+                 b200_is_unitary(noisy, kRegistryUnitaryTol) == is_unitary(noisy, kRegistryUnitaryTol) &&
+                 b200_is_unitary(perm, kRegistryUnitaryTol) && !b200_is_unitary(noisy, kRegistryUnitaryTol);
+        }
+        report("b200_is_unitary verdicts == reference is_unitary (dims 2..256)", ok, "");
+    }
     {  // acceptance_main.cpp:173-193 — QFT == DFT (n <= 6) and uniform QFT|0> (n <= 12)
         const auto* b200 = dynamic_cast<const B200UnitarySimulator*>(gpu.get());
         double worst = 0;
