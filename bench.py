@@ -340,6 +340,7 @@ def run_ours(args):
                        "gemms_per_circuit": n_gemms, "layers": info.n_layers if info else None,
                        "identity_layers_skipped": info.n_identity_layers if info else None,
                        "gemm_mode": args.gemm_mode,
+                       "gemm_splitk": info.gemm_splits if info else None,
                        "l2": ("inputs larger than L2" if flush is None else "L2 flushed between steps")},
             "tflops": job_tflops,
             "fp64_peak_frac": job_tflops / (FP64_DMMA_PEAK_TFLOPS * world),

@@ -143,6 +143,8 @@ typedef struct qsb_plan_info {
     double expand_bytes;       /* bytes written by the K1 expansion */
     int32_t gemm_tile;         /* K2 variant: QSB_TILE_* */
     int32_t v_planes;          /* planes per V buffer (2, or 3 with the 3M sum plane) */
+    int32_t gemm_splits;       /* split-K cluster size of the K2 launches (1, 2, 4) */
+    int32_t reserved;
 } qsb_plan_info;
 
 /* K2 variants reported in qsb_plan_info.gemm_tile. */

@@ -22,7 +22,11 @@ constexpr int kMaxBlocks = kMaxQubits;
 enum BlockKind : int32_t {
     kBlockGate = 0,        // 2x2 gate_matrix on one qubit            (gates.cpp:40-77)
     kBlockControlled = 1,  // controlled_unitary over a span          (gates.cpp:79-110)
-    kBlockTable = 2        // registered FunctionOp matrix, in HBM    (gates.cpp:127-133)
+    kBlockTable = 2,       // registered FunctionOp matrix, in HBM    (gates.cpp:127-133)
+    kBlockMonomial = 3     // registered matrix with at most one nonzero per row (e.g. the DJ
+                           // oracle permutation, circuit_library.cpp:45-58): per row its
+                           // column (t_col, -1 if none) and value — the same entries, 2^span
+                           // reads instead of 4^span
 };
 
 struct BlockDesc {
@@ -34,8 +38,9 @@ struct BlockDesc {
     uint32_t tmask;     // controlled: target bit within the span
     double u_re[4];     // gate / controlled: 2x2 row-major
     double u_im[4];
-    const double* t_re; // table: (2^span)^2 row-major planes on the device
+    const double* t_re; // table: (2^span)^2 row-major planes; monomial: 2^span row values
     const double* t_im;
+    const int32_t* t_col;  // monomial: column of each row's nonzero, or -1
 };
 
 struct LayerDesc {
@@ -54,6 +59,9 @@ struct GemmArgs {
     double* out;             // [2][M][N]
     int M;
     int N;
+    int splits = 1;          // warp-specialised tiles: K split over a thread-block cluster of this
+                             // size (1, 2, 4); partial accumulators are summed through
+                             // distributed shared memory in rank order (deterministic)
 };
 
 int launch_expand(const LayerDesc& layer, uint32_t row_begin, int M, int N, double* out, int planes,

@@ -65,6 +65,10 @@ __device__ __forceinline__ void block_entry(const BlockDesc& b, uint32_t r, uint
             er = b.u_re[e];
             ei = b.u_im[e];
         }
+    } else if (b.kind == kBlockMonomial) {
+        const bool hit = __ldg(b.t_col + rb) == static_cast<int32_t>(cb);
+        er = hit ? __ldg(b.t_re + rb) : 0.0;
+        ei = hit ? __ldg(b.t_im + rb) : 0.0;
     } else {
         const size_t e = (static_cast<size_t>(rb) << b.span) + cb;
         er = __ldg(b.t_re + e);
@@ -218,12 +222,20 @@ __device__ __forceinline__ void gen_batch(const LayerDesc& d, const TilePrefix& 
         const BlockDesc& B = d.blocks[b];
         const int kind = B.kind, shift = B.shift;
         const uint32_t mask = B.mask;
-        if (kind == kBlockTable) {
+        if (kind == kBlockTable || kind == kBlockMonomial) {
 #pragma unroll
             for (int k = 0; k < EB; ++k) {
                 const uint32_t rb = (r[k] >> shift) & mask, cb = (c[k] >> shift) & mask;
-                const size_t e = (static_cast<size_t>(rb) << B.span) + cb;
-                const double er = __ldg(B.t_re + e), ei = __ldg(B.t_im + e);
+                double er, ei;
+                if (kind == kBlockMonomial) {
+                    const bool hit = __ldg(B.t_col + rb) == static_cast<int32_t>(cb);
+                    er = hit ? __ldg(B.t_re + rb) : 0.0;
+                    ei = hit ? __ldg(B.t_im + rb) : 0.0;
+                } else {
+                    const size_t e = (static_cast<size_t>(rb) << B.span) + cb;
+                    er = __ldg(B.t_re + e);
+                    ei = __ldg(B.t_im + e);
+                }
                 double tr, ti;
                 if (real) {
                     vr[k] = __dmul_rn(vr[k], er);
@@ -561,6 +573,14 @@ struct WsCfg {
     static constexpr int PRODUCER_REGS = 72;
 };
 
+// All threads of the thread-block cluster: release our shared-memory writes,
+// acquire everyone else's.
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;\n" ::
+                     : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -582,7 +602,12 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
     const int lane = tid & 31;
     const int m0 = blockIdx.y * BM;
     const int n0 = blockIdx.x * BN;
-    const int KT = N / C::BK;
+    // split-K over the cluster (gridDim.z = cluster size): rank r owns k-tiles [kt0, kt1)
+    const int splits = gridDim.z;
+    const int rank = blockIdx.z;
+    const int KTall = N / C::BK;
+    const int kt0 = (KTall * rank) / splits;
+    const int KT = (KTall * (rank + 1)) / splits - kt0;
 
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
@@ -603,12 +628,13 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
             if (kt >= C::STAGES) mbar_wait(sEmpty + 8 * s, ((kt / C::STAGES) & 1) ^ 1);
             const uint32_t stage = sBase + s * C::STAGE;
             const uint32_t tma_bar = sFull + 8 * s;
+            const int ktg = kt0 + kt;  // global k-tile
             if (ptid == 0) {
                 mbar_expect_tx(tma_bar, C::A_TMA_BYTES);
-                tma_load_3d(stage, &tmA, tma_bar, kt * C::BK, m0, 0);
+                tma_load_3d(stage, &tmA, tma_bar, ktg * C::BK, m0, 0);
             }
             const uint32_t bBase = stage + C::A_BYTES;
-            const TilePrefix tp = tile_prefix<C::LOWBITS>(layer, static_cast<uint32_t>(kt * C::BK),
+            const TilePrefix tp = tile_prefix<C::LOWBITS>(layer, static_cast<uint32_t>(ktg * C::BK),
                                                           static_cast<uint32_t>(n0));
             if (tp.zero) {
                 // whole operator tile is zero: clear the B planes of this stage
@@ -624,7 +650,7 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
                         const int idx = ptid + (q0 + h) * 32 * C::PRODUCER_WARPS;
                         nn[h] = idx % BN;
                         pp[h] = idx / BN;
-                        rr[2 * h] = static_cast<uint32_t>(kt * C::BK + 2 * pp[h]);
+                        rr[2 * h] = static_cast<uint32_t>(ktg * C::BK + 2 * pp[h]);
                         rr[2 * h + 1] = rr[2 * h] + 1;
                         cc[2 * h] = cc[2 * h + 1] = static_cast<uint32_t>(n0 + nn[h]);
                     }
@@ -643,6 +669,10 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(sFull + 8 * s);
+        }
+        if (splits > 1) {  // every thread of the cluster takes part in both cluster barriers
+            cluster_sync();
+            cluster_sync();
         }
         return;
     }
@@ -745,6 +775,55 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
         if (lane == 0) mbar_arrive(sEmpty + 8 * s);
     }
 
+    if (splits > 1) {
+        // Deterministic split-K: every rank parks its partial accumulators in its
+        // own shared memory ([value][consumer thread]); rank 0 adds ranks 1..s-1
+        // in order through distributed shared memory, then writes the tile.
+        constexpr int NV = NACC * 4 * NT * 2;
+        constexpr int CT = 32 * C::CONSUMER_WARPS;
+        asm volatile("bar.sync 1, %0;" ::"n"(CT) : "memory");  // all consumers are past the last stage
+        const uint32_t part = sBase + static_cast<uint32_t>(tid) * 8;
+        {
+            int v = 0;
+#pragma unroll
+            for (int a = 0; a < NACC; ++a)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e, ++v)
+                            asm volatile("st.shared.f64 [%0], %1;" ::"r"(part + v * CT * 8), "d"(acc[a][i][j][e])
+                                         : "memory");
+        }
+        cluster_sync();
+        if (rank == 0) {
+            for (int r = 1; r < splits; ++r) {
+                uint32_t remote;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(part), "r"(r));
+                int v = 0;
+#pragma unroll
+                for (int a = 0; a < NACC; ++a)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < NT; ++j)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e, ++v) {
+                                double x;
+                                asm volatile("ld.shared::cluster.f64 %0, [%1];"
+                                             : "=d"(x)
+                                             : "r"(remote + v * CT * 8)
+                                             : "memory");
+                                acc[a][i][j][e] += x;
+                            }
+            }
+        }
+        static_assert(NV * CT * 8 <= C::STAGES * C::STAGE, "partials must fit the pipeline buffers");
+        cluster_sync();  // partner ranks keep their shared memory alive until rank 0 has read it
+        if (rank != 0) return;
+    }
+
     const size_t plane = static_cast<size_t>(M) * N;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -783,10 +862,27 @@ static int configure_ws_t() {
 template <bool THREE_M, bool SUMPLANE>
 static int launch_ws_t(const GemmArgs& a, void* stream) {
     using C = WsCfg<THREE_M, SUMPLANE>;
-    dim3 grid(a.N / C::BN, a.M / C::BM);
-    zgemm_ws_kernel<THREE_M, SUMPLANE><<<grid, C::THREADS, C::SMEM, static_cast<cudaStream_t>(stream)>>>(
-        *static_cast<const CUtensorMap*>(a.tmap), *a.layer, a.out, a.M, a.N);
-    return static_cast<int>(cudaGetLastError());
+    const int splits = a.splits > 1 ? a.splits : 1;
+    if (splits == 1) {
+        dim3 grid(a.N / C::BN, a.M / C::BM);
+        zgemm_ws_kernel<THREE_M, SUMPLANE><<<grid, C::THREADS, C::SMEM, static_cast<cudaStream_t>(stream)>>>(
+            *static_cast<const CUtensorMap*>(a.tmap), *a.layer, a.out, a.M, a.N);
+        return static_cast<int>(cudaGetLastError());
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.N / C::BN, a.M / C::BM, splits);
+    cfg.blockDim = dim3(C::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = splits;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, zgemm_ws_kernel<THREE_M, SUMPLANE>,
+                                               *static_cast<const CUtensorMap*>(a.tmap), *a.layer, a.out, a.M, a.N));
 }
 
 int gemm_tile_rows(int tile) {

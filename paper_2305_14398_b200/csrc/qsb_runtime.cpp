@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -248,6 +249,7 @@ struct qsb_plan {
     int M = 0;
     int N = 0;
     int tile = qsb::kTile32x32;
+    int splits = 1;  // K2 split-K cluster size (warp-specialised tiles)
     int planes = 2;  // V buffer planes: re, im (+ re+im for the 3M sum-plane tile)
     bool small = false;
     qsbh::Buffers b;
@@ -263,47 +265,127 @@ struct qsb_plan {
 
 namespace {
 
+// Registered matrices of the circuit, uploaded once per plan. A matrix with at
+// most one nonzero per row (a DJ oracle) goes up as per-row (column, value)
+// (kBlockMonomial): the generator reads 2^span entries instead of 4^span.
 void upload_tables(qsb_plan* p, const qsb_circuit* c) {
-    size_t total = 0;
-    std::vector<size_t> off(static_cast<size_t>(std::max(c->n_functions, 0)), 0);
+    const size_t nf = static_cast<size_t>(std::max(c->n_functions, 0));
+    std::vector<size_t> off(nf, 0);
+    std::vector<char> mono(nf, 0);
+    std::vector<std::vector<int32_t>> cols(nf);
+    std::vector<std::vector<double>> vre(nf), vim(nf);
+    size_t total = 0;  // in doubles
+    const bool force_dense = std::getenv("QSB_DENSE_TABLES") != nullptr;  // tests: exercise both layouts
     for (int f : p->cc.used_functions) {
+        const qsb_function& fn = c->functions[f];
+        const size_t d = static_cast<size_t>(fn.dim);
+        bool is_mono = !force_dense;
+        cols[f].assign(d, -1);
+        vre[f].assign(d, 0.0);
+        vim[f].assign(d, 0.0);
+        for (size_t r = 0; r < d && is_mono; ++r)
+            for (size_t k = 0; k < d; ++k) {
+                const double a = fn.re[r * d + k], b = fn.im[r * d + k];
+                if (a == 0.0 && b == 0.0) continue;
+                if (cols[f][r] >= 0) {
+                    is_mono = false;
+                    break;
+                }
+                cols[f][r] = static_cast<int32_t>(k);
+                vre[f][r] = a;
+                vim[f][r] = b;
+            }
+        mono[f] = is_mono;
         off[f] = total;
-        total += 2 * static_cast<size_t>(c->functions[f].dim) * c->functions[f].dim;
+        total += is_mono ? 2 * d + (d + 1) / 2 : 2 * d * d;
     }
     if (total == 0) return;
     p->b.tables.ensure(total * sizeof(double));
     double* base = p->b.tables.as<double>();
     for (int f : p->cc.used_functions) {
-        const size_t d2 = static_cast<size_t>(c->functions[f].dim) * c->functions[f].dim;
-        cuda_check(cudaMemcpy(base + off[f], c->functions[f].re, d2 * 8, cudaMemcpyHostToDevice), "upload function");
-        cuda_check(cudaMemcpy(base + off[f] + d2, c->functions[f].im, d2 * 8, cudaMemcpyHostToDevice),
-                   "upload function");
+        const qsb_function& fn = c->functions[f];
+        const size_t d = static_cast<size_t>(fn.dim);
+        if (mono[f]) {
+            cuda_check(cudaMemcpy(base + off[f], vre[f].data(), d * 8, cudaMemcpyHostToDevice), "upload function");
+            cuda_check(cudaMemcpy(base + off[f] + d, vim[f].data(), d * 8, cudaMemcpyHostToDevice), "upload function");
+            cuda_check(cudaMemcpy(base + off[f] + 2 * d, cols[f].data(), d * 4, cudaMemcpyHostToDevice),
+                       "upload function");
+        } else {
+            const size_t d2 = d * d;
+            cuda_check(cudaMemcpy(base + off[f], fn.re, d2 * 8, cudaMemcpyHostToDevice), "upload function");
+            cuda_check(cudaMemcpy(base + off[f] + d2, fn.im, d2 * 8, cudaMemcpyHostToDevice), "upload function");
+        }
     }
     auto patch = [&](qsb::LayerDesc& d) {
         for (int i = 0; i < d.nblocks; ++i) {
             qsb::BlockDesc& blk = d.blocks[i];
             if (blk.kind != qsb::kBlockTable) continue;
             const int f = static_cast<int>(reinterpret_cast<intptr_t>(blk.t_im));
-            const size_t d2 = static_cast<size_t>(c->functions[f].dim) * c->functions[f].dim;
-            blk.t_re = base + off[f];
-            blk.t_im = base + off[f] + d2;
+            const size_t dim = static_cast<size_t>(c->functions[f].dim);
+            if (mono[f]) {
+                blk.kind = qsb::kBlockMonomial;
+                blk.t_re = base + off[f];
+                blk.t_im = base + off[f] + dim;
+                blk.t_col = reinterpret_cast<const int32_t*>(base + off[f] + 2 * dim);
+            } else {
+                blk.t_re = base + off[f];
+                blk.t_im = base + off[f] + dim * dim;
+            }
         }
     };
     for (auto& d : p->cc.app) patch(d);
 }
 
-int pick_tile(int M, int N, int gemm_mode) {
+// Split-K factor for a warp-specialised tile grid of T output tiles (one CTA
+// per SM): the cluster size s in {1, 2, 4} whose T*s CTAs fill the last wave of
+// 148 SMs best; ties go to the smaller s. QSB_SPLITK forces it (tests: a fixed
+// summation order across shard sizes).
+int pick_splits(int64_t T, int KT) {
+    const char* force = std::getenv("QSB_SPLITK");
+    if (force && *force) {
+        const int s = std::atoi(force);
+        if ((s == 1 || s == 2 || s == 4) && KT / s >= 4) return s;
+        return 1;
+    }
+    const double sms = 148.0;
+    int best = 1;
+    double best_eff = 0.0;
+    for (int s = 1; s <= 4; s *= 2) {
+        if (KT / s < 8) break;  // keep the pipeline busy in every rank
+        const double waves = static_cast<double>(T * s) / sms;
+        const double eff = waves / std::ceil(waves);
+        if (eff > best_eff + 0.03) {
+            best_eff = eff;
+            best = s;
+        }
+    }
+    return best;
+}
+
+int pick_tile(int M, int N, int gemm_mode, int* splits) {
     const int sms = 148;
+    *splits = 1;
     const char* force = std::getenv("QSB_TILE");  // debugging / tests: force a tile variant
     if (force && *force) {
         const int t = std::atoi(force);
-        if (t >= 0 && t <= qsb::kTileWs3MS && M % qsb::gemm_tile_rows(t) == 0 && N % qsb::gemm_tile_cols(t) == 0)
+        if (t >= 0 && t <= qsb::kTileWs3MS && M % qsb::gemm_tile_rows(t) == 0 && N % qsb::gemm_tile_cols(t) == 0) {
+            if (t >= qsb::kTileWs4M)
+                *splits = pick_splits(static_cast<int64_t>(M / qsb::gemm_tile_rows(t)) * (N / qsb::gemm_tile_cols(t)),
+                                      N / 16);
             return t;
+        }
     }
     const bool three = gemm_mode != QSB_GEMM_4M;
     const int ws = three ? qsb::kTileWs3MS : qsb::kTileWs4M;
     const int wr = qsb::gemm_tile_rows(ws), wc = qsb::gemm_tile_cols(ws);
-    if (M % wr == 0 && N % wc == 0 && (M / wr) * (N / wc) >= 2 * sms) return ws;
+    if (M % wr == 0 && N % wc == 0) {
+        const int64_t T = static_cast<int64_t>(M / wr) * (N / wc);
+        const int s = pick_splits(T, N / 16);
+        if (T * s >= 2 * sms) {
+            *splits = s;
+            return ws;
+        }
+    }
     if (M % 64 == 0 && N % 64 == 0 && (M / 64) * (N / 64) >= sms) return qsb::kTile64x64;
     if (M % wr == 0 && N % wc == 0 && (M / wr) * (N / wc) >= sms) return ws;
     return qsb::kTile32x32;
@@ -350,7 +432,7 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     if (row_begin + row_count > p->eff_begin + M)
         raise(QSB_ERR_ARGUMENT, "row shard [%lld, +%lld) is not contained in one aligned window of %lld rows",
               static_cast<long long>(row_begin), static_cast<long long>(row_count), static_cast<long long>(M));
-    p->tile = p->small ? qsb::kTile32x32 : pick_tile(p->M, p->N, h->gemm_mode);
+    p->tile = p->small ? qsb::kTile32x32 : pick_tile(p->M, p->N, h->gemm_mode, &p->splits);
     if (p->tile == qsb::kTileWs3MS) {
         // the sum plane costs 50% more V memory: fall back to in-register sums if it does not fit
         size_t free_b = 0, total_b = 0;
@@ -404,6 +486,7 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     in.gemm_flops = 8.0 * static_cast<double>(p->M) * static_cast<double>(N) * static_cast<double>(N) * gemms;
     in.expand_bytes = p->small ? 0.0 : 8.0 * p->planes * static_cast<double>(p->M) * static_cast<double>(N);
     in.gemm_tile = p->small ? -1 : p->tile;
+    in.gemm_splits = p->small ? 1 : p->splits;
     in.v_planes = p->planes;
     return p;
 }
@@ -435,7 +518,7 @@ void enqueue(qsb_plan* p, cudaStream_t s) {
     if (ev) cuda_check(cudaEventRecord(p->ev[1], s), "event");
     int cur = 0;
     for (size_t i = 1; i < p->chain.size(); ++i) {
-        qsb::GemmArgs a{&p->tmap[cur], &p->chain[i], p->b.v[1 - cur].as<double>(), p->M, p->N};
+        qsb::GemmArgs a{&p->tmap[cur], &p->chain[i], p->b.v[1 - cur].as<double>(), p->M, p->N, p->splits};
         cuda_check(qsb::launch_zgemm(a, p->tile, p->h->gemm_mode, s), "zgemm_gen_kernel");
         cur ^= 1;
     }
