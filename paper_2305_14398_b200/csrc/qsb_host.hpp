@@ -115,6 +115,7 @@ struct Buffers {
     DevBuf tables;   // registered function matrices
     DevBuf p;        // probabilities
     DevBuf partial;  // reduction partials + norm
+    DevBuf lmat;     // dense path: a materialised (transposed) layer operator for K2's TMA B operand
 };
 
 }  // namespace qsbh

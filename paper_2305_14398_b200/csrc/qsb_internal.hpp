@@ -41,6 +41,10 @@ struct BlockDesc {
     const double* t_re; // table: (2^span)^2 row-major planes; monomial: 2^span row values
     const double* t_im;
     const int32_t* t_col;  // monomial: column of each row's nonzero, or -1
+    int32_t mono;          // row -> column map of a monomial block: 0 keep the block's bits
+                           // (diagonal), 1 flip the target bit (anti-diagonal u; controlled:
+                           // only where the control bit is set), 2 look up t_col
+    int32_t pad;
 };
 
 struct LayerDesc {
@@ -49,6 +53,9 @@ struct LayerDesc {
     int32_t real;       // every block entry has an exactly-zero imaginary part
     uint32_t zmask;     // bits on which r and c must agree for a nonzero entry:
                         // identity bits + every controlled block's bits except its target
+    int32_t monomial;   // every block is monomial: each operator row has one nonzero
+                        // (diagonal / permutation layers: CR, CNOT, X, DJ oracles)
+    int32_t pad;
     BlockDesc blocks[kMaxBlocks];
 };
 
@@ -59,6 +66,8 @@ struct GemmArgs {
     double* out;             // [2][M][N]
     int M;
     int N;
+    const void* tmap_b = nullptr;  // warp-specialised tiles: CUtensorMap of a materialised
+                                   // (transposed) operator; null = generate B in shared memory
     int splits = 1;          // warp-specialised tiles: K split over a thread-block cluster of this
                              // size (1, 2, 4); partial accumulators are summed through
                              // distributed shared memory in rank order (deterministic)
@@ -68,6 +77,9 @@ int launch_expand(const LayerDesc& layer, uint32_t row_begin, int M, int N, doub
                   void* stream);
 int gemm_tile_planes(int tile);  // planes of the V buffers a tile variant reads/writes (2, or 3 with Vr+Vi)
 int launch_zgemm(const GemmArgs& a, int tile, int gemm_mode, void* stream);
+// K1t: transposed operator planes for a materialised B (planes 2: re, im; 3: + re+im)
+int launch_expand_t(const LayerDesc& layer, int N, double* out, int planes, void* stream);
+int gemm_tile_b_planes(int tile);
 int launch_small_circuit(const LayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, int N,
                          const double* x, double* v, double* psi, void* stream);
 int launch_matvec(const double* v, int M, int N, const double* x, double* psi, void* stream);

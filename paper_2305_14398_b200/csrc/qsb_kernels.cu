@@ -103,6 +103,29 @@ __device__ __forceinline__ void layer_entry(const LayerDesc& d, uint32_t r, uint
     vi = ai;
 }
 
+// Column of the single nonzero of row r of a monomial layer (or -1 if the row
+// is zero): each block maps the row's bits to the column's bits.
+__device__ __forceinline__ int64_t mono_col(const LayerDesc& d, uint32_t r) {
+    uint32_t c = r;
+    for (int b = 0; b < d.nblocks; ++b) {
+        const BlockDesc& B = d.blocks[b];
+        const uint32_t rb = (r >> B.shift) & B.mask;
+        uint32_t cb = rb;
+        if (B.mono == 1) {
+            if (B.kind == kBlockGate)
+                cb = rb ^ 1u;
+            else if (rb & B.cmask)
+                cb = rb ^ B.tmask;  // controlled_unitary (gates.cpp:94-107) with an anti-diagonal u
+        } else if (B.mono == 2) {
+            const int32_t t = __ldg(B.t_col + rb);
+            if (t < 0) return -1;
+            cb = static_cast<uint32_t>(t);
+        }
+        c = (c & ~(B.mask << B.shift)) | (cb << B.shift);
+    }
+    return static_cast<int64_t>(c);
+}
+
 // Continue the left fold from block `b` with the running value (ar, ai).
 // Real layers multiply real parts only: (a, 0) * (e, 0) = (a*e - 0*0, a*0 + 0*e)
 // = (a*e, +-0), so the real product is bit-identical to the complex one.
@@ -585,10 +608,14 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-template <bool THREE_M, bool SUMPLANE>
+// MAT_B: the operator was materialised (transposed, [planes][N][N], by
+// expand_t_kernel) and B tiles arrive by TMA like A — no FP64 generation work
+// in the producer, whose FP64 instructions would otherwise queue behind DMMA on
+// the shared FP64 pipe (used for dense, non-monomial layers such as H on every qubit).
+template <bool THREE_M, bool SUMPLANE, bool MAT_B>
 __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
-    zgemm_ws_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ LayerDesc layer,
-                    double* __restrict__ out, int M, int N) {
+    zgemm_ws_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ LayerDesc layer, double* __restrict__ out, int M, int N) {
     using C = WsCfg<THREE_M, SUMPLANE>;
     constexpr int BM = C::BM, BN = C::BN;
     extern __shared__ uint8_t smem_raw[];
@@ -629,16 +656,82 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
             const uint32_t stage = sBase + s * C::STAGE;
             const uint32_t tma_bar = sFull + 8 * s;
             const int ktg = kt0 + kt;  // global k-tile
+            const uint32_t bBase = stage + C::A_BYTES;
+            if (MAT_B) {
+                if (ptid == 0) {
+                    mbar_expect_tx(tma_bar, C::A_TMA_BYTES + C::B_BYTES);
+                    tma_load_3d(stage, &tmA, tma_bar, ktg * C::BK, m0, 0);
+                    tma_load_3d(bBase, &tmB, tma_bar, ktg * C::BK, n0, 0);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(sFull + 8 * s);
+                continue;
+            }
             if (ptid == 0) {
                 mbar_expect_tx(tma_bar, C::A_TMA_BYTES);
                 tma_load_3d(stage, &tmA, tma_bar, ktg * C::BK, m0, 0);
             }
-            const uint32_t bBase = stage + C::A_BYTES;
             const TilePrefix tp = tile_prefix<C::LOWBITS>(layer, static_cast<uint32_t>(ktg * C::BK),
                                                           static_cast<uint32_t>(n0));
             if (tp.zero) {
                 // whole operator tile is zero: clear the B planes of this stage
                 for (int o = ptid * 16; o < C::B_BYTES; o += 16 * 32 * C::PRODUCER_WARPS) sts128(bBase + o, 0.0, 0.0);
+            } else if (layer.monomial) {
+                // one nonzero per operator row: thread = (line n, half of the 8 k-chunks);
+                // an entry is nonzero only where the row's column is this line's
+                static_assert(32 * C::PRODUCER_WARPS == 2 * BN, "two producer threads per tile line");
+                const int n = ptid & (BN - 1);
+                const int half = ptid / BN;
+                const uint32_t col = static_cast<uint32_t>(n0 + n);
+                // FP64 arithmetic only for the (at most BK) hits: the FP64 pipe is the DMMA pipe.
+                // Columns of this thread's 8 rows first (single-block layers — CNOT, CR, X,
+                // DJ oracle — with independent loads), then the entries of the hits.
+                int64_t cols[8];
+                const uint32_t rbase = static_cast<uint32_t>(ktg * C::BK + 8 * half);
+                if (layer.nblocks == 1) {
+                    const BlockDesc& B = layer.blocks[0];
+                    const uint32_t keep = ~(B.mask << B.shift);
+                    int32_t cb[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const uint32_t rb = ((rbase + q) >> B.shift) & B.mask;
+                        cb[q] = static_cast<int32_t>(rb);
+                        if (B.mono == 2) {
+                            cb[q] = __ldg(B.t_col + rb);
+                        } else if (B.mono == 1) {
+                            if (B.kind == kBlockGate)
+                                cb[q] = static_cast<int32_t>(rb ^ 1u);
+                            else if (rb & B.cmask)
+                                cb[q] = static_cast<int32_t>(rb ^ B.tmask);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        cols[q] = cb[q] < 0 ? -1
+                                            : static_cast<int64_t>(((rbase + q) & keep) |
+                                                                   (static_cast<uint32_t>(cb[q]) << B.shift));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) cols[q] = mono_col(layer, rbase + q);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int pch = half * 4 + q;  // k = 2 pch, 2 pch + 1
+                    const uint32_t r0 = rbase + 2 * q;
+                    double v0r = 0.0, v0i = 0.0, v1r = 0.0, v1i = 0.0, s0 = 0.0, s1 = 0.0;
+                    if (cols[2 * q] == static_cast<int64_t>(col)) {
+                        layer_entry(layer, r0, col, v0r, v0i);
+                        if (THREE_M) s0 = __dadd_rn(v0r, v0i);
+                    }
+                    if (cols[2 * q + 1] == static_cast<int64_t>(col)) {
+                        layer_entry(layer, r0 + 1, col, v1r, v1i);
+                        if (THREE_M) s1 = __dadd_rn(v1r, v1i);
+                    }
+                    const uint32_t off = n * 128 + ((pch ^ (n & 7)) << 4);
+                    sts128(bBase + off, v0r, v1r);
+                    sts128(bBase + BN * 128 + off, v0i, v1i);
+                    if (THREE_M) sts128(bBase + 2 * BN * 128 + off, s0, s1);
+                }
             } else {
                 constexpr int EB = 4;  // elements per batch = 2 (k, k+1) pairs
 #pragma unroll
@@ -661,9 +754,14 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
                         const uint32_t off = nn[h] * 128 + ((pp[h] ^ (nn[h] & 7)) << 4);
                         sts128(bBase + off, vr[2 * h], vr[2 * h + 1]);
                         sts128(bBase + BN * 128 + off, vi[2 * h], vi[2 * h + 1]);
-                        if (THREE_M)
-                            sts128(bBase + 2 * BN * 128 + off, __dadd_rn(vr[2 * h], vi[2 * h]),
-                                   __dadd_rn(vr[2 * h + 1], vi[2 * h + 1]));
+                        if (THREE_M) {
+                            // real layers: Br + Bi = Br (adding an exact zero; no FP64 op)
+                            if (layer.real)
+                                sts128(bBase + 2 * BN * 128 + off, vr[2 * h], vr[2 * h + 1]);
+                            else
+                                sts128(bBase + 2 * BN * 128 + off, __dadd_rn(vr[2 * h], vi[2 * h]),
+                                       __dadd_rn(vr[2 * h + 1], vi[2 * h + 1]));
+                        }
                     }
                 }
             }
@@ -775,98 +873,121 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
         if (lane == 0) mbar_arrive(sEmpty + 8 * s);
     }
 
+    // Output fragment (i, j) of this warp: combine the accumulators (3M: Cr = T1 - T2,
+    // Ci = T3 - T1 - T2) and store re, im (and re + im for the next 3M GEMM).
+    const size_t plane = static_cast<size_t>(M) * N;
+    auto store = [&](int i, int j, const double (&f)[NACC][2]) {
+        const int row = m0 + wm * 32 + i * 8 + g;
+        const int col = n0 + wn * C::WT_N + j * 8 + 2 * t;
+        const size_t o = static_cast<size_t>(row) * N + col;
+        double r0, r1, i0, i1;
+        if (THREE_M) {
+            r0 = f[0][0] - f[1][0];
+            r1 = f[0][1] - f[1][1];
+            i0 = f[2][0] - f[0][0] - f[1][0];
+            i1 = f[2][1] - f[0][1] - f[1][1];
+        } else {
+            r0 = f[0][0];
+            r1 = f[0][1];
+            i0 = f[1][0];
+            i1 = f[1][1];
+        }
+        *reinterpret_cast<double2*>(out + o) = make_double2(r0, r1);
+        *reinterpret_cast<double2*>(out + plane + o) = make_double2(i0, i1);
+        if (SUMPLANE)
+            *reinterpret_cast<double2*>(out + 2 * plane + o) = make_double2(__dadd_rn(r0, i0), __dadd_rn(r1, i1));
+    };
+
     if (splits > 1) {
-        // Deterministic split-K: every rank parks its partial accumulators in its
-        // own shared memory ([value][consumer thread]); rank 0 adds ranks 1..s-1
-        // in order through distributed shared memory, then writes the tile.
-        constexpr int NV = NACC * 4 * NT * 2;
+        // Deterministic split-K: every rank parks its partial accumulators in its own
+        // shared memory ([value][consumer thread]); rank r then finishes the m8 row
+        // blocks i with i * splits / 4 == r, summing the partials of ranks 0..s-1 in
+        // that fixed order through distributed shared memory, and stores them.
         constexpr int CT = 32 * C::CONSUMER_WARPS;
+        constexpr int NV = NACC * 4 * NT * 2;
+        static_assert(NV * CT * 8 <= C::STAGES * C::STAGE, "partials must fit the pipeline buffers");
         asm volatile("bar.sync 1, %0;" ::"n"(CT) : "memory");  // all consumers are past the last stage
         const uint32_t part = sBase + static_cast<uint32_t>(tid) * 8;
-        {
-            int v = 0;
+        auto vidx = [](int a, int i, int j, int e) { return ((a * 4 + i) * NT + j) * 2 + e; };
 #pragma unroll
-            for (int a = 0; a < NACC; ++a)
+        for (int a = 0; a < NACC; ++a)
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int j = 0; j < NT; ++j)
+                for (int j = 0; j < NT; ++j)
 #pragma unroll
-                        for (int e = 0; e < 2; ++e, ++v)
-                            asm volatile("st.shared.f64 [%0], %1;" ::"r"(part + v * CT * 8), "d"(acc[a][i][j][e])
-                                         : "memory");
-        }
+                    for (int e = 0; e < 2; ++e)
+                        asm volatile("st.shared.f64 [%0], %1;" ::"r"(part + vidx(a, i, j, e) * CT * 8),
+                                     "d"(acc[a][i][j][e])
+                                     : "memory");
         cluster_sync();
-        if (rank == 0) {
-            for (int r = 1; r < splits; ++r) {
-                uint32_t remote;
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(part), "r"(r));
-                int v = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if ((i * splits) / 4 != rank) continue;
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                double f[NACC][2];
 #pragma unroll
                 for (int a = 0; a < NACC; ++a)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
+                    for (int e = 0; e < 2; ++e) f[a][e] = 0.0;
+                for (int q = 0; q < splits; ++q) {
+                    uint32_t src;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(src) : "r"(part), "r"(q));
 #pragma unroll
-                        for (int j = 0; j < NT; ++j)
+                    for (int a = 0; a < NACC; ++a)
 #pragma unroll
-                            for (int e = 0; e < 2; ++e, ++v) {
-                                double x;
-                                asm volatile("ld.shared::cluster.f64 %0, [%1];"
-                                             : "=d"(x)
-                                             : "r"(remote + v * CT * 8)
-                                             : "memory");
-                                acc[a][i][j][e] += x;
-                            }
+                        for (int e = 0; e < 2; ++e) {
+                            double x;
+                            asm volatile("ld.shared::cluster.f64 %0, [%1];"
+                                         : "=d"(x)
+                                         : "r"(src + vidx(a, i, j, e) * CT * 8)
+                                         : "memory");
+                            f[a][e] = q == 0 ? x : f[a][e] + x;
+                        }
+                }
+                store(i, j, f);
             }
         }
-        static_assert(NV * CT * 8 <= C::STAGES * C::STAGE, "partials must fit the pipeline buffers");
-        cluster_sync();  // partner ranks keep their shared memory alive until rank 0 has read it
-        if (rank != 0) return;
+        cluster_sync();  // every rank keeps its shared memory alive until all have read it
+        return;
     }
 
-    const size_t plane = static_cast<size_t>(M) * N;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int row = m0 + wm * 32 + i * 8 + g;
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
-            const int col = n0 + wn * C::WT_N + j * 8 + 2 * t;
-            const size_t o = static_cast<size_t>(row) * N + col;
-            double r0, r1, i0, i1;
-            if (THREE_M) {
-                r0 = acc[0][i][j][0] - acc[1][i][j][0];
-                r1 = acc[0][i][j][1] - acc[1][i][j][1];
-                i0 = acc[2][i][j][0] - acc[0][i][j][0] - acc[1][i][j][0];
-                i1 = acc[2][i][j][1] - acc[0][i][j][1] - acc[1][i][j][1];
-            } else {
-                r0 = acc[0][i][j][0];
-                r1 = acc[0][i][j][1];
-                i0 = acc[1][i][j][0];
-                i1 = acc[1][i][j][1];
+            double f[NACC][2];
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) {
+                f[a][0] = acc[a][i][j][0];
+                f[a][1] = acc[a][i][j][1];
             }
-            *reinterpret_cast<double2*>(out + o) = make_double2(r0, r1);
-            *reinterpret_cast<double2*>(out + plane + o) = make_double2(i0, i1);
-            if (SUMPLANE)
-                *reinterpret_cast<double2*>(out + 2 * plane + o) = make_double2(__dadd_rn(r0, i0), __dadd_rn(r1, i1));
+            store(i, j, f);
         }
-    }
 }
 
 template <bool THREE_M, bool SUMPLANE>
 static int configure_ws_t() {
-    return static_cast<int>(cudaFuncSetAttribute(zgemm_ws_kernel<THREE_M, SUMPLANE>,
+    int e = static_cast<int>(cudaFuncSetAttribute(zgemm_ws_kernel<THREE_M, SUMPLANE, false>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  WsCfg<THREE_M, SUMPLANE>::SMEM));
+    if (e) return e;
+    return static_cast<int>(cudaFuncSetAttribute(zgemm_ws_kernel<THREE_M, SUMPLANE, true>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  WsCfg<THREE_M, SUMPLANE>::SMEM));
 }
 
-template <bool THREE_M, bool SUMPLANE>
+template <bool THREE_M, bool SUMPLANE, bool MAT_B>
 static int launch_ws_t(const GemmArgs& a, void* stream) {
     using C = WsCfg<THREE_M, SUMPLANE>;
     const int splits = a.splits > 1 ? a.splits : 1;
+    const CUtensorMap& tmA = *static_cast<const CUtensorMap*>(a.tmap);
+    const CUtensorMap& tmB = MAT_B ? *static_cast<const CUtensorMap*>(a.tmap_b) : tmA;
     if (splits == 1) {
         dim3 grid(a.N / C::BN, a.M / C::BM);
-        zgemm_ws_kernel<THREE_M, SUMPLANE><<<grid, C::THREADS, C::SMEM, static_cast<cudaStream_t>(stream)>>>(
-            *static_cast<const CUtensorMap*>(a.tmap), *a.layer, a.out, a.M, a.N);
+        zgemm_ws_kernel<THREE_M, SUMPLANE, MAT_B><<<grid, C::THREADS, C::SMEM, static_cast<cudaStream_t>(stream)>>>(
+            tmA, tmB, *a.layer, a.out, a.M, a.N);
         return static_cast<int>(cudaGetLastError());
     }
     cudaLaunchConfig_t cfg = {};
@@ -881,9 +1002,47 @@ static int launch_ws_t(const GemmArgs& a, void* stream) {
     attr[0].val.clusterDim.z = splits;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return static_cast<int>(cudaLaunchKernelEx(&cfg, zgemm_ws_kernel<THREE_M, SUMPLANE>,
-                                               *static_cast<const CUtensorMap*>(a.tmap), *a.layer, a.out, a.M, a.N));
+    return static_cast<int>(
+        cudaLaunchKernelEx(&cfg, zgemm_ws_kernel<THREE_M, SUMPLANE, MAT_B>, tmA, tmB, *a.layer, a.out, a.M, a.N));
 }
+
+template <bool THREE_M, bool SUMPLANE>
+static int launch_ws_any(const GemmArgs& a, void* stream) {
+    return a.tmap_b ? launch_ws_t<THREE_M, SUMPLANE, true>(a, stream) : launch_ws_t<THREE_M, SUMPLANE, false>(a, stream);
+}
+
+// K1t: the layer operator transposed, Lt[p][n][k] = L[k][n] for planes re, im
+// (and re + im when planes == 3): the TMA source of a materialised B operand.
+// Entries are layer_entry's (bit-exact); consecutive threads write consecutive k.
+__global__ void __launch_bounds__(256) expand_t_kernel(const __grid_constant__ LayerDesc d, int N,
+                                                       double* __restrict__ out, int planes) {
+    const size_t plane = static_cast<size_t>(N) * N;
+    const size_t pairs = plane / 2;
+    const uint32_t half_n = static_cast<uint32_t>(N) / 2;
+    for (size_t p = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; p < pairs;
+         p += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const uint32_t n = static_cast<uint32_t>(p / half_n);
+        const uint32_t k = static_cast<uint32_t>(p % half_n) * 2;
+        double r0, i0, r1, i1;
+        layer_entry(d, k, n, r0, i0);
+        layer_entry(d, k + 1, n, r1, i1);
+        reinterpret_cast<double2*>(out)[p] = make_double2(r0, r1);
+        reinterpret_cast<double2*>(out + plane)[p] = make_double2(i0, i1);
+        if (planes == 3)
+            reinterpret_cast<double2*>(out + 2 * plane)[p] = make_double2(__dadd_rn(r0, i0), __dadd_rn(r1, i1));
+    }
+}
+
+int launch_expand_t(const LayerDesc& layer, int N, double* out, int planes, void* stream) {
+    const size_t pairs = static_cast<size_t>(N) * N / 2;
+    int blocks = static_cast<int>((pairs + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks < 1) blocks = 1;
+    expand_t_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(layer, N, out, planes);
+    return static_cast<int>(cudaGetLastError());
+}
+
+int gemm_tile_b_planes(int tile) { return tile == kTileWs3MS || tile == kTileWs3M ? 3 : 2; }
 
 int gemm_tile_rows(int tile) {
     switch (tile) {
@@ -925,9 +1084,9 @@ static int launch_zgemm_t(const GemmArgs& a, void* stream) {
 
 int launch_zgemm(const GemmArgs& a, int tile, int /*gemm_mode*/, void* stream) {
     switch (tile) {
-    case kTileWs4M: return launch_ws_t<false, false>(a, stream);
-    case kTileWs3M: return launch_ws_t<true, false>(a, stream);
-    case kTileWs3MS: return launch_ws_t<true, true>(a, stream);
+    case kTileWs4M: return launch_ws_any<false, false>(a, stream);
+    case kTileWs3M: return launch_ws_any<true, false>(a, stream);
+    case kTileWs3MS: return launch_ws_any<true, true>(a, stream);
     case kTile128x64: return launch_zgemm_t<128, 64>(a, stream);
     case kTile64x64: return launch_zgemm_t<64, 64>(a, stream);
     default: return launch_zgemm_t<32, 32>(a, stream);

@@ -226,6 +226,31 @@ Compiled compile(const qsb_circuit* c) {
     return out;
 }
 
+// Monomial layers (one nonzero per operator row): the K2 producer generates
+// their tiles as zeros plus the at most BK nonzeros whose column falls in the tile.
+void set_monomial(qsb::LayerDesc& d) {
+    bool mono = d.nblocks > 0;
+    for (int i = 0; i < d.nblocks; ++i) {
+        qsb::BlockDesc& b = d.blocks[i];
+        const bool diag = b.u_re[1] == 0.0 && b.u_im[1] == 0.0 && b.u_re[2] == 0.0 && b.u_im[2] == 0.0;
+        const bool anti = b.u_re[0] == 0.0 && b.u_im[0] == 0.0 && b.u_re[3] == 0.0 && b.u_im[3] == 0.0;
+        if (b.kind == qsb::kBlockGate || b.kind == qsb::kBlockControlled) {
+            if (diag) {
+                b.mono = 0;
+            } else if (anti) {
+                b.mono = 1;
+            } else {
+                mono = false;
+            }
+        } else if (b.kind == qsb::kBlockMonomial) {
+            b.mono = 2;
+        } else {
+            mono = false;
+        }
+    }
+    d.monomial = (mono && !std::getenv("QSB_NO_MONOMIAL")) ? 1 : 0;  // env: tests exercise the general path
+}
+
 qsb::LayerDesc identity_layer(int n) {
     qsb::LayerDesc d;
     std::memset(&d, 0, sizeof d);
@@ -250,6 +275,8 @@ struct qsb_plan {
     int N = 0;
     int tile = qsb::kTile32x32;
     int splits = 1;  // K2 split-K cluster size (warp-specialised tiles)
+    std::vector<char> mat;  // chain[i] (i >= 1) is materialised by K1t and streamed to K2 by TMA
+    CUtensorMap tmap_b;     // the materialised operator ([planes][N][N], transposed)
     int planes = 2;  // V buffer planes: re, im (+ re+im for the 3M sum-plane tile)
     bool small = false;
     qsbh::Buffers b;
@@ -458,6 +485,46 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     p->chain.clear();
     for (auto it = p->cc.app.rbegin(); it != p->cc.app.rend(); ++it)
         if (it->nblocks != 0) p->chain.push_back(*it);
+    for (auto& d : p->chain) set_monomial(d);
+    // Dense, non-monomial layers whose generation would put several FP64 products
+    // per element on the producer warps (they queue behind DMMA on the shared FP64
+    // pipe) are materialised once by K1t and streamed to K2 by TMA instead.
+    p->mat.assign(p->chain.size(), 0);
+    if (!p->small && p->tile >= qsb::kTileWs4M) {
+        const char* env = std::getenv("QSB_MATERIALIZE");  // "0" never, "1" every layer (tests)
+        const int force = env && *env ? std::atoi(env) : -1;
+        bool any = false;
+        for (size_t i = 1; i < p->chain.size(); ++i) {
+            const qsb::LayerDesc& d = p->chain[i];
+            bool m;
+            if (force >= 0) {
+                m = force == 1;
+            } else if (h->flags & QSB_FLAG_MATERIALIZE) {
+                m = true;
+            } else {
+                int low = 0;
+                for (int b = 0; b < d.nblocks; ++b)
+                    if (d.blocks[b].shift < 6) low += d.blocks[b].kind == qsb::kBlockGate ? 1 : 4;
+                const double frac = std::ldexp(1.0, -__builtin_popcount(d.zmask >> 6));
+                m = !d.monomial && frac * low >= 1.0;
+            }
+            p->mat[i] = m ? 1 : 0;
+            any = any || m;
+        }
+        if (any) {
+            const int bp = qsb::gemm_tile_b_planes(p->tile);
+            const size_t bytes = static_cast<size_t>(bp) * static_cast<size_t>(N) * static_cast<size_t>(N) * 8;
+            size_t free_b = 0, total_b = 0;
+            cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+            if (static_cast<double>(bytes) < 0.9 * static_cast<double>(free_b)) {
+                p->b.lmat.ensure(bytes);
+                p->tmap_b = make_tmap(p->b.lmat.p, static_cast<int>(N), static_cast<int>(N),
+                                      qsb::gemm_tile_cols(p->tile), bp);
+            } else {
+                std::fill(p->mat.begin(), p->mat.end(), 0);  // does not fit next to V: generate instead
+            }
+        }
+    }
     if (p->chain.empty()) p->chain.push_back(identity_layer(n));
     // psi0 = |0...0> (zero_state, state.cpp:37-47)
     std::vector<double> x(2 * static_cast<size_t>(N), 0.0);
@@ -480,7 +547,7 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     in.n_layers = static_cast<int>(p->cc.app.size());
     in.n_gemms = gemms;
     in.n_identity_layers = p->n_identity;
-    in.n_launches = p->small ? 1 : 1 + gemms + 1;
+    in.n_launches = p->small ? 1 : 1 + gemms + 1 + static_cast<int>(std::count(p->mat.begin(), p->mat.end(), 1));
     in.row_begin = row_begin;
     in.row_count = row_count;
     in.gemm_flops = 8.0 * static_cast<double>(p->M) * static_cast<double>(N) * static_cast<double>(N) * gemms;
@@ -518,7 +585,13 @@ void enqueue(qsb_plan* p, cudaStream_t s) {
     if (ev) cuda_check(cudaEventRecord(p->ev[1], s), "event");
     int cur = 0;
     for (size_t i = 1; i < p->chain.size(); ++i) {
-        qsb::GemmArgs a{&p->tmap[cur], &p->chain[i], p->b.v[1 - cur].as<double>(), p->M, p->N, p->splits};
+        const bool mat = p->mat[i] != 0;
+        if (mat)
+            cuda_check(qsb::launch_expand_t(p->chain[i], p->N, p->b.lmat.as<double>(),
+                                            qsb::gemm_tile_b_planes(p->tile), s),
+                       "expand_t_kernel");
+        qsb::GemmArgs a{&p->tmap[cur], &p->chain[i], p->b.v[1 - cur].as<double>(), p->M, p->N,
+                        mat ? &p->tmap_b : nullptr, p->splits};
         cuda_check(qsb::launch_zgemm(a, p->tile, p->h->gemm_mode, s), "zgemm_gen_kernel");
         cur ^= 1;
     }

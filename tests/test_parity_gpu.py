@@ -387,3 +387,72 @@ def orc_col(flat, col):
     import oracle
 
     return oracle.Oracle().unitary_column(flat, col)
+
+
+@pytest.mark.parametrize("name,n", [("qft", 10), ("entangle", 10), ("deutsch-jozsa", 10), ("qft", 11)])
+def test_monomial_tiles_match_general_generator(monkeypatch, sim, name, n):
+    """Monomial layers (CR, CNOT, X, DJ oracle) are generated as zeros plus one
+    nonzero per operator row; the operator entries are the same bits as the
+    general generator's, so U is bit-identical with QSB_NO_MONOMIAL."""
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+
+    c, reg = q.make_named_circuit(name, n)
+    flat = native.flatten(c, reg)
+    for tile in ("3", "5"):
+        monkeypatch.setenv("QSB_TILE", tile)
+        monkeypatch.delenv("QSB_NO_MONOMIAL", raising=False)
+        a = sim.build_unitary(flat)
+        monkeypatch.setenv("QSB_NO_MONOMIAL", "1")
+        b = sim.build_unitary(flat)
+        assert bit_equal(a[0], b[0]) and bit_equal(a[1], b[1]), tile
+
+
+@pytest.mark.parametrize("tile", ["3", "4", "5"])
+@pytest.mark.parametrize("name,n", [("deutsch-jozsa", 10), ("qft", 10), ("entangle", 9)])
+def test_materialised_operator_matches_generated(monkeypatch, sim, orc, tile, name, n):
+    """A layer materialised by K1t (transposed planes) and streamed to K2 by TMA
+    carries the same operator bits as the shared-memory generator: U is
+    bit-identical (== semantics) with every layer generated, and matches the oracle."""
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+
+    monkeypatch.setenv("QSB_TILE", tile)
+    monkeypatch.setenv("QSB_SPLITK", "1")
+    c, reg = q.make_named_circuit(name, n)
+    flat = native.flatten(c, reg)
+    monkeypatch.setenv("QSB_MATERIALIZE", "1")
+    plan = sim.plan(flat)
+    assert plan.info.n_launches == 2 + 2 * plan.info.n_gemms
+    plan.close()
+    a = sim.build_unitary(flat)
+    monkeypatch.setenv("QSB_MATERIALIZE", "0")
+    b = sim.build_unitary(flat)
+    assert bit_equal(a[0], b[0]) and bit_equal(a[1], b[1])
+    for col in (0, (1 << n) - 1):
+        cr, ci = orc.unitary_column(flat, col)
+        assert rel_frob(a[0][:, col], a[1][:, col], cr, ci) <= TOL
+
+
+def test_materialise_flag_and_dense_layer_choice(sim, orc):
+    """QSB_FLAG_MATERIALIZE materialises every layer; by default only dense,
+    non-monomial layers are (DJ's H on every qubit)."""
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+    from paper_2305_14398_b200.simulator import B200UnitarySimulator
+
+    c, reg = q.make_named_circuit("deutsch-jozsa", 11)
+    flat = native.flatten(c, reg)
+    plan = sim.plan(flat)
+    assert plan.info.n_launches == 2 + plan.info.n_gemms + 1  # one layer (X + H on 10 qubits) materialised
+    plan.close()
+    mat = B200UnitarySimulator(flags=native.FLAG_MATERIALIZE)
+    plan = mat.plan(flat)
+    assert plan.info.n_launches == 2 + 2 * plan.info.n_gemms
+    plan.close()
+    a = mat.simulate_full_state(flat)
+    b = sim.simulate_full_state(flat)
+    assert rel_frob(a.re, a.im, b.re, b.im) <= TOL
+    re, im = orc.fsv(flat)
+    assert rel_frob(a.re, a.im, re, im) <= TOL
+    mat.close()
