@@ -59,6 +59,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--gemm-mode", default="auto", choices=["auto", "4m", "3m"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--virtual-ranks", type=int, default=1,
+                    help="with one GPU: time only rank 0's row block of a G-way shard (the work each of G "
+                         "GPUs does, with no communication but the final psi all-gather) and report it "
+                         "as a projection next to the measured line")
     ap.add_argument("--backend", default="dense", choices=["dense", "structured", "fsv"],
                     help="dense: Algorithm 1 on the FP64 tensor cores (the headline); structured: U built by "
                          "the state-vector engine (U[:,c] = fsv(e_c)); fsv: the full-state-vector backend")
@@ -253,7 +257,8 @@ def run_ours(args):
     sim = B200UnitarySimulator(device=local, gemm_mode=mode)
     c, reg = q.make_named_circuit(name, n)
     flat = native.flatten(c, reg)
-    begin, count = row_shard(N, world, rank)
+    vr = args.virtual_ranks if world == 1 and args.virtual_ranks > 1 else 1
+    begin, count = row_shard(N, world * vr, rank)
     # A dedicated stream: every launch of the plan, the all-gather and the
     # timing events share it (the legacy default stream has handle 0).
     stream = torch.cuda.Stream()
@@ -324,7 +329,10 @@ def run_ours(args):
     job_tflops = float(tot.item()) / (ms_max * 1e-3) / 1e12
 
     # ---- e2e through the public API with host buffers ----
-    e2e_ms, h2d, d2h = e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr)
+    if vr > 1:
+        e2e_ms, h2d, d2h = None, 0, 0  # the projection times one shard, not a full circuit
+    else:
+        e2e_ms, h2d, d2h = e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr)
     if plan is not None:
         plan.close()
 
@@ -361,7 +369,17 @@ def run_ours(args):
             "gpu_launches": (info.n_launches if info else 0) * args.steps,
             "clocks": clocks,
         }
-        if world == 1 and not args.no_cpu_baseline:
+        if vr > 1:
+            line["n_gpus"] = 1
+            line["config"]["parallelism"] = f"row block 0 of {vr} (one shard on one GPU)"
+            line["projection"] = {
+                "n_gpus": vr, "ms_per_circuit": ms_max,
+                "tflops_aggregate": job_tflops * vr,
+                "fp64_peak_frac_aggregate": job_tflops / FP64_DMMA_PEAK_TFLOPS,
+                "method": f"rows [0, N/{vr}) of U timed alone on one B200: every rank does identical, "
+                          "independent work (row blocks, operators regenerated locally); excludes the "
+                          f"NCCL all-gather of psi ({16 * N // vr} bytes per rank)"}
+        if world == 1 and vr == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_sample(args.workload)
         print(json.dumps(line), flush=True)
     sim.close()
