@@ -133,7 +133,7 @@ int reg_k_default() {
     const char* e = std::getenv("QSB_SV_REG_K");  // tuning / tests
     if (e && *e) {
         const int v = std::atoi(e);
-        if (v >= 1 && v <= qsb::kSvRegMaxK) return v;
+        if (v >= 1 && v <= qsb::kSvRegDefaultK) return v;
     }
     return qsb::kSvRegDefaultK;
 }
@@ -212,14 +212,17 @@ void push_reg_batch(qsb_sv_plan* p, const std::vector<FlatOp>& flat, size_t i, s
     for (size_t q = i; q < j; ++q) {
         const FlatOp& f = flat[q];
         qsb::SvRegOp& o = rb->ops[q - i];
-        o.cls = f.cls;
         o.tb = index_of[f.tbit];
+        int cb = -1;
         if (f.cbit >= 0) {
-            if (index_of[f.cbit] >= 0)
-                o.emask = 1u << index_of[f.cbit];
-            else
+            if (index_of[f.cbit] >= 0) {
+                cb = index_of[f.cbit];
+                o.emask = 1u << cb;
+            } else {
                 o.ocmask = 1u << f.cbit;
+            }
         }
+        o.code = qsb::sv_reg_code(f.cls, o.tb, cb);
         std::memcpy(o.u_re, f.u_re, sizeof o.u_re);
         std::memcpy(o.u_im, f.u_im, sizeof o.u_im);
         if (o.tb < 0) raise(QSB_ERR_INTERNAL, "sv register batch: target outside the batch");

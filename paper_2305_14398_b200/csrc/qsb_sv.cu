@@ -224,75 +224,133 @@ __global__ void __launch_bounds__(kSvThreads) sv_batch_kernel(double* __restrict
 // Pair (e, e | 1 << TB) of a group held in registers; a control inside the
 // batch's targets is the e-space mask emask (e is a compile-time index, so the
 // predicate never forces a register array into local memory).
-template <int K, int TB, int CLS>
-__device__ __forceinline__ void reg_apply(const SvRegOp& op, double (&vr)[1 << K], double (&vi)[1 << K],
-                                          uint32_t emask) {
+// CB >= 0: the control is target bit CB of the batch (pairs with that bit clear
+// are skipped at compile time); CB == -1: no control inside the targets;
+// CB == -2: control mask op.emask tested at run time (e is a compile-time index,
+// so no predicate ever forces a register array into local memory).
+template <int K, int CLS, int CB, int TB>
+__device__ __forceinline__ void reg_apply(const SvRegOp& op, double (&vr)[1 << K], double (&vi)[1 << K]) {
+    if constexpr (TB < K && CB < K && CB != TB) {
 #pragma unroll
-    for (int e = 0; e < (1 << K); ++e) {
-        if (e & (1 << TB)) continue;
-        if ((static_cast<uint32_t>(e) & emask) != emask) continue;
-        pair_math<CLS>(op, vr[e], vi[e], vr[e | (1 << TB)], vi[e | (1 << TB)]);
+        for (int e = 0; e < (1 << K); ++e) {
+            if (e & (1 << TB)) continue;
+            if constexpr (CB >= 0) {
+                if (!(e & (1 << CB))) continue;
+            }
+            if constexpr (CB == -2) {
+                if ((static_cast<uint32_t>(e) & op.emask) != op.emask) continue;
+            }
+            pair_math<CLS>(op, vr[e], vi[e], vr[e | (1 << TB)], vi[e | (1 << TB)]);
+        }
     }
 }
 
-template <int K, int CLS>
-__device__ __forceinline__ void reg_dispatch_tb(const SvRegOp& op, double (&vr)[1 << K], double (&vi)[1 << K]) {
-    const uint32_t emask = op.emask;
-    switch (op.tb) {
-    case 0: reg_apply<K, 0, CLS>(op, vr, vi, emask); break;
-    case 1: if constexpr (K > 1) reg_apply<K, 1, CLS>(op, vr, vi, emask); break;
-    case 2: if constexpr (K > 2) reg_apply<K, 2, CLS>(op, vr, vi, emask); break;
-    case 3: if constexpr (K > 3) reg_apply<K, 3, CLS>(op, vr, vi, emask); break;
-    case 4: if constexpr (K > 4) reg_apply<K, 4, CLS>(op, vr, vi, emask); break;
+#define QSB_REG_CASES(CAT, CLS, CB)                                      \
+    case (CAT) * kSvRegMaxK + 0: reg_apply<K, CLS, CB, 0>(op, vr, vi); break; \
+    case (CAT) * kSvRegMaxK + 1: reg_apply<K, CLS, CB, 1>(op, vr, vi); break; \
+    case (CAT) * kSvRegMaxK + 2: reg_apply<K, CLS, CB, 2>(op, vr, vi); break; \
+    case (CAT) * kSvRegMaxK + 3: reg_apply<K, CLS, CB, 3>(op, vr, vi); break; \
+    case (CAT) * kSvRegMaxK + 4: reg_apply<K, CLS, CB, 4>(op, vr, vi); break;
+
+// One indirect branch per operation: op.code = category * kSvRegMaxK + target
+// index (categories: sv_reg_code in qsb_sv.hpp).
+template <int K>
+__device__ __forceinline__ void reg_dispatch(const SvRegOp& op, double (&vr)[1 << K], double (&vi)[1 << K]) {
+    switch (op.code) {
+        QSB_REG_CASES(0, kPairGeneral, -1)
+        QSB_REG_CASES(1, kPairReal, -1)
+        QSB_REG_CASES(2, kPairDiag, -1)
+        QSB_REG_CASES(3, kPairDiag1, -1)
+        QSB_REG_CASES(4, kPairAnti, -1)
+        QSB_REG_CASES(5, kPairSwap, -1)
+        QSB_REG_CASES(6, kPairGeneral, -2)
+        QSB_REG_CASES(7, kPairReal, -2)
+        QSB_REG_CASES(8, kPairDiag, -2)
+        QSB_REG_CASES(9, kPairDiag1, -2)
+        QSB_REG_CASES(10, kPairAnti, -2)
+        QSB_REG_CASES(11, kPairSwap, -2)
+        QSB_REG_CASES(12, kPairDiag1, 0)
+        QSB_REG_CASES(13, kPairDiag1, 1)
+        QSB_REG_CASES(14, kPairDiag1, 2)
+        QSB_REG_CASES(15, kPairDiag1, 3)
+        QSB_REG_CASES(16, kPairDiag1, 4)
+        QSB_REG_CASES(17, kPairSwap, 0)
+        QSB_REG_CASES(18, kPairSwap, 1)
+        QSB_REG_CASES(19, kPairSwap, 2)
+        QSB_REG_CASES(20, kPairSwap, 3)
+        QSB_REG_CASES(21, kPairSwap, 4)
     default: break;
     }
 }
+#undef QSB_REG_CASES
 
+__device__ __forceinline__ void cp_async8(uint32_t dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+
+// Each thread owns one group per iteration: the 2^K elements differing only in
+// the batch's K target bits. The next group is prefetched into this thread's
+// shared-memory slots with cp.async while the current one is updated in
+// registers and stored, so HBM traffic overlaps the FP64 work; slots are
+// [element][plane][thread] (consecutive threads, consecutive 8-byte words).
 template <int K>
 __global__ void __launch_bounds__(kSvRegThreads, 3) sv_reg_kernel(double* __restrict__ re, double* __restrict__ im,
                                                              const __grid_constant__ SvRegBatch b) {
     constexpr int E = 1 << K;
+    extern __shared__ double sv_pref[];
     // flat indices fit 32 bits: m <= 32 (host-checked)
     uint32_t tb[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) tb[i] = 1u << b.t[i];
-    for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < b.groups;
-         g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        // element 0 of the group: the group number with a zero inserted at every
-        // target bit (ascending positions, so each insert is in final coordinates)
+    // element 0 of group g: g with a zero inserted at every target bit
+    // (ascending positions, so each insert is in final coordinates)
+    auto base_of = [&](int64_t g) {
         uint32_t f = static_cast<uint32_t>(g);
 #pragma unroll
         for (int i = 0; i < K; ++i) f = ((f & ~(tb[i] - 1u)) << 1) | (f & (tb[i] - 1u));
-        double vr[E], vi[E];
+        return f;
+    };
+    auto offset = [&](uint32_t f, int e) {
+        uint32_t off = f;
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+            if (e & (1 << i)) off |= tb[i];
+        return off;
+    };
+    const uint32_t slot = static_cast<uint32_t>(__cvta_generic_to_shared(sv_pref)) + threadIdx.x * 8;
+    constexpr uint32_t SLOT_STRIDE = kSvRegThreads * 8;
+    auto prefetch = [&](uint32_t f) {
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            uint32_t off = f;
-#pragma unroll
-            for (int i = 0; i < K; ++i)
-                if (e & (1 << i)) off |= tb[i];
-            vr[e] = __ldcs(re + off);
-            vi[e] = __ldcs(im + off);
+            const uint32_t off = offset(f, e);
+            cp_async8(slot + (2 * e) * SLOT_STRIDE, re + off);
+            cp_async8(slot + (2 * e + 1) * SLOT_STRIDE, im + off);
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (g < b.groups) prefetch(base_of(g));
+    for (; g < b.groups; g += stride) {
+        const uint32_t f = base_of(g);
+        double vr[E], vi[E];
+        asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(vr[e]) : "r"(slot + (2 * e) * SLOT_STRIDE) : "memory");
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(vi[e]) : "r"(slot + (2 * e + 1) * SLOT_STRIDE) : "memory");
+        }
+        if (g + stride < b.groups) prefetch(base_of(g + stride));
 #pragma unroll 1
         for (int o = 0; o < b.op_count; ++o) {
             const SvRegOp& op = b.ops[o];
             const uint32_t oc = op.ocmask;
             if ((f & oc) != oc) continue;  // a control outside the targets is clear
-            switch (op.cls) {
-            case kPairSwap: reg_dispatch_tb<K, kPairSwap>(op, vr, vi); break;
-            case kPairDiag1: reg_dispatch_tb<K, kPairDiag1>(op, vr, vi); break;
-            case kPairDiag: reg_dispatch_tb<K, kPairDiag>(op, vr, vi); break;
-            case kPairAnti: reg_dispatch_tb<K, kPairAnti>(op, vr, vi); break;
-            case kPairReal: reg_dispatch_tb<K, kPairReal>(op, vr, vi); break;
-            default: reg_dispatch_tb<K, kPairGeneral>(op, vr, vi); break;
-            }
+            reg_dispatch<K>(op, vr, vi);
         }
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            uint32_t off = f;
-#pragma unroll
-            for (int i = 0; i < K; ++i)
-                if (e & (1 << i)) off |= tb[i];
+            const uint32_t off = offset(f, e);
             __stcs(re + off, vr[e]);
             __stcs(im + off, vi[e]);
         }
@@ -353,8 +411,9 @@ int grid_for(int64_t work, int per_sm) {
 using namespace detail;
 
 int sv_configure() {
-    return static_cast<int>(cudaFuncSetAttribute(sv_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 2 * (1 << kSvMaxSlabBits) * static_cast<int>(sizeof(double))));
+    int e = static_cast<int>(cudaFuncSetAttribute(sv_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  2 * (1 << kSvMaxSlabBits) * static_cast<int>(sizeof(double))));
+    return e;
 }
 
 int sv_launch_batch(double* re, double* im, const SvLocalOp* ops, const SvBatch& b, void* stream) {
@@ -369,7 +428,8 @@ int sv_launch_batch(double* re, double* im, const SvLocalOp* ops, const SvBatch&
 template <int K>
 static int launch_reg_t(double* re, double* im, const SvRegBatch& b, cudaStream_t st) {
     const int64_t blocks = (b.groups + kSvRegThreads - 1) / kSvRegThreads;
-    sv_reg_kernel<K><<<grid_for(blocks, 12), kSvRegThreads, 0, st>>>(re, im, b);
+    const int smem = 2 * (1 << K) * kSvRegThreads * static_cast<int>(sizeof(double));
+    sv_reg_kernel<K><<<grid_for(blocks, 3), kSvRegThreads, smem, st>>>(re, im, b);
     return static_cast<int>(cudaGetLastError());
 }
 
@@ -379,8 +439,7 @@ int sv_launch_reg(double* re, double* im, const SvRegBatch& b, void* stream) {
     case 1: return launch_reg_t<1>(re, im, b, st);
     case 2: return launch_reg_t<2>(re, im, b, st);
     case 3: return launch_reg_t<3>(re, im, b, st);
-    case 4: return launch_reg_t<4>(re, im, b, st);
-    default: return launch_reg_t<5>(re, im, b, st);
+    default: return launch_reg_t<4>(re, im, b, st);  // K <= kSvRegDefaultK (host-capped)
     }
 }
 

@@ -90,13 +90,31 @@ struct SvBatch {
 // one read + one write of the array per batch, no shared memory, no barriers.
 // The operations travel in the kernel's parameter space (constant bank:
 // uniform, no global-load latency per operation).
-constexpr int kSvRegMaxK = 5;
-constexpr int kSvRegDefaultK = 4;  // 2^4 complex per thread: no spills at 168 registers
+constexpr int kSvRegMaxK = 5;      // dispatch-code stride (sv_reg_code)
+constexpr int kSvRegDefaultK = 4;  // largest K launched: 2^4 complex per thread, 160 registers, no spills
 constexpr int kSvRegThreads = 128;
 constexpr int kSvRegMaxOps = 192;  // 192 x 80 B: the launch stays under the 32 KB parameter limit
 
+// Dispatch code of a register-batch op: category * kSvRegMaxK + target index.
+// Categories 0-5: class (SvPairClass order) with no control inside the targets;
+// 6-11: class with the control mask emask tested at run time; 12-16: diag-1
+// (controlled phase) with the control at target index 0-4; 17-21: X (CNOT) likewise.
+inline int32_t sv_reg_code(int32_t cls, int32_t tb, int32_t cb /* control index in t[], or -1 */) {
+    static const int kCat[6] = {0, 1, 2, 3, 4, 5};  // SvPairClass -> category without control
+    int cat;
+    if (cb < 0)
+        cat = kCat[cls];
+    else if (cls == 3 /* kPairDiag1 */)
+        cat = 12 + cb;
+    else if (cls == 5 /* kPairSwap */)
+        cat = 17 + cb;
+    else
+        cat = 6 + cls;
+    return cat * 5 /* kSvRegMaxK */ + tb;
+}
+
 struct SvRegOp {
-    int32_t cls;      // SvPairClass
+    int32_t code;     // sv_reg_code(cls, tb, control index)
     int32_t tb;       // index of the target within t[]
     uint32_t emask;   // control inside t[] (e-space bit), or 0
     uint32_t ocmask;  // control outside t[] (flat bit, tested on the group's element 0), or 0
