@@ -125,6 +125,23 @@ struct DeviceCtx {
     int device = 0;
     cudaStream_t stream = nullptr;
     qsbh::Buffers cache;  // reused by the host-API calls
+    // Pinned host staging for uploads on `stream` (descriptor arrays): reused by
+    // the next call only after that call's stream synchronisation.
+    void* pinned = nullptr;
+    size_t pinned_cap = 0;
+    void* stage(size_t bytes) {
+        if (bytes > pinned_cap) {
+            if (pinned) cudaFreeHost(pinned);
+            pinned = nullptr;
+            pinned_cap = 0;
+            qsbh::cuda_check(cudaMallocHost(&pinned, bytes), "cudaMallocHost");
+            pinned_cap = bytes;
+        }
+        return pinned;
+    }
+    ~DeviceCtx() {
+        if (pinned) cudaFreeHost(pinned);
+    }
 };
 
 struct qsb_handle {

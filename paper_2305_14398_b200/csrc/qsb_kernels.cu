@@ -1101,27 +1101,54 @@ size_t small_circuit_smem_bytes(int M, int N) {
     return sizeof(double) * (2 * static_cast<size_t>(M) * N * 2 + 2 * static_cast<size_t>(N) * N);
 }
 
-__global__ void __launch_bounds__(256) small_circuit_kernel(const LayerDesc* __restrict__ layers, int nlayers,
+// One CTA runs the whole chain for 2^n <= 32: V and V' ping-pong in shared
+// memory (two barriers per layer), every thread owns M*N/blockDim outputs.
+// x == nullptr means psi0 = |0...0>: psi = V[:, 0] (the reference's matvec with
+// e_0 adds only exact zeros to V[i][0]).
+__global__ void __launch_bounds__(512) small_circuit_kernel(const LayerDesc* __restrict__ layers, int nlayers,
                                                             uint32_t row_begin, int M, int N,
                                                             const double* __restrict__ x,
                                                             double* __restrict__ v_out,
                                                             double* __restrict__ psi) {
     extern __shared__ double sm[];
+    // Layer descriptors are staged in shared memory one ahead (cp.async), so the
+    // generator's field reads never chase pointers through global memory.
+    __shared__ __align__(16) LayerDesc desc[2];
+    constexpr int DESC_WORDS = static_cast<int>(sizeof(LayerDesc) / 8);
+    static_assert(sizeof(LayerDesc) % 8 == 0, "LayerDesc is copied in 8-byte words");
     const int MN = M * N;
-    double* vr = sm;
-    double* vi = vr + MN;
-    double* tr = vi + MN;
-    double* ti = tr + MN;
-    double* lr = ti + MN;
+    double* buf[2][2] = {{sm, sm + MN}, {sm + 2 * MN, sm + 3 * MN}};
+    double* lr = sm + 4 * MN;
     double* li = lr + N * N;
     const int tid = threadIdx.x;
-    for (int e = tid; e < MN; e += blockDim.x) {
-        layer_entry(layers[0], row_begin + e / N, e % N, vr[e], vi[e]);
+    auto fetch = [&](int l, int slot) {
+        const uint64_t* src = reinterpret_cast<const uint64_t*>(layers + l);
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&desc[slot]));
+        for (int w = tid; w < DESC_WORDS; w += blockDim.x)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8 * w), "l"(src + w) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    fetch(0, 0);
+    if (nlayers > 1) {
+        fetch(1, 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // layer 0 has landed
+    } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
+    __syncthreads();
+    for (int e = tid; e < MN; e += blockDim.x) layer_entry(desc[0], row_begin + e / N, e % N, buf[0][0][e], buf[0][1][e]);
+    int cur = 0;
     for (int l = 1; l < nlayers; ++l) {
-        const LayerDesc& d = layers[l];
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();  // desc[l & 1] has landed; every thread is done with desc[(l - 1) & 1]
+        if (l + 1 < nlayers) fetch(l + 1, (l + 1) & 1);
+        const LayerDesc& d = desc[l & 1];
         for (int e = tid; e < N * N; e += blockDim.x) layer_entry(d, e / N, e % N, lr[e], li[e]);
         __syncthreads();
+        const double* vr = buf[cur][0];
+        const double* vi = buf[cur][1];
+        double* tr = buf[cur ^ 1][0];
+        double* ti = buf[cur ^ 1][1];
         for (int e = tid; e < MN; e += blockDim.x) {
             const int i = e / N, j = e % N;
             double sr = 0.0, si = 0.0;
@@ -1134,19 +1161,21 @@ __global__ void __launch_bounds__(256) small_circuit_kernel(const LayerDesc* __r
             tr[e] = sr;
             ti[e] = si;
         }
-        __syncthreads();
-        for (int e = tid; e < MN; e += blockDim.x) {
-            vr[e] = tr[e];
-            vi[e] = ti[e];
-        }
+        cur ^= 1;
         __syncthreads();
     }
-    __syncthreads();
+    const double* vr = buf[cur][0];
+    const double* vi = buf[cur][1];
     for (int e = tid; e < MN; e += blockDim.x) {
         v_out[e] = vr[e];
         v_out[MN + e] = vi[e];
     }
     for (int i = tid; i < M; i += blockDim.x) {
+        if (x == nullptr) {
+            psi[i] = vr[i * N];
+            psi[M + i] = vi[i * N];
+            continue;
+        }
         double sr = 0.0, si = 0.0;
         for (int k = 0; k < N; ++k) {
             const double ar = vr[i * N + k], ai = vi[i * N + k];
@@ -1161,8 +1190,11 @@ __global__ void __launch_bounds__(256) small_circuit_kernel(const LayerDesc* __r
 int launch_small_circuit(const LayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, int N,
                          const double* x, double* v, double* psi, void* stream) {
     const size_t smem = small_circuit_smem_bytes(M, N);
-    small_circuit_kernel<<<1, 256, smem, static_cast<cudaStream_t>(stream)>>>(d_layers, nlayers, row_begin, M,
-                                                                              N, x, v, psi);
+    int threads = M * N;
+    if (threads > 512) threads = 512;
+    threads = (threads + 31) / 32 * 32;
+    small_circuit_kernel<<<1, threads, smem, static_cast<cudaStream_t>(stream)>>>(d_layers, nlayers, row_begin, M,
+                                                                                  N, x, v, psi);
     return static_cast<int>(cudaGetLastError());
 }
 

@@ -283,6 +283,7 @@ struct qsb_plan {
     bool borrowed = false;
     CUtensorMap tmap[2];
     int final_buf = 0;
+    bool x_is_e0 = true;  // psi0 = |0...0>: the one-CTA path reads psi as column 0
     cudaGraphExec_t graph = nullptr;
     bool timing = false;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -371,18 +372,21 @@ int pick_splits(int64_t T, int KT) {
     const char* force = std::getenv("QSB_SPLITK");
     if (force && *force) {
         const int s = std::atoi(force);
-        if ((s == 1 || s == 2 || s == 4) && KT / s >= 4) return s;
+        if ((s == 1 || s == 2 || s == 4 || s == 8) && KT / s >= 2) return s;
         return 1;
     }
-    const double sms = 148.0;
+    // time model per GEMM: waves x (per-CTA fixed cost + k-tiles per rank x k-tile time),
+    // fitted on B200 (QFT-12, DJ-11, Entangle-10 launch lists): 5.4 us fixed per CTA,
+    // +9.4 us for the cluster reduction, 1.63 us per 64x64x16 3M k-tile
+    const double sms = 148.0, fixed_us = 5.4, reduce_us = 9.4, ktile_us = 1.63;
     int best = 1;
-    double best_eff = 0.0;
-    for (int s = 1; s <= 4; s *= 2) {
-        if (KT / s < 8) break;  // keep the pipeline busy in every rank
-        const double waves = static_cast<double>(T * s) / sms;
-        const double eff = waves / std::ceil(waves);
-        if (eff > best_eff + 0.03) {
-            best_eff = eff;
+    double best_t = 1e30;
+    for (int s = 1; s <= 8; s *= 2) {
+        if (KT / s < 2) break;
+        const double waves = std::ceil(static_cast<double>(T * s) / sms);
+        const double t = waves * (fixed_us + (s > 1 ? reduce_us : 0.0) + ktile_us * static_cast<double>(KT) / s);
+        if (t < 0.97 * best_t) {
+            best_t = t;
             best = s;
         }
     }
@@ -405,16 +409,14 @@ int pick_tile(int M, int N, int gemm_mode, int* splits) {
     const bool three = gemm_mode != QSB_GEMM_4M;
     const int ws = three ? qsb::kTileWs3MS : qsb::kTileWs4M;
     const int wr = qsb::gemm_tile_rows(ws), wc = qsb::gemm_tile_cols(ws);
-    if (M % wr == 0 && N % wc == 0) {
+    if (M % wr == 0 && N % wc == 0 && N >= 128) {
+        // the warp-specialised tile with cluster split-K covers every shape from N = 128 up;
+        // small grids get their parallelism from the K split
         const int64_t T = static_cast<int64_t>(M / wr) * (N / wc);
-        const int s = pick_splits(T, N / 16);
-        if (T * s >= 2 * sms) {
-            *splits = s;
-            return ws;
-        }
+        *splits = pick_splits(T, N / 16);
+        return ws;
     }
     if (M % 64 == 0 && N % 64 == 0 && (M / 64) * (N / 64) >= sms) return qsb::kTile64x64;
-    if (M % wr == 0 && N % wc == 0 && (M / wr) * (N / wc) >= sms) return ws;
     return qsb::kTile32x32;
 }
 
@@ -526,20 +528,23 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
         }
     }
     if (p->chain.empty()) p->chain.push_back(identity_layer(n));
-    // psi0 = |0...0> (zero_state, state.cpp:37-47)
-    std::vector<double> x(2 * static_cast<size_t>(N), 0.0);
-    x[0] = 1.0;
-    cuda_check(cudaMemcpy(p->b.x.p, x.data(), x.size() * 8, cudaMemcpyHostToDevice), "upload psi0");
+    // psi0 = |0...0> (zero_state, state.cpp:37-47), written on the device
+    cuda_check(qsb::sv_launch_init_identity(p->b.x.as<double>(), p->b.x.as<double>() + N, N, 1, 0, dc->stream),
+               "init psi0");
+    p->x_is_e0 = true;
     if (p->small) {
-        p->b.layers.ensure(sizeof(qsb::LayerDesc) * p->chain.size());
-        cuda_check(cudaMemcpy(p->b.layers.p, p->chain.data(), sizeof(qsb::LayerDesc) * p->chain.size(),
-                              cudaMemcpyHostToDevice),
-                   "upload layers");
+        const size_t bytes = sizeof(qsb::LayerDesc) * p->chain.size();
+        p->b.layers.ensure(bytes);
+        void* st = dc->stage(bytes);
+        std::memcpy(st, p->chain.data(), bytes);
+        cuda_check(cudaMemcpyAsync(p->b.layers.p, st, bytes, cudaMemcpyHostToDevice, dc->stream), "upload layers");
     } else {
         const int rows = qsb::gemm_tile_rows(p->tile);
         p->tmap[0] = make_tmap(p->b.v[0].p, p->M, p->N, rows, p->planes);
         if (p->b.v[1].p) p->tmap[1] = make_tmap(p->b.v[1].p, p->M, p->N, rows, p->planes);
     }
+    // Plans executed on a caller's stream (qsb_plan_execute) must see the uploads.
+    if (!borrow_cache) cuda_check(cudaStreamSynchronize(dc->stream), "cudaStreamSynchronize");
     const int gemms = p->small ? static_cast<int>(p->chain.size()) - 1 : static_cast<int>(p->chain.size()) - 1;
     qsb_plan_info& in = p->info;
     in.n_qubits = n;
@@ -572,8 +577,8 @@ void enqueue(qsb_plan* p, cudaStream_t s) {
     const uint32_t rb = static_cast<uint32_t>(p->eff_begin);
     if (p->small) {
         cuda_check(qsb::launch_small_circuit(p->b.layers.as<qsb::LayerDesc>(), static_cast<int>(p->chain.size()), rb,
-                                             p->M, p->N, p->b.x.as<double>(), p->b.v[0].as<double>(),
-                                             p->b.psi.as<double>(), s),
+                                             p->M, p->N, p->x_is_e0 ? nullptr : p->b.x.as<double>(),
+                                             p->b.v[0].as<double>(), p->b.psi.as<double>(), s),
                    "small_circuit_kernel");
         p->final_buf = 0;
         return;
@@ -763,6 +768,7 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
             DeviceScope ds(p->dc->device);
             cudaStream_t s = p->dc->stream;
             if (psi0_re) {
+                p->x_is_e0 = false;
                 cuda_check(cudaMemcpyAsync(p->b.x.p, psi0_re, N * 8, cudaMemcpyHostToDevice, s), "upload psi0");
                 cuda_check(cudaMemcpyAsync(p->b.x.as<double>() + N, psi0_im, N * 8, cudaMemcpyHostToDevice, s),
                            "upload psi0");
@@ -1020,6 +1026,11 @@ qsb_status qsb_plan_set_initial_state(qsb_plan* plan, const double* re, const do
         DeviceScope ds(plan->dc->device);
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->dc->stream;
         const size_t N = static_cast<size_t>(plan->N);
+        plan->x_is_e0 = false;
+        if (plan->graph) {  // the captured one-CTA launch baked in x == nullptr
+            cudaGraphExecDestroy(plan->graph);
+            plan->graph = nullptr;
+        }
         cuda_check(cudaMemcpyAsync(plan->b.x.p, re, N * 8, cudaMemcpyDefault, s), "copy psi0");
         cuda_check(cudaMemcpyAsync(plan->b.x.as<double>() + N, im, N * 8, cudaMemcpyDefault, s), "copy psi0");
     });

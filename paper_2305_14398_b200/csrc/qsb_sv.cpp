@@ -257,14 +257,15 @@ void build_passes(qsb_sv_plan* p, const std::vector<FlatOp>& flat, const std::ve
             ++i;
             continue;
         }
-        const bool fn_run = f0.kind == qsb::kSvFunction;
-        const int cap = fn_run ? kmax : KR;
+        // a state of at most one slab: every op in one shared-memory launch
+        const bool fn_run = f0.kind == qsb::kSvFunction || m <= L;
+        const int cap = m <= L ? m : (fn_run ? kmax : KR);
         uint64_t T = 0;
         size_t j = i;
         while (j < flat.size()) {
             const FlatOp& f = flat[j];
-            if ((f.kind == qsb::kSvFunction) != fn_run) break;
-            if (fn_run && f.k > kmax) break;
+            if (m > L && (f.kind == qsb::kSvFunction) != fn_run) break;
+            if (f.kind == qsb::kSvFunction && f.k > kmax) break;
             if (!fn_run && j - i >= static_cast<size_t>(qsb::kSvRegMaxOps)) break;
             const uint64_t need = T | target_bits(f);
             if (popcount64(need) > cap) break;
@@ -381,14 +382,16 @@ std::unique_ptr<qsb_sv_plan> make_sv_plan(qsb_handle* h, DeviceCtx* dc, const qs
         p->b.x.ensure(2 * elems * sizeof(double));
         double* x = p->b.x.as<double>();
         cuda_check(qsb::sv_launch_init_identity(x, x + elems, N, 1, 0, dc->stream), "sv_init_identity");
-        cuda_check(cudaStreamSynchronize(dc->stream), "cudaStreamSynchronize");
     }
     if (!p->ops.empty()) {
-        p->b.layers.ensure(p->ops.size() * sizeof(qsb::SvLocalOp));
-        cuda_check(cudaMemcpy(p->b.layers.p, p->ops.data(), p->ops.size() * sizeof(qsb::SvLocalOp),
-                              cudaMemcpyHostToDevice),
-                   "upload ops");
+        const size_t bytes = p->ops.size() * sizeof(qsb::SvLocalOp);
+        p->b.layers.ensure(bytes);
+        void* st = dc->stage(bytes);
+        std::memcpy(st, p->ops.data(), bytes);
+        cuda_check(cudaMemcpyAsync(p->b.layers.p, st, bytes, cudaMemcpyHostToDevice, dc->stream), "upload ops");
     }
+    // Plans executed on a caller's stream must see the uploads (host-API calls run on dc->stream).
+    if (!borrow_cache) cuda_check(cudaStreamSynchronize(dc->stream), "cudaStreamSynchronize");
     qsb_sv_plan_info& in = p->info;
     in.n_qubits = p->n;
     in.mode = mode;

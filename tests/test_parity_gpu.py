@@ -308,7 +308,7 @@ def test_host_api_row_blocks_over_devices(monkeypatch, golden, orc, mode):
     one.close()
 
 
-@pytest.mark.parametrize("splits", ["1", "2", "4"])
+@pytest.mark.parametrize("splits", ["1", "2", "4", "8"])
 @pytest.mark.parametrize("tile", ["3", "5"])
 @pytest.mark.parametrize("name,n", [("qft", 10), ("entangle", 10), ("deutsch-jozsa", 10), ("qft", 11)])
 def test_cluster_split_k(monkeypatch, sim, orc, splits, tile, name, n):
@@ -336,13 +336,14 @@ def test_cluster_split_k(monkeypatch, sim, orc, splits, tile, name, n):
 
 
 def test_split_k_chosen_for_small_grids(sim):
-    """Entangle-10 (256 tiles of 64x64) fills 148 SMs with a 4-way split."""
+    """Small grids take their parallelism from the K split (N = 256: 16 tiles x 8
+    ranks); large ones do not split."""
     import paper_2305_14398_b200 as q
     from paper_2305_14398_b200 import native
 
-    c, reg = q.make_named_circuit("entangle", 10)
+    c, reg = q.make_named_circuit("qft", 8)
     plan = sim.plan(native.flatten(c, reg))
-    assert plan.info.gemm_splits == 4 and plan.info.gemm_tile == 5
+    assert plan.info.gemm_splits == 8 and plan.info.gemm_tile == 5
     plan.close()
     c, reg = q.make_named_circuit("qft", 12)
     plan = sim.plan(native.flatten(c, reg))
@@ -456,3 +457,31 @@ def test_materialise_flag_and_dense_layer_choice(sim, orc):
     re, im = orc.fsv(flat)
     assert rel_frob(a.re, a.im, re, im) <= TOL
     mat.close()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6])
+def test_single_layer_and_tiny_circuits(sim, orc, n):
+    """One-layer and few-layer circuits through the one-CTA path (N <= 32) and
+    the first tiled sizes: every gate kind, controls above / below targets."""
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+
+    rng = np.random.default_rng(n)
+    gates = [q.GateType.h(), q.GateType.x(), q.GateType.y(), q.GateType.z(), q.GateType.s(), q.GateType.t(),
+             q.GateType.r(0.3)]
+    for trial in range(40):
+        c = q.Circuit(n)
+        for _ in range(1 + trial % 4):
+            g = gates[rng.integers(len(gates))]
+            if n > 1 and rng.random() < 0.5:
+                a, b = rng.choice(n, 2, replace=False)
+                c.add_control_gate(g, int(a), int(b))
+            else:
+                c.add_gate(g, int(rng.integers(n)))
+        flat = native.flatten(c, None)
+        out = sim.simulate_full_state(flat)
+        re, im = orc.unitary_simulate(flat, guard=n)
+        assert rel_frob(out.re, out.im, re, im) <= TOL, (n, trial)
+        ur, ui = sim.build_unitary(flat)
+        orr, ori = orc.circuit_unitary(flat)
+        assert rel_frob(ur, ui, orr, ori) <= TOL, (n, trial)
