@@ -127,21 +127,26 @@ struct DeviceCtx {
     qsbh::Buffers cache;  // reused by the host-API calls
     // Pinned host staging for uploads on `stream` (descriptor arrays): reused by
     // the next call only after that call's stream synchronisation.
-    void* pinned = nullptr;
-    size_t pinned_cap = 0;
-    void* stage(size_t bytes) {
-        if (bytes > pinned_cap) {
-            if (pinned) cudaFreeHost(pinned);
-            pinned = nullptr;
-            pinned_cap = 0;
-            qsbh::cuda_check(cudaMallocHost(&pinned, bytes), "cudaMallocHost");
-            pinned_cap = bytes;
+    struct Pinned {
+        void* p = nullptr;
+        size_t cap = 0;
+        void* get(size_t bytes) {
+            if (bytes > cap) {
+                if (p) cudaFreeHost(p);
+                p = nullptr;
+                cap = 0;
+                qsbh::cuda_check(cudaMallocHost(&p, bytes), "cudaMallocHost");
+                cap = bytes;
+            }
+            return p;
         }
-        return pinned;
-    }
-    ~DeviceCtx() {
-        if (pinned) cudaFreeHost(pinned);
-    }
+        ~Pinned() {
+            if (p) cudaFreeHost(p);
+        }
+    };
+    Pinned pinned_in, pinned_out;  // uploads / downloads of small results
+    void* stage(size_t bytes) { return pinned_in.get(bytes); }
+    void* stage_out(size_t bytes) { return pinned_out.get(bytes); }
 };
 
 struct qsb_handle {

@@ -1103,10 +1103,13 @@ size_t small_circuit_smem_bytes(int M, int N) {
 
 // One CTA runs the whole chain for 2^n <= 32: V and V' ping-pong in shared
 // memory (two barriers per layer), every thread owns M*N/blockDim outputs.
+// N is a template parameter: index arithmetic by constants and a fully
+// unrolled k-loop whose shared-memory loads issue ahead of the FMA chain.
 // x == nullptr means psi0 = |0...0>: psi = V[:, 0] (the reference's matvec with
 // e_0 adds only exact zeros to V[i][0]).
+template <int N>
 __global__ void __launch_bounds__(512) small_circuit_kernel(const LayerDesc* __restrict__ layers, int nlayers,
-                                                            uint32_t row_begin, int M, int N,
+                                                            uint32_t row_begin, int M,
                                                             const double* __restrict__ x,
                                                             double* __restrict__ v_out,
                                                             double* __restrict__ psi) {
@@ -1117,7 +1120,6 @@ __global__ void __launch_bounds__(512) small_circuit_kernel(const LayerDesc* __r
     constexpr int DESC_WORDS = static_cast<int>(sizeof(LayerDesc) / 8);
     static_assert(sizeof(LayerDesc) % 8 == 0, "LayerDesc is copied in 8-byte words");
     const int MN = M * N;
-    double* buf[2][2] = {{sm, sm + MN}, {sm + 2 * MN, sm + 3 * MN}};
     double* lr = sm + 4 * MN;
     double* li = lr + N * N;
     const int tid = threadIdx.x;
@@ -1136,8 +1138,8 @@ __global__ void __launch_bounds__(512) small_circuit_kernel(const LayerDesc* __r
         asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-    for (int e = tid; e < MN; e += blockDim.x) layer_entry(desc[0], row_begin + e / N, e % N, buf[0][0][e], buf[0][1][e]);
-    int cur = 0;
+    for (int e = tid; e < MN; e += blockDim.x) layer_entry(desc[0], row_begin + e / N, e % N, sm[e], sm[MN + e]);
+    int cur = 0;  // V in planes [2 cur, 2 cur + 1] of sm
     for (int l = 1; l < nlayers; ++l) {
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();  // desc[l & 1] has landed; every thread is done with desc[(l - 1) & 1]
@@ -1145,18 +1147,25 @@ __global__ void __launch_bounds__(512) small_circuit_kernel(const LayerDesc* __r
         const LayerDesc& d = desc[l & 1];
         for (int e = tid; e < N * N; e += blockDim.x) layer_entry(d, e / N, e % N, lr[e], li[e]);
         __syncthreads();
-        const double* vr = buf[cur][0];
-        const double* vi = buf[cur][1];
-        double* tr = buf[cur ^ 1][0];
-        double* ti = buf[cur ^ 1][1];
+        const double* vr = sm + (2 * cur) * MN;
+        const double* vi = vr + MN;
+        double* tr = sm + (2 * (cur ^ 1)) * MN;
+        double* ti = tr + MN;
         for (int e = tid; e < MN; e += blockDim.x) {
             const int i = e / N, j = e % N;
-            double sr = 0.0, si = 0.0;
+            double ar[N], ai[N], br[N], bi[N];
+#pragma unroll
             for (int k = 0; k < N; ++k) {
-                const double ar = vr[i * N + k], ai = vi[i * N + k];
-                const double br = lr[k * N + j], bi = li[k * N + j];
-                sr = fma(ar, br, fma(-ai, bi, sr));
-                si = fma(ar, bi, fma(ai, br, si));
+                ar[k] = vr[i * N + k];
+                ai[k] = vi[i * N + k];
+                br[k] = lr[k * N + j];
+                bi[k] = li[k * N + j];
+            }
+            double sr = 0.0, si = 0.0;
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                sr = fma(ar[k], br[k], fma(-ai[k], bi[k], sr));
+                si = fma(ar[k], bi[k], fma(ai[k], br[k], si));
             }
             tr[e] = sr;
             ti[e] = si;
@@ -1164,8 +1173,8 @@ __global__ void __launch_bounds__(512) small_circuit_kernel(const LayerDesc* __r
         cur ^= 1;
         __syncthreads();
     }
-    const double* vr = buf[cur][0];
-    const double* vi = buf[cur][1];
+    const double* vr = sm + (2 * cur) * MN;
+    const double* vi = vr + MN;
     for (int e = tid; e < MN; e += blockDim.x) {
         v_out[e] = vr[e];
         v_out[MN + e] = vi[e];
@@ -1178,24 +1187,37 @@ __global__ void __launch_bounds__(512) small_circuit_kernel(const LayerDesc* __r
         }
         double sr = 0.0, si = 0.0;
         for (int k = 0; k < N; ++k) {
-            const double ar = vr[i * N + k], ai = vi[i * N + k];
-            sr += ar * x[k] - ai * x[N + k];
-            si += ar * x[N + k] + ai * x[k];
+            const double a_r = vr[i * N + k], a_i = vi[i * N + k];
+            sr += a_r * x[k] - a_i * x[N + k];
+            si += a_r * x[N + k] + a_i * x[k];
         }
         psi[i] = sr;
         psi[M + i] = si;
     }
 }
 
-int launch_small_circuit(const LayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, int N,
-                         const double* x, double* v, double* psi, void* stream) {
+template <int N>
+static int launch_small_t(const LayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, const double* x, double* v,
+                          double* psi, cudaStream_t st) {
     const size_t smem = small_circuit_smem_bytes(M, N);
     int threads = M * N;
     if (threads > 512) threads = 512;
     threads = (threads + 31) / 32 * 32;
-    small_circuit_kernel<<<1, threads, smem, static_cast<cudaStream_t>(stream)>>>(d_layers, nlayers, row_begin, M,
-                                                                                  N, x, v, psi);
+    small_circuit_kernel<N><<<1, threads, smem, st>>>(d_layers, nlayers, row_begin, M, x, v, psi);
     return static_cast<int>(cudaGetLastError());
+}
+
+int launch_small_circuit(const LayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, int N,
+                         const double* x, double* v, double* psi, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    switch (N) {
+    case 2: return launch_small_t<2>(d_layers, nlayers, row_begin, M, x, v, psi, st);
+    case 4: return launch_small_t<4>(d_layers, nlayers, row_begin, M, x, v, psi, st);
+    case 8: return launch_small_t<8>(d_layers, nlayers, row_begin, M, x, v, psi, st);
+    case 16: return launch_small_t<16>(d_layers, nlayers, row_begin, M, x, v, psi, st);
+    case 32: return launch_small_t<32>(d_layers, nlayers, row_begin, M, x, v, psi, st);
+    default: return static_cast<int>(cudaErrorInvalidValue);
+    }
 }
 
 // ----------------------------------------------------------------------------
@@ -1302,7 +1324,7 @@ int configure_kernels() {
     if ((e = configure_ws_t<false, false>())) return e;
     if ((e = configure_ws_t<true, false>())) return e;
     if ((e = configure_ws_t<true, true>())) return e;
-    return static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel,
+    return static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel<32>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
 }
 

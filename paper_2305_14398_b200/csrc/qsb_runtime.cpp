@@ -528,9 +528,11 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
         }
     }
     if (p->chain.empty()) p->chain.push_back(identity_layer(n));
-    // psi0 = |0...0> (zero_state, state.cpp:37-47), written on the device
-    cuda_check(qsb::sv_launch_init_identity(p->b.x.as<double>(), p->b.x.as<double>() + N, N, 1, 0, dc->stream),
-               "init psi0");
+    // psi0 = |0...0> (zero_state, state.cpp:37-47), written on the device (the
+    // one-CTA path reads psi as column 0 and never touches x for |0...0>)
+    if (!p->small)
+        cuda_check(qsb::sv_launch_init_identity(p->b.x.as<double>(), p->b.x.as<double>() + N, N, 1, 0, dc->stream),
+                   "init psi0");
     p->x_is_e0 = true;
     if (p->small) {
         const size_t bytes = sizeof(qsb::LayerDesc) * p->chain.size();
@@ -758,6 +760,7 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
     }
     const int64_t rows = N / G;
     std::vector<std::unique_ptr<qsb_plan>> plans(G);
+    std::vector<double*> staged(G, nullptr);
     auto release_all = [&] {
         for (auto& p : plans) release_plan(p);
     };
@@ -775,7 +778,12 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
             }
             execute(p, s, false);
             const int64_t off = p->row_begin - p->eff_begin;
-            if (psi_re) {
+            if (psi_re && p->M <= 65536) {
+                // one copy of both psi planes into pinned staging; scattered on the host after the sync
+                staged[g] = static_cast<double*>(p->dc->stage_out(2 * static_cast<size_t>(p->M) * 8));
+                cuda_check(cudaMemcpyAsync(staged[g], p->b.psi.p, 2 * static_cast<size_t>(p->M) * 8,
+                                           cudaMemcpyDeviceToHost, s), "download psi");
+            } else if (psi_re) {
                 cuda_check(cudaMemcpyAsync(psi_re + p->row_begin, p->b.psi.as<double>() + off, rows * 8,
                                            cudaMemcpyDeviceToHost, s), "download psi");
                 cuda_check(cudaMemcpyAsync(psi_im + p->row_begin, p->b.psi.as<double>() + p->M + off, rows * 8,
@@ -793,6 +801,12 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
         for (int g = 0; g < G; ++g) {
             DeviceScope ds(plans[g]->dc->device);
             cuda_check(cudaStreamSynchronize(plans[g]->dc->stream), "cudaStreamSynchronize");
+            if (staged[g]) {
+                const qsb_plan* p = plans[g].get();
+                const int64_t off = p->row_begin - p->eff_begin;
+                std::memcpy(psi_re + p->row_begin, staged[g] + off, rows * 8);
+                std::memcpy(psi_im + p->row_begin, staged[g] + p->M + off, rows * 8);
+            }
         }
     } catch (...) {
         release_all();

@@ -515,9 +515,17 @@ void run_fsv(qsb_handle* h, const qsb_circuit* c, const double* psi0_re, const d
         }
         sv_execute(p.get(), dc.stream);
         const double* v = sv_result(p.get());
-        cuda_check(cudaMemcpyAsync(psi_re, v, N * 8, cudaMemcpyDeviceToHost, dc.stream), "download psi");
-        cuda_check(cudaMemcpyAsync(psi_im, v + N, N * 8, cudaMemcpyDeviceToHost, dc.stream), "download psi");
-        cuda_check(cudaStreamSynchronize(dc.stream), "cudaStreamSynchronize");
+        if (N <= 65536) {  // both planes in one copy through pinned staging
+            double* st = static_cast<double*>(dc.stage_out(2 * N * 8));
+            cuda_check(cudaMemcpyAsync(st, v, 2 * N * 8, cudaMemcpyDeviceToHost, dc.stream), "download psi");
+            cuda_check(cudaStreamSynchronize(dc.stream), "cudaStreamSynchronize");
+            std::memcpy(psi_re, st, N * 8);
+            std::memcpy(psi_im, st + N, N * 8);
+        } else {
+            cuda_check(cudaMemcpyAsync(psi_re, v, N * 8, cudaMemcpyDeviceToHost, dc.stream), "download psi");
+            cuda_check(cudaMemcpyAsync(psi_im, v + N, N * 8, cudaMemcpyDeviceToHost, dc.stream), "download psi");
+            cuda_check(cudaStreamSynchronize(dc.stream), "cudaStreamSynchronize");
+        }
     } catch (...) {
         release_sv_plan(p);
         throw;
