@@ -1108,7 +1108,7 @@ size_t small_circuit_smem_bytes(int M, int N) {
 // x == nullptr means psi0 = |0...0>: psi = V[:, 0] (the reference's matvec with
 // e_0 adds only exact zeros to V[i][0]).
 template <int N>
-__global__ void __launch_bounds__(512) small_circuit_kernel(const LayerDesc* __restrict__ layers, int nlayers,
+__global__ void __launch_bounds__(1024) small_circuit_kernel(const LayerDesc* __restrict__ layers, int nlayers,
                                                             uint32_t row_begin, int M,
                                                             const double* __restrict__ x,
                                                             double* __restrict__ v_out,
@@ -1201,7 +1201,7 @@ static int launch_small_t(const LayerDesc* d_layers, int nlayers, uint32_t row_b
                           double* psi, cudaStream_t st) {
     const size_t smem = small_circuit_smem_bytes(M, N);
     int threads = M * N;
-    if (threads > 512) threads = 512;
+    if (threads > 1024) threads = 1024;
     threads = (threads + 31) / 32 * 32;
     small_circuit_kernel<N><<<1, threads, smem, st>>>(d_layers, nlayers, row_begin, M, x, v, psi);
     return static_cast<int>(cudaGetLastError());
@@ -1216,6 +1216,7 @@ int launch_small_circuit(const LayerDesc* d_layers, int nlayers, uint32_t row_be
     case 8: return launch_small_t<8>(d_layers, nlayers, row_begin, M, x, v, psi, st);
     case 16: return launch_small_t<16>(d_layers, nlayers, row_begin, M, x, v, psi, st);
     case 32: return launch_small_t<32>(d_layers, nlayers, row_begin, M, x, v, psi, st);
+    case 64: return launch_small_t<64>(d_layers, nlayers, row_begin, M, x, v, psi, st);
     default: return static_cast<int>(cudaErrorInvalidValue);
     }
 }
@@ -1324,8 +1325,12 @@ int configure_kernels() {
     if ((e = configure_ws_t<false, false>())) return e;
     if ((e = configure_ws_t<true, false>())) return e;
     if ((e = configure_ws_t<true, true>())) return e;
-    return static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel<32>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    if ((e = static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel<32>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024))))
+        return e;
+    return static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel<64>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(small_circuit_smem_bytes(64, 64))));
 }
 
 }  // namespace qsb
