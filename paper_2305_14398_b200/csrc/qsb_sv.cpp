@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -19,6 +20,7 @@
 
 #include "../../include/qsb.h"
 #include "qsb_host.hpp"
+#include "qsb_jit.hpp"
 #include "qsb_sv.hpp"
 
 using namespace qsbh;
@@ -37,6 +39,8 @@ struct qsb_sv_plan {
     struct Pass {
         int kind;
         std::shared_ptr<qsb::SvRegBatch> reg;  // kReg: gates / controlled gates, elements in registers
+        void* jit = nullptr;                   // kReg: the batch compiled straight-line (qsb_jit.hpp), or null
+        std::vector<double> coef;              // kReg + jit: the coefficients, in the kernel's parameter order
         qsb::SvBatch batch;   // kSlab: small apply_function blocks in shared memory
         FnPass f;             // kFn: apply_function blocks larger than a slab
     };
@@ -129,13 +133,19 @@ uint64_t target_bits(const FlatOp& f) {
     return ((uint64_t{1} << f.k) - 1) << f.tbit;
 }
 
-int reg_k_default() {
-    const char* e = std::getenv("QSB_SV_REG_K");  // tuning / tests
+// Targets per register batch: 5 when the batch is compiled straight-line (no
+// merge points, 2^5 complex per thread fit in registers) and the array has
+// column bits below the targets (structured unitary: coalesced, warp-uniform
+// controls); 4 otherwise (measured: r35). QSB_SV_REG_K overrides (tests / tuning).
+int reg_k_default(int w) {
+    const bool jit = qsbjit::available();
+    const int cap = jit ? qsb::kSvRegMaxK : qsb::kSvRegDefaultK;
+    const char* e = std::getenv("QSB_SV_REG_K");
     if (e && *e) {
         const int v = std::atoi(e);
-        if (v >= 1 && v <= qsb::kSvRegDefaultK) return v;
+        if (v >= 1 && v <= cap) return v;
     }
-    return qsb::kSvRegDefaultK;
+    return (jit && w >= 5) ? qsb::kSvRegMaxK : qsb::kSvRegDefaultK;
 }
 
 // A shared-memory slab batch over ops [i, j) whose target bits are T.
@@ -233,6 +243,183 @@ void push_reg_batch(qsb_sv_plan* p, const std::vector<FlatOp>& flat, size_t i, s
     p->passes.push_back(ps);
 }
 
+// ---- straight-line register batches (qsb_jit.hpp) ----------------------------
+
+const char* kJitPrelude = R"(
+#define QSB_MUL(a, b) __dmul_rn(a, b)
+#define QSB_ADD(a, b) __dadd_rn(a, b)
+#define QSB_SUB(a, b) __dsub_rn(a, b)
+)";
+
+// The kernel of one register batch: the same pair updates as pair_math
+// (fsv_backend.cpp:52-55, classes qsb_sv.hpp), with every target, control and
+// class a constant; X / CNOT pairs without an outer control are a renaming of
+// the element variables. Coefficients are appended to *coef in parameter order.
+std::string emit_reg_kernel(const std::string& name, const qsb::SvRegBatch& b, std::vector<double>* coef) {
+    const int K = b.K, E = 1 << K;
+    std::string o;
+    char buf[512];
+    auto put = [&](const char* fmt, auto... a) {
+        std::snprintf(buf, sizeof buf, fmt, a...);
+        o += buf;
+    };
+    std::vector<int> loc(E);
+    for (int e = 0; e < E; ++e) loc[e] = e;
+    std::string body;
+    auto bput = [&](const char* fmt, auto... a) {
+        std::snprintf(buf, sizeof buf, fmt, a...);
+        body += buf;
+    };
+    auto cref = [&](double v) {
+        coef->push_back(v);
+        return static_cast<int>(coef->size()) - 1;
+    };
+    for (int k = 0; k < b.op_count; ++k) {
+        const qsb::SvRegOp& op = b.ops[k];
+        const int cat = op.code / qsb::kSvRegMaxK;
+        const int cls = cat < 6 ? cat : (cat < 12 ? cat - 6 : (cat < 17 ? qsb::kPairDiag1 : qsb::kPairSwap));
+        const int tb = op.tb;
+        const int cb = op.emask ? __builtin_ctz(op.emask) : -1;
+        const bool outer = op.ocmask != 0;
+        if (outer) bput("    if (f & 0x%xu) {\n", op.ocmask);
+        int u[8];
+        if (cls == qsb::kPairDiag1) {
+            u[0] = cref(op.u_re[3]);
+            u[1] = cref(op.u_im[3]);
+        } else if (cls == qsb::kPairDiag) {
+            u[0] = cref(op.u_re[0]); u[1] = cref(op.u_im[0]); u[2] = cref(op.u_re[3]); u[3] = cref(op.u_im[3]);
+        } else if (cls == qsb::kPairAnti) {
+            u[0] = cref(op.u_re[1]); u[1] = cref(op.u_im[1]); u[2] = cref(op.u_re[2]); u[3] = cref(op.u_im[2]);
+        } else if (cls == qsb::kPairReal) {
+            for (int e = 0; e < 4; ++e) u[e] = cref(op.u_re[e]);
+        } else if (cls == qsb::kPairGeneral) {
+            for (int e = 0; e < 4; ++e) {
+                u[2 * e] = cref(op.u_re[e]);
+                u[2 * e + 1] = cref(op.u_im[e]);
+            }
+        }
+        for (int e0 = 0; e0 < E; ++e0) {
+            if (e0 & (1 << tb)) continue;
+            if (cb >= 0 && !(e0 & (1 << cb))) continue;
+            const int e1 = e0 | (1 << tb);
+            const int A = loc[e0], B = loc[e1];
+            switch (cls) {
+            case qsb::kPairSwap:
+                if (!outer)
+                    std::swap(loc[e0], loc[e1]);
+                else
+                    bput("      { double t = r%d; r%d = r%d; r%d = t; t = i%d; i%d = i%d; i%d = t; }\n", A, A, B, B, A,
+                         A, B, B);
+                break;
+            case qsb::kPairDiag1:
+                bput("      { const double nr = QSB_SUB(QSB_MUL(c.v[%d], r%d), QSB_MUL(c.v[%d], i%d));"
+                     " const double ni = QSB_ADD(QSB_MUL(c.v[%d], i%d), QSB_MUL(c.v[%d], r%d)); r%d = nr; i%d = ni; }\n",
+                     u[0], B, u[1], B, u[0], B, u[1], B, B, B);
+                break;
+            case qsb::kPairDiag:
+                bput("      { const double n0r = QSB_SUB(QSB_MUL(c.v[%d], r%d), QSB_MUL(c.v[%d], i%d));"
+                     " const double n0i = QSB_ADD(QSB_MUL(c.v[%d], i%d), QSB_MUL(c.v[%d], r%d));\n",
+                     u[0], A, u[1], A, u[0], A, u[1], A);
+                bput("        const double n1r = QSB_SUB(QSB_MUL(c.v[%d], r%d), QSB_MUL(c.v[%d], i%d));"
+                     " const double n1i = QSB_ADD(QSB_MUL(c.v[%d], i%d), QSB_MUL(c.v[%d], r%d));"
+                     " r%d = n0r; i%d = n0i; r%d = n1r; i%d = n1i; }\n",
+                     u[2], B, u[3], B, u[2], B, u[3], B, A, A, B, B);
+                break;
+            case qsb::kPairAnti:
+                bput("      { const double n0r = QSB_SUB(QSB_MUL(c.v[%d], r%d), QSB_MUL(c.v[%d], i%d));"
+                     " const double n0i = QSB_ADD(QSB_MUL(c.v[%d], i%d), QSB_MUL(c.v[%d], r%d));\n",
+                     u[0], B, u[1], B, u[0], B, u[1], B);
+                bput("        const double n1r = QSB_SUB(QSB_MUL(c.v[%d], r%d), QSB_MUL(c.v[%d], i%d));"
+                     " const double n1i = QSB_ADD(QSB_MUL(c.v[%d], i%d), QSB_MUL(c.v[%d], r%d));"
+                     " r%d = n0r; i%d = n0i; r%d = n1r; i%d = n1i; }\n",
+                     u[2], A, u[3], A, u[2], A, u[3], A, A, A, B, B);
+                break;
+            case qsb::kPairReal:
+                bput("      { const double n0r = QSB_ADD(QSB_MUL(c.v[%d], r%d), QSB_MUL(c.v[%d], r%d));"
+                     " const double n0i = QSB_ADD(QSB_MUL(c.v[%d], i%d), QSB_MUL(c.v[%d], i%d));\n",
+                     u[0], A, u[1], B, u[0], A, u[1], B);
+                bput("        const double n1r = QSB_ADD(QSB_MUL(c.v[%d], r%d), QSB_MUL(c.v[%d], r%d));"
+                     " const double n1i = QSB_ADD(QSB_MUL(c.v[%d], i%d), QSB_MUL(c.v[%d], i%d));"
+                     " r%d = n0r; i%d = n0i; r%d = n1r; i%d = n1i; }\n",
+                     u[2], A, u[3], B, u[2], A, u[3], B, A, A, B, B);
+                break;
+            default: {
+                // u00r*a0r - u00i*a0i + u01r*a1r - u01i*a1i, left to right (fsv_backend.cpp:52-55)
+                bput("      { const double n0r = QSB_SUB(QSB_ADD(QSB_SUB(QSB_MUL(c.v[%d], r%d), QSB_MUL(c.v[%d], i%d)),"
+                     " QSB_MUL(c.v[%d], r%d)), QSB_MUL(c.v[%d], i%d));\n",
+                     u[0], A, u[1], A, u[2], B, u[3], B);
+                bput("        const double n0i = QSB_ADD(QSB_ADD(QSB_ADD(QSB_MUL(c.v[%d], i%d), QSB_MUL(c.v[%d], r%d)),"
+                     " QSB_MUL(c.v[%d], i%d)), QSB_MUL(c.v[%d], r%d));\n",
+                     u[0], A, u[1], A, u[2], B, u[3], B);
+                bput("        const double n1r = QSB_SUB(QSB_ADD(QSB_SUB(QSB_MUL(c.v[%d], r%d), QSB_MUL(c.v[%d], i%d)),"
+                     " QSB_MUL(c.v[%d], r%d)), QSB_MUL(c.v[%d], i%d));\n",
+                     u[4], A, u[5], A, u[6], B, u[7], B);
+                bput("        const double n1i = QSB_ADD(QSB_ADD(QSB_ADD(QSB_MUL(c.v[%d], i%d), QSB_MUL(c.v[%d], r%d)),"
+                     " QSB_MUL(c.v[%d], i%d)), QSB_MUL(c.v[%d], r%d)); r%d = n0r; i%d = n0i; r%d = n1r; i%d = n1i; }\n",
+                     u[4], A, u[5], A, u[6], B, u[7], B, A, A, B, B);
+            }
+            }
+        }
+        if (outer) body += "    }\n";
+    }
+    const int NC = std::max<int>(1, static_cast<int>(coef->size()));
+    put("struct QsbCoef_%s { double v[%d]; };\n", name.c_str(), NC);
+    put("extern \"C\" __global__ void __launch_bounds__(%d) %s(double* __restrict__ re, double* __restrict__ im,"
+        " long long groups, const __grid_constant__ QsbCoef_%s c) {\n",
+        qsb::kSvRegThreads, name.c_str(), name.c_str());
+    o += "  const long long stride = (long long)gridDim.x * blockDim.x;\n";
+    o += "  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {\n";
+    o += "    unsigned f = (unsigned)g;\n";
+    for (int i = 0; i < K; ++i) {
+        const unsigned low = (1u << b.t[i]) - 1u;
+        put("    f = ((f & ~0x%xu) << 1) | (f & 0x%xu);\n", low, low);
+    }
+    auto pat = [&](int e) {
+        unsigned p = 0;
+        for (int i = 0; i < K; ++i)
+            if (e & (1 << i)) p |= 1u << b.t[i];
+        return p;
+    };
+    for (int e = 0; e < E; ++e)
+        put("    double r%d = __ldcs(re + (f | 0x%xu)); double i%d = __ldcs(im + (f | 0x%xu));\n", e, pat(e), e,
+            pat(e));
+    o += body;
+    for (int e = 0; e < E; ++e)
+        put("    __stcs(re + (f | 0x%xu), r%d); __stcs(im + (f | 0x%xu), i%d);\n", pat(e), loc[e], pat(e), loc[e]);
+    o += "  }\n}\n";
+    return o;
+}
+
+// Compile every register batch of the plan into one module (cached by source).
+void jit_register_batches(qsb_sv_plan* p) {
+    if (!qsbjit::available()) return;
+    std::string src = kJitPrelude;
+    std::vector<std::string> names;
+    std::vector<size_t> idx;
+    for (size_t i = 0; i < p->passes.size(); ++i) {
+        qsb_sv_plan::Pass& ps = p->passes[i];
+        if (ps.kind != qsb_sv_plan::kReg) continue;
+        const std::string name = "qsb_sv_b" + std::to_string(i);
+        ps.coef.clear();
+        src += emit_reg_kernel(name, *ps.reg, &ps.coef);
+        names.push_back(name);
+        idx.push_back(i);
+    }
+    if (names.empty()) return;
+    if (const char* dump = std::getenv("QSB_SV_JIT_DUMP")) {  // debugging: the generated source
+        if (FILE* fp = std::fopen(dump, "w")) {
+            std::fputs(src.c_str(), fp);
+            std::fclose(fp);
+        }
+    }
+    const std::vector<void*> fns = qsbjit::kernels(src, names);
+    for (size_t k = 0; k < idx.size(); ++k) {
+        qsb_sv_plan::Pass& ps = p->passes[idx[k]];
+        ps.jit = fns[k];
+        if (ps.coef.empty()) ps.coef.push_back(0.0);
+    }
+}
+
 // Group the ops into passes, in order: runs of gates / controlled gates on at
 // most K distinct targets become register batches; apply_function blocks that
 // fit a shared-memory slab become slab batches (consecutive ones merged); larger
@@ -243,7 +430,7 @@ void build_passes(qsb_sv_plan* p, const std::vector<FlatOp>& flat, const std::ve
     // blocks of up to 2^6 run inside a slab; larger ones get their own pass
     // (one thread per output: a 2^k-term sum per element is too long for one CTA)
     const int kmax = std::min((m <= L) ? m : L - 5, 6);
-    const int KR = std::min(reg_k_default(), m);
+    const int KR = std::min(reg_k_default(p->w), m);
     size_t i = 0;
     int max_targets = 0;
     while (i < flat.size()) {
@@ -375,6 +562,7 @@ std::unique_ptr<qsb_sv_plan> make_sv_plan(qsb_handle* h, DeviceCtx* dc, const qs
         }
     }
     build_passes(p.get(), flat, tabs);
+    jit_register_batches(p.get());
     const size_t elems = static_cast<size_t>(N) * static_cast<size_t>(p->col_count);
     p->b.v[0].ensure(2 * elems * sizeof(double));
     if (p->info.n_function_passes > 0) p->b.v[1].ensure(2 * elems * sizeof(double));
@@ -434,7 +622,15 @@ void sv_execute(qsb_sv_plan* p, cudaStream_t s) {
     const qsb::SvLocalOp* ops = p->b.layers.as<qsb::SvLocalOp>();
     for (const auto& ps : p->passes) {
         double* v = p->b.v[cur].as<double>();
-        if (ps.kind == qsb_sv_plan::kReg) {
+        if (ps.kind == qsb_sv_plan::kReg && ps.jit) {
+            double* vre = v;
+            double* vim = v + elems;
+            long long groups = static_cast<long long>(ps.reg->groups);
+            void* args[] = {&vre, &vim, &groups, const_cast<double*>(ps.coef.data())};
+            const long long blocks = (groups + qsb::kSvRegThreads - 1) / qsb::kSvRegThreads;
+            const unsigned grid = static_cast<unsigned>(std::min<long long>(blocks, 148LL * 8));
+            cuda_check(qsbjit::launch(ps.jit, grid, qsb::kSvRegThreads, s, args), "sv jit kernel");
+        } else if (ps.kind == qsb_sv_plan::kReg) {
             cuda_check(qsb::sv_launch_reg(v, v + elems, *ps.reg, s), "sv_reg_kernel");
         } else if (ps.kind == qsb_sv_plan::kSlab) {
             cuda_check(qsb::sv_launch_batch(v, v + elems, ops, ps.batch, s), "sv_batch_kernel");

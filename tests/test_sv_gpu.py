@@ -286,3 +286,19 @@ def test_is_unitary_dj_oracles(sim):
             reg.register_function("bad", bad)
     finally:
         circuit.set_unitarity_check(None)
+
+
+@pytest.mark.parametrize("jit,k", [("0", "4"), ("0", "2"), ("1", "5"), ("1", "3"), ("1", "1")])
+def test_register_batches_interpreted_and_compiled(monkeypatch, golden, jit, k):
+    """Register batches run either interpreted (sv_reg_kernel) or compiled
+    straight-line by NVRTC (qsb_jit): both bit-exact with the reference fsv,
+    for every batch width."""
+    from paper_2305_14398_b200.simulator import B200FsvSimulator
+
+    monkeypatch.setenv("QSB_SV_JIT", jit)
+    monkeypatch.setenv("QSB_SV_REG_K", k)
+    s = B200FsvSimulator()
+    for case in golden.suites["fsvbig"]:
+        out = s.simulate_full_state(golden.flat(case))
+        assert bit_equal(out.re, golden[f"{case}:fsv_re"]) and bit_equal(out.im, golden[f"{case}:fsv_im"]), case
+    s.close()
