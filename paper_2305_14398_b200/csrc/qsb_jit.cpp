@@ -83,6 +83,11 @@ bool available() {
     return nvrtc().ok && driver<ModuleLoadFn>("cuModuleLoadData") && driver<LaunchFn>("cuLaunchKernel");
 }
 
+bool forced() {
+    const char* e = std::getenv("QSB_SV_JIT");
+    return e && std::strcmp(e, "1") == 0 && available();
+}
+
 std::vector<void*> kernels(const std::string& source, const std::vector<std::string>& names) {
     using qsbh::raise;
     int dev = 0;

@@ -24,6 +24,10 @@ namespace qsbjit {
 // NVRTC present and QSB_SV_JIT != "0".
 bool available();
 
+// QSB_SV_JIT == "1": compile every register batch, whatever the array size
+// (by default only arrays of >= 2^18 elements, where compilation pays off).
+bool forced();
+
 // CUfunction handles (as void*) for `names` in `source`, compiled for the
 // current device (sm_100a) or taken from the process-wide cache.
 std::vector<void*> kernels(const std::string& source, const std::vector<std::string>& names);

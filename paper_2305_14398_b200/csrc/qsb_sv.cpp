@@ -137,8 +137,8 @@ uint64_t target_bits(const FlatOp& f) {
 // merge points, 2^5 complex per thread fit in registers) and the array has
 // column bits below the targets (structured unitary: coalesced, warp-uniform
 // controls); 4 otherwise (measured: r35). QSB_SV_REG_K overrides (tests / tuning).
-int reg_k_default(int w) {
-    const bool jit = qsbjit::available();
+int reg_k_default(int w, int m) {
+    const bool jit = qsbjit::available() && (m >= 18 || qsbjit::forced());
     const int cap = jit ? qsb::kSvRegMaxK : qsb::kSvRegDefaultK;
     const char* e = std::getenv("QSB_SV_REG_K");
     if (e && *e) {
@@ -393,6 +393,7 @@ std::string emit_reg_kernel(const std::string& name, const qsb::SvRegBatch& b, s
 // Compile every register batch of the plan into one module (cached by source).
 void jit_register_batches(qsb_sv_plan* p) {
     if (!qsbjit::available()) return;
+    if (p->m < 18 && !qsbjit::forced()) return;  // small arrays: the interpreted kernel, no compile latency
     std::string src = kJitPrelude;
     std::vector<std::string> names;
     std::vector<size_t> idx;
@@ -430,7 +431,7 @@ void build_passes(qsb_sv_plan* p, const std::vector<FlatOp>& flat, const std::ve
     // blocks of up to 2^6 run inside a slab; larger ones get their own pass
     // (one thread per output: a 2^k-term sum per element is too long for one CTA)
     const int kmax = std::min((m <= L) ? m : L - 5, 6);
-    const int KR = std::min(reg_k_default(p->w), m);
+    const int KR = std::min(reg_k_default(p->w, m), m);
     size_t i = 0;
     int max_targets = 0;
     while (i < flat.size()) {
