@@ -78,7 +78,19 @@ def dist_env():
 
 # --------------------------------------------------------------- CPU baseline
 
+def oracle_available() -> bool:
+    import oracle
+
+    return oracle.reference_available()
+
+
 def cpu_sample(workload: str, repeats: int = 1):
+    """Reference CPU time of a named BASELINE workload (cpu_sample_circuit)."""
+    name, n = WORKLOADS[workload]
+    return cpu_sample_circuit(name, n, repeats)
+
+
+def cpu_sample_circuit(name: str, n: int, repeats: int = 1):
     """Time the reference CPU path on a bounded sample and extrapolate to one
     circuit. Components:
       T = sum_steps [fold(step) + GEMM_par(N)] + extra_layers * GEMM_ser(N)
@@ -89,7 +101,7 @@ def cpu_sample(workload: str, repeats: int = 1):
     import paper_2305_14398_b200 as q
     from paper_2305_14398_b200 import native
 
-    name, n = WORKLOADS[workload]
+    workload = f"{name}-{n}"
     N = 1 << n
     cores = os.cpu_count() or 1
     c, reg = q.make_named_circuit(name, n)

@@ -1097,31 +1097,45 @@ int launch_zgemm(const GemmArgs& a, int tile, int /*gemm_mode*/, void* stream) {
 // K2s: whole circuit in one CTA (2^n <= 32): launch-latency bound sizes.
 // ----------------------------------------------------------------------------
 
+// Operator rows generated per chunk: the whole operator up to N = 64, 32 rows at N = 128, 16 at N = 256.
+__host__ __device__ constexpr int small_kc(int N) { return N <= 64 ? N : (N == 128 ? 32 : 16); }
+
 size_t small_circuit_smem_bytes(int M, int N) {
-    return sizeof(double) * (2 * static_cast<size_t>(M) * N * 2 + 2 * static_cast<size_t>(N) * N);
+    return sizeof(double) * (2 * static_cast<size_t>(M) * N * 2 + 2 * static_cast<size_t>(small_kc(N)) * N);
 }
 
-// One CTA runs the whole chain for 2^n <= 32: V and V' ping-pong in shared
-// memory (two barriers per layer), every thread owns M*N/blockDim outputs.
-// N is a template parameter: index arithmetic by constants and a fully
-// unrolled k-loop whose shared-memory loads issue ahead of the FMA chain.
-// x == nullptr means psi0 = |0...0>: psi = V[:, 0] (the reference's matvec with
-// e_0 adds only exact zeros to V[i][0]).
+// The whole chain for N <= 256 in one launch, no inter-CTA exchange: CTA b owns
+// rows [b R, b R + R) of V for every layer (rows of V <- V L depend only on the
+// same rows of V). V and V' ping-pong in shared memory; each layer operator is
+// generated KC rows at a time into shared memory (every CTA generates the whole
+// operator — cheap next to the products), and every thread accumulates its
+// outputs over the chunks. N is a template parameter: index arithmetic by
+// constants and fully unrolled inner loops. x == nullptr means psi0 = |0...0>:
+// psi = V[:, 0] (the reference's matvec with e_0 adds only exact zeros to V[i][0]).
 template <int N>
 __global__ void __launch_bounds__(1024) small_circuit_kernel(const LayerDesc* __restrict__ layers, int nlayers,
                                                             uint32_t row_begin, int M,
                                                             const double* __restrict__ x,
                                                             double* __restrict__ v_out,
                                                             double* __restrict__ psi) {
+    constexpr int KC = small_kc(N);
+    constexpr int MAXQ = 2;  // outputs per thread (R N <= 2048 with 1024 threads)
     extern __shared__ double sm[];
     // Layer descriptors are staged in shared memory one ahead (cp.async), so the
     // generator's field reads never chase pointers through global memory.
     __shared__ __align__(16) LayerDesc desc[2];
     constexpr int DESC_WORDS = static_cast<int>(sizeof(LayerDesc) / 8);
     static_assert(sizeof(LayerDesc) % 8 == 0, "LayerDesc is copied in 8-byte words");
-    const int MN = M * N;
+    const int R = M / gridDim.x;
+    const int cta_row = blockIdx.x * R;
+    row_begin += static_cast<uint32_t>(cta_row);
+    const int out_plane = M * N;
+    v_out += static_cast<size_t>(cta_row) * N;
+    psi += cta_row;
+    const int psi_plane = M;
+    const int MN = R * N;
     double* lr = sm + 4 * MN;
-    double* li = lr + N * N;
+    double* li = lr + KC * N;
     const int tid = threadIdx.x;
     auto fetch = [&](int l, int slot) {
         const uint64_t* src = reinterpret_cast<const uint64_t*>(layers + l);
@@ -1145,30 +1159,42 @@ __global__ void __launch_bounds__(1024) small_circuit_kernel(const LayerDesc* __
         __syncthreads();  // desc[l & 1] has landed; every thread is done with desc[(l - 1) & 1]
         if (l + 1 < nlayers) fetch(l + 1, (l + 1) & 1);
         const LayerDesc& d = desc[l & 1];
-        for (int e = tid; e < N * N; e += blockDim.x) layer_entry(d, e / N, e % N, lr[e], li[e]);
-        __syncthreads();
         const double* vr = sm + (2 * cur) * MN;
         const double* vi = vr + MN;
         double* tr = sm + (2 * (cur ^ 1)) * MN;
         double* ti = tr + MN;
-        for (int e = tid; e < MN; e += blockDim.x) {
-            const int i = e / N, j = e % N;
-            double ar[N], ai[N], br[N], bi[N];
+        double accr[MAXQ], acci[MAXQ];
 #pragma unroll
-            for (int k = 0; k < N; ++k) {
-                ar[k] = vr[i * N + k];
-                ai[k] = vi[i * N + k];
-                br[k] = lr[k * N + j];
-                bi[k] = li[k * N + j];
-            }
-            double sr = 0.0, si = 0.0;
+        for (int q = 0; q < MAXQ; ++q) accr[q] = acci[q] = 0.0;
+        for (int k0 = 0; k0 < N; k0 += KC) {
+            if (k0 > 0) __syncthreads();  // the previous chunk is consumed
+            for (int e = tid; e < KC * N; e += blockDim.x)
+                layer_entry(d, static_cast<uint32_t>(k0 + e / N), static_cast<uint32_t>(e % N), lr[e], li[e]);
+            __syncthreads();
 #pragma unroll
-            for (int k = 0; k < N; ++k) {
-                sr = fma(ar[k], br[k], fma(-ai[k], bi[k], sr));
-                si = fma(ar[k], bi[k], fma(ai[k], br[k], si));
+            for (int q = 0; q < MAXQ; ++q) {
+                const int e = tid + q * blockDim.x;
+                if (e >= MN) break;
+                const int i = e / N, j = e % N;
+                double sr = accr[q], si = acci[q];
+#pragma unroll
+                for (int k = 0; k < KC; ++k) {
+                    const double ar = vr[i * N + k0 + k], ai = vi[i * N + k0 + k];
+                    const double br = lr[k * N + j], bi = li[k * N + j];
+                    sr = fma(ar, br, fma(-ai, bi, sr));
+                    si = fma(ar, bi, fma(ai, br, si));
+                }
+                accr[q] = sr;
+                acci[q] = si;
             }
-            tr[e] = sr;
-            ti[e] = si;
+        }
+#pragma unroll
+        for (int q = 0; q < MAXQ; ++q) {
+            const int e = tid + q * blockDim.x;
+            if (e < MN) {
+                tr[e] = accr[q];
+                ti[e] = acci[q];
+            }
         }
         cur ^= 1;
         __syncthreads();
@@ -1177,12 +1203,12 @@ __global__ void __launch_bounds__(1024) small_circuit_kernel(const LayerDesc* __
     const double* vi = vr + MN;
     for (int e = tid; e < MN; e += blockDim.x) {
         v_out[e] = vr[e];
-        v_out[MN + e] = vi[e];
+        v_out[out_plane + e] = vi[e];
     }
-    for (int i = tid; i < M; i += blockDim.x) {
+    for (int i = tid; i < R; i += blockDim.x) {
         if (x == nullptr) {
             psi[i] = vr[i * N];
-            psi[M + i] = vi[i * N];
+            psi[psi_plane + i] = vi[i * N];
             continue;
         }
         double sr = 0.0, si = 0.0;
@@ -1192,18 +1218,20 @@ __global__ void __launch_bounds__(1024) small_circuit_kernel(const LayerDesc* __
             si += a_r * x[N + k] + a_i * x[k];
         }
         psi[i] = sr;
-        psi[M + i] = si;
+        psi[psi_plane + i] = si;
     }
 }
 
 template <int N>
 static int launch_small_t(const LayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, const double* x, double* v,
                           double* psi, cudaStream_t st) {
-    const size_t smem = small_circuit_smem_bytes(M, N);
-    int threads = M * N;
+    // rows per CTA: 8 from N = 32 (several SMs), all of them below
+    const int R = (N >= 32 && M % 8 == 0) ? 8 : M;
+    const size_t smem = small_circuit_smem_bytes(R, N);
+    int threads = R * N;
     if (threads > 1024) threads = 1024;
     threads = (threads + 31) / 32 * 32;
-    small_circuit_kernel<N><<<1, threads, smem, st>>>(d_layers, nlayers, row_begin, M, x, v, psi);
+    small_circuit_kernel<N><<<M / R, threads, smem, st>>>(d_layers, nlayers, row_begin, M, x, v, psi);
     return static_cast<int>(cudaGetLastError());
 }
 
@@ -1217,6 +1245,8 @@ int launch_small_circuit(const LayerDesc* d_layers, int nlayers, uint32_t row_be
     case 16: return launch_small_t<16>(d_layers, nlayers, row_begin, M, x, v, psi, st);
     case 32: return launch_small_t<32>(d_layers, nlayers, row_begin, M, x, v, psi, st);
     case 64: return launch_small_t<64>(d_layers, nlayers, row_begin, M, x, v, psi, st);
+    case 128: return launch_small_t<128>(d_layers, nlayers, row_begin, M, x, v, psi, st);
+    case 256: return launch_small_t<256>(d_layers, nlayers, row_begin, M, x, v, psi, st);
     default: return static_cast<int>(cudaErrorInvalidValue);
     }
 }
@@ -1328,9 +1358,17 @@ int configure_kernels() {
     if ((e = static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel<32>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024))))
         return e;
-    return static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel<64>,
+    if ((e = static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel<64>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(small_circuit_smem_bytes(8, 64))))))
+        return e;
+    if ((e = static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel<128>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(small_circuit_smem_bytes(8, 128))))))
+        return e;
+    return static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel<256>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(small_circuit_smem_bytes(64, 64))));
+                                                 static_cast<int>(small_circuit_smem_bytes(8, 256))));
 }
 
 }  // namespace qsb

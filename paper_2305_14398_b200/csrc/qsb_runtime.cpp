@@ -445,7 +445,7 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
         else
             p->chain.push_back(*it);
     }
-    p->small = N <= 64;
+    p->small = N <= 64;  // measured: row-resident CUDA-core chains lose to K2 from N = 128 (r39)
     int64_t M = row_count;
     if (!p->small) {
         // The tiled kernels need at least 32 rows and power-of-two shards; widen
@@ -750,7 +750,7 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
     validate_circuit_shape(c);
     check_guard(c, h->guard);
     const int64_t N = int64_t{1} << c->n_qubits;
-    // equal power-of-two row blocks of at least 32 rows (the one-CTA path takes N <= 64 whole)
+    // equal power-of-two row blocks of at least 32 rows (the row-resident path computes N <= 64 whole)
     int G = static_cast<int>(h->devs.size());
     while (G > 1 && (N / G < 32 || N % G != 0)) --G;
     if (G > 1 && (G & (G - 1)) != 0) {

@@ -336,14 +336,18 @@ def test_cluster_split_k(monkeypatch, sim, orc, splits, tile, name, n):
 
 
 def test_split_k_chosen_for_small_grids(sim):
-    """Small grids take their parallelism from the K split (N = 256: 16 tiles x 8
-    ranks); large ones do not split."""
+    """Small grids take their parallelism from the K split (N = 512: 64 tiles x 2
+    ranks); large ones do not split; N <= 64 runs row-resident in one launch."""
     import paper_2305_14398_b200 as q
     from paper_2305_14398_b200 import native
 
-    c, reg = q.make_named_circuit("qft", 8)
+    c, reg = q.make_named_circuit("qft", 9)
     plan = sim.plan(native.flatten(c, reg))
-    assert plan.info.gemm_splits == 8 and plan.info.gemm_tile == 5
+    assert plan.info.gemm_splits == 2 and plan.info.gemm_tile == 5
+    plan.close()
+    c, reg = q.make_named_circuit("qft", 6)
+    plan = sim.plan(native.flatten(c, reg))
+    assert plan.info.gemm_tile == -1 and plan.info.n_launches == 1
     plan.close()
     c, reg = q.make_named_circuit("qft", 12)
     plan = sim.plan(native.flatten(c, reg))
