@@ -367,9 +367,11 @@ def run_ours(args):
             "roofline": {"bound": "tensor", "kernel": (native.TILE_NAMES.get(info.gemm_tile, "small_circuit_kernel") + " (K2)") if info else None,
                          "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": (achieved / FP64_DMMA_PEAK_TFLOPS) if achieved else None,
-                         # 3M issues 6N^3 hardware FLOPs per complex GEMM (credited 8N^3 above)
-                         "hw_frac": (achieved * (0.75 if info.gemm_tile in (4, 5) else 1.0)
-                                     / FP64_DMMA_PEAK_TFLOPS) if achieved else None,
+                         # hardware FLOPs the DMMAs execute: 6N^3 (3M), 4N^3 (real layer), 8N^3 (4M)
+                         # per GEMM, against the credited 8N^3 above
+                         "hw_frac": (achieved * (info.gemm_hw_flops / info.gemm_flops)
+                                     / FP64_DMMA_PEAK_TFLOPS) if achieved and info.gemm_flops else None,
+                         "real_gemms": info.n_real_gemms if info else None,
                          "traffic": traffic,
                          "algorithmic_flops_per_launch": per_launch_flops,
                          "mean_launch_ms": mean_gemm_ms,

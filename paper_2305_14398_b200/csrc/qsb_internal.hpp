@@ -68,6 +68,9 @@ struct GemmArgs {
     int N;
     const void* tmap_b = nullptr;  // warp-specialised tiles: CUtensorMap of a materialised
                                    // (transposed) operator; null = generate B in shared memory
+    bool real = false;             // 3M warp-specialised tiles: the operator is real -> two real GEMMs
+    const void* tmap_real = nullptr;    // two-plane (re, im) view of A for the real variant
+    const void* tmap_b_real = nullptr;  // one-plane (re) view of a materialised operator
     int splits = 1;          // warp-specialised tiles: K split over a thread-block cluster of this
                              // size (1, 2, 4); partial accumulators are summed through
                              // distributed shared memory in rank order (deterministic)

@@ -567,7 +567,12 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN>::THREADS, 1)
 //     Ci = T3 - T1 - T2 (warp tile 32x16, CTA 64x64; the producer writes the
 //     Br+Bi plane, consumers form Ar+Ai in registers).
 
-template <bool THREE_M, bool SUMPLANE = false>
+// REAL: the layer operator has an exactly-zero imaginary plane (H, X, CNOT, SWAP,
+// DJ oracles): V' = V L is two real GEMMs, Vr' = Vr Lr and Vi' = Vi Lr — the
+// products with Li are exact zeros in every arithmetic — so B is one plane and
+// the consumers issue 2 instead of 3 (3M) DMMAs per fragment pair. Same tile
+// shape as 3M, so plans mix both variants freely.
+template <bool THREE_M, bool SUMPLANE = false, bool REAL = false>
 struct WsCfg {
     static constexpr int BK = 16;
     static constexpr int CONSUMER_WARPS = 8;
@@ -579,10 +584,10 @@ struct WsCfg {
     static constexpr int CWN = CONSUMER_WARPS / CWM; // consumer warps along N
     static constexpr int BM = CWM * 32;
     static constexpr int BN = CWN * WT_N;
-    static constexpr int B_PLANES = THREE_M ? 3 : 2;
+    static constexpr int B_PLANES = REAL ? 1 : (THREE_M ? 3 : 2);
     // SUMPLANE: V carries a third plane Vr+Vi written by the previous GEMM's
     // epilogue (or K1), so 3M consumers load it instead of adding in registers.
-    static constexpr int A_PLANES = (THREE_M && SUMPLANE) ? 3 : 2;
+    static constexpr int A_PLANES = (THREE_M && SUMPLANE && !REAL) ? 3 : 2;
     static constexpr int A_TMA_BYTES = A_PLANES * BM * BK * 8;
     static constexpr int A_BYTES = A_TMA_BYTES;
     static constexpr int B_BYTES = B_PLANES * BN * BK * 8;
@@ -612,11 +617,11 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 // expand_t_kernel) and B tiles arrive by TMA like A — no FP64 generation work
 // in the producer, whose FP64 instructions would otherwise queue behind DMMA on
 // the shared FP64 pipe (used for dense, non-monomial layers such as H on every qubit).
-template <bool THREE_M, bool SUMPLANE, bool MAT_B>
-__global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
+template <bool THREE_M, bool SUMPLANE, bool MAT_B, bool REAL = false>
+__global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
     zgemm_ws_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ LayerDesc layer, double* __restrict__ out, int M, int N) {
-    using C = WsCfg<THREE_M, SUMPLANE>;
+    using C = WsCfg<THREE_M, SUMPLANE, REAL>;
     constexpr int BM = C::BM, BN = C::BN;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -721,16 +726,16 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
                     double v0r = 0.0, v0i = 0.0, v1r = 0.0, v1i = 0.0, s0 = 0.0, s1 = 0.0;
                     if (cols[2 * q] == static_cast<int64_t>(col)) {
                         layer_entry(layer, r0, col, v0r, v0i);
-                        if (THREE_M) s0 = __dadd_rn(v0r, v0i);
+                        if (THREE_M && !REAL) s0 = __dadd_rn(v0r, v0i);
                     }
                     if (cols[2 * q + 1] == static_cast<int64_t>(col)) {
                         layer_entry(layer, r0 + 1, col, v1r, v1i);
-                        if (THREE_M) s1 = __dadd_rn(v1r, v1i);
+                        if (THREE_M && !REAL) s1 = __dadd_rn(v1r, v1i);
                     }
                     const uint32_t off = n * 128 + ((pch ^ (n & 7)) << 4);
                     sts128(bBase + off, v0r, v1r);
-                    sts128(bBase + BN * 128 + off, v0i, v1i);
-                    if (THREE_M) sts128(bBase + 2 * BN * 128 + off, s0, s1);
+                    if (!REAL) sts128(bBase + BN * 128 + off, v0i, v1i);
+                    if (THREE_M && !REAL) sts128(bBase + 2 * BN * 128 + off, s0, s1);
                 }
             } else {
                 constexpr int EB = 4;  // elements per batch = 2 (k, k+1) pairs
@@ -753,6 +758,7 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
                     for (int h = 0; h < EB / 2; ++h) {
                         const uint32_t off = nn[h] * 128 + ((pp[h] ^ (nn[h] & 7)) << 4);
                         sts128(bBase + off, vr[2 * h], vr[2 * h + 1]);
+                        if (REAL) continue;
                         sts128(bBase + BN * 128 + off, vi[2 * h], vi[2 * h + 1]);
                         if (THREE_M) {
                             // real layers: Br + Bi = Br (adding an exact zero; no FP64 op)
@@ -782,7 +788,7 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
     const int wm = warp / C::CWN;
     const int wn = warp % C::CWN;
     constexpr int NT = C::NT;
-    constexpr int NACC = THREE_M ? 3 : 2;
+    constexpr int NACC = (THREE_M && !REAL) ? 3 : 2;
     double acc[NACC][4][NT][2];
 #pragma unroll
     for (int a = 0; a < NACC; ++a)
@@ -809,14 +815,14 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
                 const uint32_t line = static_cast<uint32_t>(wm * 32 + i * 8 + g) * 128 + choff;
                 ar[i] = lds128(aRe + line);
                 ai[i] = lds128(aIm + line);
-                if (SUMPLANE) as2[i] = lds128(aSm + line);
+                if (SUMPLANE && !REAL) as2[i] = lds128(aSm + line);
             }
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
                 const uint32_t line = static_cast<uint32_t>(wn * C::WT_N + j * 8 + g) * 128 + choff;
                 br[j] = lds128(bRe + line);
-                bi[j] = lds128(bIm + line);
-                if (THREE_M) bs[j] = lds128(bSm + line);
+                if (!REAL) bi[j] = lds128(bIm + line);
+                if (THREE_M && !REAL) bs[j] = lds128(bSm + line);
             }
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
@@ -829,9 +835,19 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
 #pragma unroll
                 for (int j = 0; j < NT; ++j) {
                     yr[j] = e ? br[j].y : br[j].x;
-                    yi[j] = e ? bi[j].y : bi[j].x;
+                    if (!REAL) yi[j] = e ? bi[j].y : bi[j].x;
                 }
-                if (THREE_M) {
+                if (REAL) {
+                    // Cr += Ar Br, Ci += Ai Br (Bi = 0 exactly)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < NT; ++j) dmma(acc[0][i][j], xr[i], yr[j]);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < NT; ++j) dmma(acc[1][i][j], xi[i], yr[j]);
+                } else if (THREE_M) {
                     double xs[4], ys[NT];
 #pragma unroll
                     for (int i = 0; i < 4; ++i) xs[i] = SUMPLANE ? (e ? as2[i].y : as2[i].x) : __dadd_rn(xr[i], xi[i]);
@@ -881,7 +897,7 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
         const int col = n0 + wn * C::WT_N + j * 8 + 2 * t;
         const size_t o = static_cast<size_t>(row) * N + col;
         double r0, r1, i0, i1;
-        if (THREE_M) {
+        if (THREE_M && !REAL) {
             r0 = f[0][0] - f[1][0];
             r1 = f[0][1] - f[1][1];
             i0 = f[2][0] - f[0][0] - f[1][0];
@@ -967,27 +983,36 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE>::THREADS, 1)
         }
 }
 
-template <bool THREE_M, bool SUMPLANE>
-static int configure_ws_t() {
-    int e = static_cast<int>(cudaFuncSetAttribute(zgemm_ws_kernel<THREE_M, SUMPLANE, false>,
+template <bool THREE_M, bool SUMPLANE, bool REAL>
+static int configure_ws_one() {
+    int e = static_cast<int>(cudaFuncSetAttribute(zgemm_ws_kernel<THREE_M, SUMPLANE, false, REAL>,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  WsCfg<THREE_M, SUMPLANE>::SMEM));
+                                                  WsCfg<THREE_M, SUMPLANE, REAL>::SMEM));
     if (e) return e;
-    return static_cast<int>(cudaFuncSetAttribute(zgemm_ws_kernel<THREE_M, SUMPLANE, true>,
+    return static_cast<int>(cudaFuncSetAttribute(zgemm_ws_kernel<THREE_M, SUMPLANE, true, REAL>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 WsCfg<THREE_M, SUMPLANE>::SMEM));
+                                                 WsCfg<THREE_M, SUMPLANE, REAL>::SMEM));
 }
 
-template <bool THREE_M, bool SUMPLANE, bool MAT_B>
+template <bool THREE_M, bool SUMPLANE>
+static int configure_ws_t() {
+    int e = configure_ws_one<THREE_M, SUMPLANE, false>();
+    if (e || !THREE_M) return e;
+    return configure_ws_one<THREE_M, SUMPLANE, true>();
+}
+
+template <bool THREE_M, bool SUMPLANE, bool MAT_B, bool REAL>
 static int launch_ws_t(const GemmArgs& a, void* stream) {
-    using C = WsCfg<THREE_M, SUMPLANE>;
+    using C = WsCfg<THREE_M, SUMPLANE, REAL>;
     const int splits = a.splits > 1 ? a.splits : 1;
-    const CUtensorMap& tmA = *static_cast<const CUtensorMap*>(a.tmap);
-    const CUtensorMap& tmB = MAT_B ? *static_cast<const CUtensorMap*>(a.tmap_b) : tmA;
+    // REAL reads two planes of V (and one of a materialised operator): their own tensor maps
+    const CUtensorMap& tmA = *static_cast<const CUtensorMap*>(REAL && a.tmap_real ? a.tmap_real : a.tmap);
+    const CUtensorMap& tmB =
+        MAT_B ? *static_cast<const CUtensorMap*>(REAL && a.tmap_b_real ? a.tmap_b_real : a.tmap_b) : tmA;
     if (splits == 1) {
         dim3 grid(a.N / C::BN, a.M / C::BM);
-        zgemm_ws_kernel<THREE_M, SUMPLANE, MAT_B><<<grid, C::THREADS, C::SMEM, static_cast<cudaStream_t>(stream)>>>(
-            tmA, tmB, *a.layer, a.out, a.M, a.N);
+        zgemm_ws_kernel<THREE_M, SUMPLANE, MAT_B, REAL>
+            <<<grid, C::THREADS, C::SMEM, static_cast<cudaStream_t>(stream)>>>(tmA, tmB, *a.layer, a.out, a.M, a.N);
         return static_cast<int>(cudaGetLastError());
     }
     cudaLaunchConfig_t cfg = {};
@@ -1002,13 +1027,18 @@ static int launch_ws_t(const GemmArgs& a, void* stream) {
     attr[0].val.clusterDim.z = splits;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return static_cast<int>(
-        cudaLaunchKernelEx(&cfg, zgemm_ws_kernel<THREE_M, SUMPLANE, MAT_B>, tmA, tmB, *a.layer, a.out, a.M, a.N));
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, zgemm_ws_kernel<THREE_M, SUMPLANE, MAT_B, REAL>, tmA, tmB,
+                                               *a.layer, a.out, a.M, a.N));
 }
 
 template <bool THREE_M, bool SUMPLANE>
 static int launch_ws_any(const GemmArgs& a, void* stream) {
-    return a.tmap_b ? launch_ws_t<THREE_M, SUMPLANE, true>(a, stream) : launch_ws_t<THREE_M, SUMPLANE, false>(a, stream);
+    if (THREE_M && a.real) {
+        return a.tmap_b ? launch_ws_t<THREE_M, SUMPLANE, true, true>(a, stream)
+                        : launch_ws_t<THREE_M, SUMPLANE, false, true>(a, stream);
+    }
+    return a.tmap_b ? launch_ws_t<THREE_M, SUMPLANE, true, false>(a, stream)
+                    : launch_ws_t<THREE_M, SUMPLANE, false, false>(a, stream);
 }
 
 // K1t: the layer operator transposed, Lt[p][n][k] = L[k][n] for planes re, im

@@ -277,6 +277,9 @@ struct qsb_plan {
     int splits = 1;  // K2 split-K cluster size (warp-specialised tiles)
     std::vector<char> mat;  // chain[i] (i >= 1) is materialised by K1t and streamed to K2 by TMA
     CUtensorMap tmap_b;     // the materialised operator ([planes][N][N], transposed)
+    CUtensorMap tmap_b_real;  // its real plane alone (box of one plane) for real layers
+    CUtensorMap tmap_real[2]; // two-plane (re, im) views of the V buffers for real layers
+    bool real_ok = false;     // 3M warp-specialised tile: real layers run as two real GEMMs
     int planes = 2;  // V buffer planes: re, im (+ re+im for the 3M sum-plane tile)
     bool small = false;
     qsbh::Buffers b;
@@ -522,6 +525,8 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
                 p->b.lmat.ensure(bytes);
                 p->tmap_b = make_tmap(p->b.lmat.p, static_cast<int>(N), static_cast<int>(N),
                                       qsb::gemm_tile_cols(p->tile), bp);
+                p->tmap_b_real = make_tmap(p->b.lmat.p, static_cast<int>(N), static_cast<int>(N),
+                                           qsb::gemm_tile_cols(p->tile), 1);
             } else {
                 std::fill(p->mat.begin(), p->mat.end(), 0);  // does not fit next to V: generate instead
             }
@@ -544,6 +549,12 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
         const int rows = qsb::gemm_tile_rows(p->tile);
         p->tmap[0] = make_tmap(p->b.v[0].p, p->M, p->N, rows, p->planes);
         if (p->b.v[1].p) p->tmap[1] = make_tmap(p->b.v[1].p, p->M, p->N, rows, p->planes);
+        // real layers (Li = 0) as two real GEMMs on the 3M tiles (QSB_NO_REAL: tests keep 3M)
+        p->real_ok = (p->tile == qsb::kTileWs3M || p->tile == qsb::kTileWs3MS) && !std::getenv("QSB_NO_REAL");
+        if (p->real_ok) {
+            p->tmap_real[0] = make_tmap(p->b.v[0].p, p->M, p->N, rows, 2);
+            if (p->b.v[1].p) p->tmap_real[1] = make_tmap(p->b.v[1].p, p->M, p->N, rows, 2);
+        }
     }
     // Plans executed on a caller's stream (qsb_plan_execute) must see the uploads.
     if (!borrow_cache) cuda_check(cudaStreamSynchronize(dc->stream), "cudaStreamSynchronize");
@@ -561,6 +572,18 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     in.expand_bytes = p->small ? 0.0 : 8.0 * p->planes * static_cast<double>(p->M) * static_cast<double>(N);
     in.gemm_tile = p->small ? -1 : p->tile;
     in.gemm_splits = p->small ? 1 : p->splits;
+    {
+        const double mn2 = static_cast<double>(p->M) * static_cast<double>(N) * static_cast<double>(N);
+        const bool three = p->tile == qsb::kTileWs3M || p->tile == qsb::kTileWs3MS;
+        in.n_real_gemms = 0;
+        in.gemm_hw_flops = 0.0;
+        for (size_t i = 1; i < p->chain.size() && !p->small; ++i) {
+            const bool real = p->real_ok && p->chain[i].real != 0;
+            in.n_real_gemms += real ? 1 : 0;
+            in.gemm_hw_flops += (real ? 4.0 : (three ? 6.0 : 8.0)) * mn2;
+        }
+        if (p->small) in.gemm_hw_flops = in.gemm_flops;
+    }
     in.v_planes = p->planes;
     return p;
 }
@@ -597,8 +620,12 @@ void enqueue(qsb_plan* p, cudaStream_t s) {
             cuda_check(qsb::launch_expand_t(p->chain[i], p->N, p->b.lmat.as<double>(),
                                             qsb::gemm_tile_b_planes(p->tile), s),
                        "expand_t_kernel");
-        qsb::GemmArgs a{&p->tmap[cur], &p->chain[i], p->b.v[1 - cur].as<double>(), p->M, p->N,
-                        mat ? &p->tmap_b : nullptr, p->splits};
+        qsb::GemmArgs a{&p->tmap[cur], &p->chain[i], p->b.v[1 - cur].as<double>(), p->M, p->N};
+        a.tmap_b = mat ? &p->tmap_b : nullptr;
+        a.real = p->real_ok && p->chain[i].real != 0;
+        a.tmap_real = &p->tmap_real[cur];
+        a.tmap_b_real = &p->tmap_b_real;
+        a.splits = p->splits;
         cuda_check(qsb::launch_zgemm(a, p->tile, p->h->gemm_mode, s), "zgemm_gen_kernel");
         cur ^= 1;
     }

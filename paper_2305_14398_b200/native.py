@@ -60,7 +60,7 @@ class QsbPlanInfo(ctypes.Structure):
         ("row_begin", ctypes.c_int64), ("row_count", ctypes.c_int64),
         ("gemm_flops", ctypes.c_double), ("expand_bytes", ctypes.c_double),
         ("gemm_tile", ctypes.c_int32), ("v_planes", ctypes.c_int32),
-        ("gemm_splits", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("gemm_splits", ctypes.c_int32), ("n_real_gemms", ctypes.c_int32), ("gemm_hw_flops", ctypes.c_double),
     ]
 
 

@@ -181,7 +181,7 @@ def test_abi_struct_layout():
     assert ctypes.sizeof(native.QsbCircuit) == 40
     assert ctypes.sizeof(native.QsbOptions) == 32
     assert ctypes.sizeof(native.QsbFunction) == 24
-    assert ctypes.sizeof(native.QsbPlanInfo) == 72
+    assert ctypes.sizeof(native.QsbPlanInfo) == 80
 
 
 def test_abi_rejects_bad_circuits():

@@ -489,3 +489,21 @@ def test_single_layer_and_tiny_circuits(sim, orc, n):
         ur, ui = sim.build_unitary(flat)
         orr, ori = orc.circuit_unitary(flat)
         assert rel_frob(ur, ui, orr, ori) <= TOL, (n, trial)
+
+
+@pytest.mark.parametrize("name,n", [("deutsch-jozsa", 11), ("entangle", 10), ("qft", 10)])
+def test_real_layers_as_two_real_gemms(monkeypatch, sim, orc, name, n):
+    """Layers with an exactly-zero imaginary plane (H, X, CNOT, DJ oracle) run as
+    two real GEMMs on the 3M tiles; U matches the full-3M run and the oracle."""
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+
+    c, reg = q.make_named_circuit(name, n)
+    flat = native.flatten(c, reg)
+    a = sim.build_unitary(flat)
+    monkeypatch.setenv("QSB_NO_REAL", "1")
+    b = sim.build_unitary(flat)
+    assert rel_frob(a[0], a[1], b[0], b[1]) <= TOL
+    for col in (0, 3, (1 << n) - 1):
+        cr, ci = orc.unitary_column(flat, col)
+        assert rel_frob(a[0][:, col], a[1][:, col], cr, ci) <= TOL
