@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -791,8 +792,13 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
     auto release_all = [&] {
         for (auto& p : plans) release_plan(p);
     };
+    // QSB_TRACE=1: host-side phase timings of this call on stderr
+    static const bool trace = std::getenv("QSB_TRACE") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    const auto t0 = now();
     try {
         for (int g = 0; g < G; ++g) plans[g] = make_plan(h, h->devs[g].get(), c, g * rows, rows, true);
+        const auto t1 = now();
         for (int g = 0; g < G; ++g) {
             qsb_plan* p = plans[g].get();
             DeviceScope ds(p->dc->device);
@@ -825,6 +831,7 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
                                            cudaMemcpyDeviceToHost, s), "download U");
             }
         }
+        const auto t2 = now();
         for (int g = 0; g < G; ++g) {
             DeviceScope ds(plans[g]->dc->device);
             cuda_check(cudaStreamSynchronize(plans[g]->dc->stream), "cudaStreamSynchronize");
@@ -834,6 +841,12 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
                 std::memcpy(psi_re + p->row_begin, staged[g] + off, rows * 8);
                 std::memcpy(psi_im + p->row_begin, staged[g] + p->M + off, rows * 8);
             }
+        }
+        if (trace) {
+            const auto t3 = now();
+            auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+            std::fprintf(stderr, "qsb trace: n=%d plans %.0f us, enqueue %.0f us, wait+copy %.0f us\n",
+                         c->n_qubits, us(t0, t1), us(t1, t2), us(t2, t3));
         }
     } catch (...) {
         release_all();
