@@ -302,3 +302,34 @@ def test_register_batches_interpreted_and_compiled(monkeypatch, golden, jit, k):
         out = s.simulate_full_state(golden.flat(case))
         assert bit_equal(out.re, golden[f"{case}:fsv_re"]) and bit_equal(out.im, golden[f"{case}:fsv_im"]), case
     s.close()
+
+
+def test_function_errors_match_reference(fsv, structured, sim):
+    """apply_function's dimension check (fsv_backend.cpp:90-95) and the unitary
+    backend's registry re-check (unitary_backend.cpp:50-53) through the C ABI."""
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+    from paper_2305_14398_b200.errors import LookupError_, ValidationError
+
+    reg = q.GateRegistry()
+    reg.register_function("swap2", np.array([[1, 0, 0, 0], [0, 0, 1, 0], [0, 1, 0, 0], [0, 0, 0, 1]], dtype=complex))
+    c = q.Circuit(3).h(0)
+    c.add_function("swap2", 1, 2, reg)
+    flat = native.flatten(c, reg)
+    ops = flat.ops.copy()
+    # the registered matrix no longer matches the op's 2 qubits
+    bad_tab = [(np.eye(8), np.zeros((8, 8)))]
+    bad = native.flat_from_arrays(3, flat.step_offsets, ops, bad_tab)
+    with pytest.raises(ValidationError, match="apply_function: matrix dimension 8 does not match 2\\^2"):
+        fsv.simulate_full_state(bad)
+    with pytest.raises(ValidationError):
+        structured.simulate_full_state(bad)
+    with pytest.raises(ValidationError):
+        sim.simulate_full_state(bad)
+    # an op naming a function the registry does not hold
+    ops2 = ops.copy()
+    ops2["function"][ops2["kind"] == native.OP_FUNCTION] = 3
+    missing = native.flat_from_arrays(3, flat.step_offsets, ops2, [(np.eye(4), np.zeros((4, 4)))])
+    for s in (fsv, structured, sim):
+        with pytest.raises(LookupError_):
+            s.simulate_full_state(missing)
