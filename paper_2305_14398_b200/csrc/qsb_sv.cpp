@@ -380,12 +380,30 @@ std::string emit_reg_kernel(const std::string& name, const qsb::SvRegBatch& b, s
             if (e & (1 << i)) p |= 1u << b.t[i];
         return p;
     };
-    for (int e = 0; e < E; ++e)
-        put("    double r%d = __ldcs(re + (f | 0x%xu)); double i%d = __ldcs(im + (f | 0x%xu));\n", e, pat(e), e,
-            pat(e));
+    // With flat bit 0 among the targets, elements e and e | 1 are adjacent words:
+    // one 16-byte access for the pair (f has bit 0 clear, so it is aligned).
+    const bool pairs = K > 0 && b.t[0] == 0;
+    if (pairs) {
+        for (int e = 0; e < E; e += 2)
+            put("    double r%d, r%d, i%d, i%d; { const double2 a = __ldcs(reinterpret_cast<const double2*>(re + (f | 0x%xu)));"
+                " const double2 b = __ldcs(reinterpret_cast<const double2*>(im + (f | 0x%xu)));"
+                " r%d = a.x; r%d = a.y; i%d = b.x; i%d = b.y; }\n",
+                e, e + 1, e, e + 1, pat(e), pat(e), e, e + 1, e, e + 1);
+    } else {
+        for (int e = 0; e < E; ++e)
+            put("    double r%d = __ldcs(re + (f | 0x%xu)); double i%d = __ldcs(im + (f | 0x%xu));\n", e, pat(e), e,
+                pat(e));
+    }
     o += body;
-    for (int e = 0; e < E; ++e)
-        put("    __stcs(re + (f | 0x%xu), r%d); __stcs(im + (f | 0x%xu), i%d);\n", pat(e), loc[e], pat(e), loc[e]);
+    if (pairs) {
+        for (int e = 0; e < E; e += 2)
+            put("    __stcs(reinterpret_cast<double2*>(re + (f | 0x%xu)), make_double2(r%d, r%d));"
+                " __stcs(reinterpret_cast<double2*>(im + (f | 0x%xu)), make_double2(i%d, i%d));\n",
+                pat(e), loc[e], loc[e + 1], pat(e), loc[e], loc[e + 1]);
+    } else {
+        for (int e = 0; e < E; ++e)
+            put("    __stcs(re + (f | 0x%xu), r%d); __stcs(im + (f | 0x%xu), i%d);\n", pat(e), loc[e], pat(e), loc[e]);
+    }
     o += "  }\n}\n";
     return o;
 }

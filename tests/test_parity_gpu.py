@@ -507,3 +507,37 @@ def test_real_layers_as_two_real_gemms(monkeypatch, sim, orc, name, n):
     for col in (0, 3, (1 << n) - 1):
         cr, ci = orc.unitary_column(flat, col)
         assert rel_frob(a[0][:, col], a[1][:, col], cr, ci) <= TOL
+
+
+def test_concurrent_host_calls_on_one_handle(golden):
+    """simulate_full_state is const and reentrant (simulator.hpp:44-45): calls from
+    several host threads on one handle serialise internally and stay correct."""
+    import threading
+
+    from paper_2305_14398_b200.simulator import (B200FsvSimulator, B200StructuredUnitarySimulator,
+                                                 B200UnitarySimulator)
+
+    cases = ["qft9", "dj9", "entangle10", "qft5", "edge_wide_span"] + golden.suites["cross"][:10]
+    # the npz archive is not thread-safe: load every input and expectation up front
+    data = {case: (golden.flat(case), golden.psi(case)) for case in cases}
+    for cls in (B200UnitarySimulator, B200StructuredUnitarySimulator, B200FsvSimulator):
+        s = cls()
+        errors = []
+
+        def worker(k):
+            try:
+                for case in cases[k::3] * 3:
+                    flat, (re, im) = data[case]
+                    out = s.simulate_full_state(flat)
+                    if rel_frob(out.re, out.im, re, im) > TOL:
+                        errors.append((cls.__name__, case))
+            except Exception as e:  # noqa: BLE001
+                errors.append((cls.__name__, repr(e)))
+
+        threads = [threading.Thread(target=worker, args=(k,)) for k in range(3)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        s.close()
+        assert not errors, errors[:3]
