@@ -541,3 +541,35 @@ def test_concurrent_host_calls_on_one_handle(golden):
             t.join()
         s.close()
         assert not errors, errors[:3]
+
+
+def test_qft14_row_shard_matches_dft(sim):
+    """The north-star size: rows [0, N/8) of the QFT-14 unitary (one rank's
+    shard of the 8-GPU decomposition, 16384 x 2048 complex) equal the DFT
+    matrix within 1e-10 relative (QFT == DFT: test_circuit_library.cpp:161-167,
+    acceptance_main.cpp:173-180)."""
+    import torch
+
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+    from paper_2305_14398_b200.simulator import torch_view
+
+    n = 14
+    N = 1 << n
+    rows = N // 8
+    c, reg = q.make_named_circuit("qft", n)
+    plan = sim.plan(native.flatten(c, reg), None, 0, rows)
+    plan.execute()
+    torch.cuda.synchronize()
+    re_p, im_p = plan.unitary_device()
+    ur = torch_view(re_p, (rows, N))
+    ui = torch_view(im_p, (rows, N))
+    j = torch.arange(rows, device=ur.device, dtype=torch.int64)[:, None]
+    k = torch.arange(N, device=ur.device, dtype=torch.int64)[None, :]
+    ang = (2.0 * np.pi / N) * ((j * k) % N).to(torch.float64)
+    dr = torch.cos(ang) / np.sqrt(N)
+    di = torch.sin(ang) / np.sqrt(N)
+    num = torch.sqrt(((ur - dr) ** 2 + (ui - di) ** 2).sum()).item()
+    den = torch.sqrt((dr ** 2 + di ** 2).sum()).item()
+    plan.close()
+    assert num / den <= TOL, num / den
