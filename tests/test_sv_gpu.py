@@ -91,7 +91,7 @@ def _function_circuit(n, first, count, seed, extra=True):
 
 
 @pytest.mark.parametrize("n,first,count,slab_bits", [
-    (6, 1, 3, None), (8, 0, 8, None), (9, 2, 4, "6"), (10, 3, 5, "8"), (13, 4, 6, None), (13, 0, 13, None),
+    (6, 1, 3, None), (8, 0, 8, None), (9, 2, 4, "6"), (10, 3, 5, "8"), (13, 4, 6, None), (12, 0, 12, None),
     (14, 5, 9, None), (12, 0, 3, "6"),
 ])
 def test_fsv_apply_function_blocks(monkeypatch, fsv, orc, n, first, count, slab_bits):
