@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "qsb_internal.hpp"
 
@@ -648,7 +649,14 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        if (MAT_B) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     }
+    // Programmatic dependent launch: everything above overlapped the previous
+    // GEMM's tail; from here on we read its output (A) and overwrite its input
+    // (out), so wait for its completion. Then let the next GEMM start launching.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     __syncthreads();
 
     if (warp >= C::CONSUMER_WARPS) {
@@ -1009,24 +1017,26 @@ static int launch_ws_t(const GemmArgs& a, void* stream) {
     const CUtensorMap& tmA = *static_cast<const CUtensorMap*>(REAL && a.tmap_real ? a.tmap_real : a.tmap);
     const CUtensorMap& tmB =
         MAT_B ? *static_cast<const CUtensorMap*>(REAL && a.tmap_b_real ? a.tmap_b_real : a.tmap_b) : tmA;
-    if (splits == 1) {
-        dim3 grid(a.N / C::BN, a.M / C::BM);
-        zgemm_ws_kernel<THREE_M, SUMPLANE, MAT_B, REAL>
-            <<<grid, C::THREADS, C::SMEM, static_cast<cudaStream_t>(stream)>>>(tmA, tmB, *a.layer, a.out, a.M, a.N);
-        return static_cast<int>(cudaGetLastError());
-    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.N / C::BN, a.M / C::BM, splits);
     cfg.blockDim = dim3(C::THREADS, 1, 1);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = static_cast<cudaStream_t>(stream);
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 1;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = splits;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    // chained GEMMs overlap launch and prologue with the previous one's tail (griddepcontrol)
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = std::getenv("QSB_NO_PDL") ? 0 : 1;
+    ++na;
+    if (splits > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = 1;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = splits;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     return static_cast<int>(cudaLaunchKernelEx(&cfg, zgemm_ws_kernel<THREE_M, SUMPLANE, MAT_B, REAL>, tmA, tmB,
                                                *a.layer, a.out, a.M, a.N));
 }
