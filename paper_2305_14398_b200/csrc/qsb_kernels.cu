@@ -945,31 +945,40 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
                                      "d"(acc[a][i][j][e])
                                      : "memory");
         cluster_sync();
+        // Rank r's share: the row blocks i with i * splits / 4 == r (none when splits = 8 and r is
+        // odd). All remote loads of a fragment are issued before any add, so their DSMEM latencies
+        // overlap instead of chaining; the sum then runs over ranks 0..s-1 in order (deterministic).
+        uint32_t src[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (q < splits) asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(src[q]) : "r"(part), "r"(q));
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             if ((i * splits) / 4 != rank) continue;
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
+                double x[8][NACC][2];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (q >= splits) break;
+#pragma unroll
+                    for (int a = 0; a < NACC; ++a)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e)
+                            asm volatile("ld.shared::cluster.f64 %0, [%1];"
+                                         : "=d"(x[q][a][e])
+                                         : "r"(src[q] + vidx(a, i, j, e) * CT * 8));
+                }
                 double f[NACC][2];
 #pragma unroll
                 for (int a = 0; a < NACC; ++a)
 #pragma unroll
-                    for (int e = 0; e < 2; ++e) f[a][e] = 0.0;
-                for (int q = 0; q < splits; ++q) {
-                    uint32_t src;
-                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(src) : "r"(part), "r"(q));
+                    for (int e = 0; e < 2; ++e) {
+                        f[a][e] = x[0][a][e];
 #pragma unroll
-                    for (int a = 0; a < NACC; ++a)
-#pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            double x;
-                            asm volatile("ld.shared::cluster.f64 %0, [%1];"
-                                         : "=d"(x)
-                                         : "r"(src + vidx(a, i, j, e) * CT * 8)
-                                         : "memory");
-                            f[a][e] = q == 0 ? x : f[a][e] + x;
-                        }
-                }
+                        for (int q = 1; q < 8; ++q)
+                            if (q < splits) f[a][e] = f[a][e] + x[q][a][e];
+                    }
                 store(i, j, f);
             }
         }
