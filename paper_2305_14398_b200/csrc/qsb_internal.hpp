@@ -99,6 +99,7 @@ int launch_gram_small(const double* re, const double* im, int N, unsigned long l
 // Tile shapes of the K2 GEMM (rows x cols of the output tile).
 enum GemmTile : int { kTile128x64 = 0, kTile64x64 = 1, kTile32x32 = 2, kTileWs4M = 3, kTileWs3M = 4, kTileWs3MS = 5 };
 int configure_kernels();
+int ws_max_active_clusters(int splits);  // co-resident clusters of the warp-specialised K2 per split size
 int gemm_tile_rows(int tile);
 int gemm_tile_cols(int tile);
 size_t small_circuit_smem_bytes(int M, int N);

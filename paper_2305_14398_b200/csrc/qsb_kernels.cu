@@ -1093,6 +1093,41 @@ int launch_expand_t(const LayerDesc& layer, int N, double* out, int planes, void
 
 int gemm_tile_b_planes(int tile) { return tile == kTileWs3MS || tile == kTileWs3M ? 3 : 2; }
 
+// Co-resident clusters of the warp-specialised kernel per split size (index log2 s),
+// from the occupancy API at configure time: clusters must fit inside a GPC, so
+// e.g. clusters of 8 do not tile 148 SMs.
+static int g_ws_clusters[4] = {148, 74, 37, 18};
+
+int ws_max_active_clusters(int splits) {
+    const int i = splits >= 8 ? 3 : (splits >= 4 ? 2 : (splits >= 2 ? 1 : 0));
+    return g_ws_clusters[i];
+}
+
+static void query_ws_clusters() {
+    using C = WsCfg<true, true>;
+    for (int i = 1; i < 4; ++i) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(1, 1, 1 << i);
+        cfg.blockDim = dim3(C::THREADS, 1, 1);
+        cfg.dynamicSmemBytes = C::SMEM;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 1;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1 << i;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, zgemm_ws_kernel<true, true, false, false>, &cfg) == cudaSuccess && n > 0)
+            g_ws_clusters[i] = n;
+        else
+            cudaGetLastError();
+    }
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    g_ws_clusters[0] = sms;
+}
+
 int gemm_tile_rows(int tile) {
     switch (tile) {
     case kTile128x64: return 128;
@@ -1404,6 +1439,7 @@ int configure_kernels() {
     if ((e = configure_ws_t<false, false>())) return e;
     if ((e = configure_ws_t<true, false>())) return e;
     if ((e = configure_ws_t<true, true>())) return e;
+    query_ws_clusters();
     if ((e = static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel<32>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024))))
         return e;

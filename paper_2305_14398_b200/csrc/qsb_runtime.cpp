@@ -387,7 +387,9 @@ int pick_splits(int64_t T, int KT) {
     double best_t = 1e30;
     for (int s = 1; s <= 8; s *= 2) {
         if (KT / s < 2) break;
-        const double waves = std::ceil(static_cast<double>(T * s) / sms);
+        // clusters of s CTAs must fit inside a GPC: waves from the co-resident cluster count
+        const double active = std::min(sms / s, static_cast<double>(qsb::ws_max_active_clusters(s)));
+        const double waves = std::ceil(static_cast<double>(T) / active);
         const double t = waves * (fixed_us + (s > 1 ? reduce_us : 0.0) + ktile_us * static_cast<double>(KT) / s);
         if (t < 0.97 * best_t) {
             best_t = t;
