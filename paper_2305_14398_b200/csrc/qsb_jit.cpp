@@ -138,10 +138,18 @@ std::vector<void*> kernels(const std::string& source, const std::vector<std::str
     return out;
 }
 
-int launch(void* fn, unsigned grid, unsigned block, void* stream, void** args) {
+int launch(void* fn, unsigned grid, unsigned block, void* stream, void** args, int smem) {
     static LaunchFn l = driver<LaunchFn>("cuLaunchKernel");
+    using SetAttrFn = CUresult (*)(CUfunction, CUfunction_attribute, int);
+    static SetAttrFn set_attr = driver<SetAttrFn>("cuFuncSetAttribute");
     if (!l) return static_cast<int>(cudaErrorNotSupported);
-    const CUresult r = l(reinterpret_cast<CUfunction>(fn), grid, 1, 1, block, 1, 1, 0,
+    if (smem > 48 * 1024) {
+        if (!set_attr ||
+            set_attr(reinterpret_cast<CUfunction>(fn), CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem) !=
+                CUDA_SUCCESS)
+            return static_cast<int>(cudaErrorLaunchFailure);
+    }
+    const CUresult r = l(reinterpret_cast<CUfunction>(fn), grid, 1, 1, block, 1, 1, static_cast<unsigned>(smem),
                          reinterpret_cast<CUstream>(stream), args, nullptr);
     return r == CUDA_SUCCESS ? 0 : static_cast<int>(cudaErrorLaunchFailure);
 }

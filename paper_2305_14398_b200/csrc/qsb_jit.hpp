@@ -32,7 +32,7 @@ bool forced();
 // current device (sm_100a) or taken from the process-wide cache.
 std::vector<void*> kernels(const std::string& source, const std::vector<std::string>& names);
 
-// cuLaunchKernel(fn, grid x 1 x 1, block x 1 x 1, no dynamic shared memory).
-int launch(void* fn, unsigned grid, unsigned block, void* stream, void** args);
+// cuLaunchKernel(fn, grid x 1 x 1, block x 1 x 1, smem bytes of dynamic shared memory).
+int launch(void* fn, unsigned grid, unsigned block, void* stream, void** args, int smem = 0);
 
 }  // namespace qsbjit

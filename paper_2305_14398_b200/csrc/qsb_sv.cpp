@@ -41,6 +41,7 @@ struct qsb_sv_plan {
         std::shared_ptr<qsb::SvRegBatch> reg;  // kReg: gates / controlled gates, elements in registers
         void* jit = nullptr;                   // kReg: the batch compiled straight-line (qsb_jit.hpp), or null
         std::vector<double> coef;              // kReg + jit: the coefficients, in the kernel's parameter order
+        int jit_smem = 0;                      // kReg + jit: dynamic shared memory (prefetch slots)
         qsb::SvBatch batch;   // kSlab: small apply_function blocks in shared memory
         FnPass f;             // kFn: apply_function blocks larger than a slab
     };
@@ -255,7 +256,8 @@ const char* kJitPrelude = R"(
 // (fsv_backend.cpp:52-55, classes qsb_sv.hpp), with every target, control and
 // class a constant; X / CNOT pairs without an outer control are a renaming of
 // the element variables. Coefficients are appended to *coef in parameter order.
-std::string emit_reg_kernel(const std::string& name, const qsb::SvRegBatch& b, std::vector<double>* coef) {
+std::string emit_reg_kernel(const std::string& name, const qsb::SvRegBatch& b, std::vector<double>* coef,
+                            bool prefetch) {
     const int K = b.K, E = 1 << K;
     std::string o;
     char buf[512];
@@ -367,32 +369,67 @@ std::string emit_reg_kernel(const std::string& name, const qsb::SvRegBatch& b, s
     put("extern \"C\" __global__ void __launch_bounds__(%d) %s(double* __restrict__ re, double* __restrict__ im,"
         " long long groups, const __grid_constant__ QsbCoef_%s c) {\n",
         qsb::kSvRegThreads, name.c_str(), name.c_str());
-    o += "  const long long stride = (long long)gridDim.x * blockDim.x;\n";
-    o += "  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {\n";
-    o += "    unsigned f = (unsigned)g;\n";
-    for (int i = 0; i < K; ++i) {
-        const unsigned low = (1u << b.t[i]) - 1u;
-        put("    f = ((f & ~0x%xu) << 1) | (f & 0x%xu);\n", low, low);
-    }
     auto pat = [&](int e) {
         unsigned p = 0;
         for (int i = 0; i < K; ++i)
             if (e & (1 << i)) p |= 1u << b.t[i];
         return p;
     };
+    std::string base_fn;  // element 0 of group g: g with a zero inserted at every target bit
+    for (int i = 0; i < K; ++i) {
+        const unsigned low = (1u << b.t[i]) - 1u;
+        std::snprintf(buf, sizeof buf, "    f = ((f & ~0x%xu) << 1) | (f & 0x%xu);\n", low, low);
+        base_fn += buf;
+    }
     // With flat bit 0 among the targets, elements e and e | 1 are adjacent words:
     // one 16-byte access for the pair (f has bit 0 clear, so it is aligned).
     const bool pairs = K > 0 && b.t[0] == 0;
-    if (pairs) {
-        for (int e = 0; e < E; e += 2)
-            put("    double r%d, r%d, i%d, i%d; { const double2 a = __ldcs(reinterpret_cast<const double2*>(re + (f | 0x%xu)));"
-                " const double2 b = __ldcs(reinterpret_cast<const double2*>(im + (f | 0x%xu)));"
-                " r%d = a.x; r%d = a.y; i%d = b.x; i%d = b.y; }\n",
-                e, e + 1, e, e + 1, pat(e), pat(e), e, e + 1, e, e + 1);
-    } else {
+    o += "  const long long stride = (long long)gridDim.x * blockDim.x;\n";
+    if (prefetch) {
+        // The next group streams into this thread's shared-memory slots (cp.async,
+        // [element][plane][thread]) while the current one is updated and stored.
+        auto issue = [&](const char* indent) {
+            for (int e = 0; e < E; ++e)
+                put("%sasm volatile(\"cp.async.ca.shared.global [%%0], [%%1], 8;\" :: \"r\"(slot + %uu), \"l\"(re + (f | 0x%xu)) : \"memory\");"
+                    " asm volatile(\"cp.async.ca.shared.global [%%0], [%%1], 8;\" :: \"r\"(slot + %uu), \"l\"(im + (f | 0x%xu)) : \"memory\");\n",
+                    indent, static_cast<unsigned>((2 * e) * qsb::kSvRegThreads * 8), pat(e),
+                    static_cast<unsigned>((2 * e + 1) * qsb::kSvRegThreads * 8), pat(e));
+            put("%sasm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n", indent);
+        };
+        o += "  extern __shared__ double qsb_slots[];\n";
+        o += "  const unsigned slot = (unsigned)__cvta_generic_to_shared(qsb_slots) + threadIdx.x * 8u;\n";
+        o += "  long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;\n";
+        o += "  if (g < groups) {\n    unsigned f = (unsigned)g;\n" + base_fn;
+        issue("    ");
+        o += "  }\n";
+        o += "  for (; g < groups; g += stride) {\n    unsigned f = (unsigned)g;\n" + base_fn;
+        o += "    asm volatile(\"cp.async.wait_all;\" ::: \"memory\");\n";
         for (int e = 0; e < E; ++e)
-            put("    double r%d = __ldcs(re + (f | 0x%xu)); double i%d = __ldcs(im + (f | 0x%xu));\n", e, pat(e), e,
-                pat(e));
+            put("    double r%d = qsb_slots[%d * %d + threadIdx.x]; double i%d = qsb_slots[%d * %d + threadIdx.x];\n", e,
+                2 * e, qsb::kSvRegThreads, e, 2 * e + 1, qsb::kSvRegThreads);
+        o += "    if (g + stride < groups) {\n      const unsigned f0 = f;\n      { unsigned f = (unsigned)(g + stride);\n";
+        std::string indented;
+        for (size_t q = 0; q < base_fn.size(); ++q) {
+            if (q == 0 || base_fn[q - 1] == '\n') indented += "    ";
+            indented += base_fn[q];
+        }
+        o += indented;
+        issue("        ");
+        o += "      }\n      (void)f0;\n    }\n";
+    } else {
+        o += "  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {\n";
+        o += "    unsigned f = (unsigned)g;\n" + base_fn;
+        if (pairs) {
+            for (int e = 0; e < E; e += 2)
+                put("    double r%d, r%d, i%d, i%d; { const double2 a = __ldcs(reinterpret_cast<const double2*>(re + (f | 0x%xu)));"
+                    " const double2 b = __ldcs(reinterpret_cast<const double2*>(im + (f | 0x%xu)));"
+                    " r%d = a.x; r%d = a.y; i%d = b.x; i%d = b.y; }\n",
+                    e, e + 1, e, e + 1, pat(e), pat(e), e, e + 1, e, e + 1);
+        } else {
+            for (int e = 0; e < E; ++e)
+                put("    double r%d = __ldcs(re + (f | 0x%xu)); double i%d = __ldcs(im + (f | 0x%xu));\n", e, pat(e), e,
+                    pat(e));
+        }
     }
     o += body;
     if (pairs) {
@@ -413,6 +450,9 @@ void jit_register_batches(qsb_sv_plan* p) {
     if (!qsbjit::available()) return;
     if (p->m < 18 && !qsbjit::forced()) return;  // small arrays: the interpreted kernel, no compile latency
     std::string src = kJitPrelude;
+    // cp.async prefetch of the next group (QSB_SV_JIT_PREFETCH=0: direct loads)
+    const char* pe = std::getenv("QSB_SV_JIT_PREFETCH");
+    const bool prefetch = !(pe && std::strcmp(pe, "0") == 0);
     std::vector<std::string> names;
     std::vector<size_t> idx;
     for (size_t i = 0; i < p->passes.size(); ++i) {
@@ -420,7 +460,7 @@ void jit_register_batches(qsb_sv_plan* p) {
         if (ps.kind != qsb_sv_plan::kReg) continue;
         const std::string name = "qsb_sv_b" + std::to_string(i);
         ps.coef.clear();
-        src += emit_reg_kernel(name, *ps.reg, &ps.coef);
+        src += emit_reg_kernel(name, *ps.reg, &ps.coef, prefetch);
         names.push_back(name);
         idx.push_back(i);
     }
@@ -435,6 +475,7 @@ void jit_register_batches(qsb_sv_plan* p) {
     for (size_t k = 0; k < idx.size(); ++k) {
         qsb_sv_plan::Pass& ps = p->passes[idx[k]];
         ps.jit = fns[k];
+        ps.jit_smem = prefetch ? 2 * (1 << ps.reg->K) * qsb::kSvRegThreads * 8 : 0;
         if (ps.coef.empty()) ps.coef.push_back(0.0);
     }
 }
@@ -648,7 +689,7 @@ void sv_execute(qsb_sv_plan* p, cudaStream_t s) {
             void* args[] = {&vre, &vim, &groups, const_cast<double*>(ps.coef.data())};
             const long long blocks = (groups + qsb::kSvRegThreads - 1) / qsb::kSvRegThreads;
             const unsigned grid = static_cast<unsigned>(std::min<long long>(blocks, 148LL * 8));
-            cuda_check(qsbjit::launch(ps.jit, grid, qsb::kSvRegThreads, s, args), "sv jit kernel");
+            cuda_check(qsbjit::launch(ps.jit, grid, qsb::kSvRegThreads, s, args, ps.jit_smem), "sv jit kernel");
         } else if (ps.kind == qsb_sv_plan::kReg) {
             cuda_check(qsb::sv_launch_reg(v, v + elems, *ps.reg, s), "sv_reg_kernel");
         } else if (ps.kind == qsb_sv_plan::kSlab) {
