@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <thread>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -140,6 +142,23 @@ std::vector<int> first_fit(const qsb_circuit* c, int step, int* n_layers) {
     return layer;
 }
 
+// Every entry exactly zero? Large planes are scanned in parallel chunks.
+bool all_zero(const double* x, size_t n) {
+    auto chunk = [x](size_t b, size_t e) {
+        for (size_t i = b; i < e; ++i)
+            if (x[i] != 0.0) return false;
+        return true;
+    };
+    const size_t workers = n >= (size_t{1} << 20) ? std::min<size_t>(16, std::max(1u, std::thread::hardware_concurrency())) : 1;
+    if (workers <= 1) return chunk(0, n);
+    std::vector<char> ok(workers, 1);
+    std::vector<std::thread> pool;
+    for (size_t w = 0; w < workers; ++w)
+        pool.emplace_back([&, w] { ok[w] = chunk(n * w / workers, n * (w + 1) / workers); });
+    for (auto& t : pool) t.join();
+    return std::all_of(ok.begin(), ok.end(), [](char v) { return v != 0; });
+}
+
 // LayerDesc of one layer: non-identity blocks sorted by first qubit (fill_layer order).
 qsb::LayerDesc build_layer(const qsb_circuit* c, int step, const std::vector<int>& layer_of, int layer) {
     const int n = c->n_qubits;
@@ -185,8 +204,7 @@ qsb::LayerDesc build_layer(const qsb_circuit* c, int step, const std::vector<int
         if (blk.kind == qsb::kBlockTable) {
             const qsb_function& f = c->functions[reinterpret_cast<intptr_t>(blk.t_im)];
             const size_t d2 = static_cast<size_t>(f.dim) * f.dim;
-            for (size_t e = 0; e < d2 && d.real; ++e)
-                if (f.im[e] != 0.0) d.real = 0;
+            if (!all_zero(f.im, d2)) d.real = 0;
         } else {
             for (int e = 0; e < 4; ++e)
                 if (blk.u_im[e] != 0.0) d.real = 0;
@@ -311,23 +329,34 @@ void upload_tables(qsb_plan* p, const qsb_circuit* c) {
     for (int f : p->cc.used_functions) {
         const qsb_function& fn = c->functions[f];
         const size_t d = static_cast<size_t>(fn.dim);
-        bool is_mono = !force_dense;
         cols[f].assign(d, -1);
         vre[f].assign(d, 0.0);
         vim[f].assign(d, 0.0);
-        for (size_t r = 0; r < d && is_mono; ++r)
-            for (size_t k = 0; k < d; ++k) {
-                const double a = fn.re[r * d + k], b = fn.im[r * d + k];
-                if (a == 0.0 && b == 0.0) continue;
-                if (cols[f][r] >= 0) {
-                    is_mono = false;
-                    break;
+        // rows scanned in parallel chunks on the host's cores (a DJ-11 oracle is 4M entries)
+        std::atomic<bool> is_mono{!force_dense};
+        auto scan = [&](size_t r0, size_t r1) {
+            for (size_t r = r0; r < r1 && is_mono.load(std::memory_order_relaxed); ++r)
+                for (size_t k = 0; k < d; ++k) {
+                    const double a = fn.re[r * d + k], b = fn.im[r * d + k];
+                    if (a == 0.0 && b == 0.0) continue;
+                    if (cols[f][r] >= 0) {
+                        is_mono.store(false, std::memory_order_relaxed);
+                        return;
+                    }
+                    cols[f][r] = static_cast<int32_t>(k);
+                    vre[f][r] = a;
+                    vim[f][r] = b;
                 }
-                cols[f][r] = static_cast<int32_t>(k);
-                vre[f][r] = a;
-                vim[f][r] = b;
-            }
-        mono[f] = is_mono;
+        };
+        const size_t workers = d >= 512 ? std::min<size_t>(16, std::max(1u, std::thread::hardware_concurrency())) : 1;
+        if (workers <= 1 || !is_mono) {
+            if (is_mono) scan(0, d);
+        } else {
+            std::vector<std::thread> pool;
+            for (size_t w = 0; w < workers; ++w) pool.emplace_back(scan, d * w / workers, d * (w + 1) / workers);
+            for (auto& t : pool) t.join();
+        }
+        mono[f] = is_mono.load();
         off[f] = total;
         total += is_mono ? 2 * d + (d + 1) / 2 : 2 * d * d;
     }

@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <thread>
 #include <vector>
 
 #include "../../include/qsb.h"
@@ -587,18 +588,43 @@ std::unique_ptr<qsb_sv_plan> make_sv_plan(qsb_handle* h, DeviceCtx* dc, const qs
             const qsb_function& fn = c->functions[fi];
             const int64_t d = fn.dim;
             Csr& cs = csr[fi];
-            cs.rp.reserve(d + 1);
-            cs.rp.push_back(0);
-            for (int64_t r = 0; r < d; ++r) {
-                for (int64_t k = 0; k < d; ++k) {
-                    const double a = fn.re[r * d + k], b = fn.im[r * d + k];
-                    if (a == 0.0 && b == 0.0) continue;
-                    cs.ci.push_back(static_cast<int32_t>(k));
-                    cs.vr.push_back(a);
-                    cs.vi.push_back(b);
+            // two parallel sweeps over row chunks (count, then fill) on the host's cores
+            const int64_t workers =
+                d >= 512 ? std::min<int64_t>(16, std::max(1u, std::thread::hardware_concurrency())) : 1;
+            auto run = [&](auto&& body) {
+                if (workers <= 1) {
+                    body(int64_t{0}, d);
+                    return;
                 }
-                cs.rp.push_back(static_cast<int32_t>(cs.ci.size()));
-            }
+                std::vector<std::thread> pool;
+                for (int64_t w = 0; w < workers; ++w) pool.emplace_back(body, d * w / workers, d * (w + 1) / workers);
+                for (auto& t : pool) t.join();
+            };
+            cs.rp.assign(d + 1, 0);
+            run([&](int64_t r0, int64_t r1) {
+                for (int64_t r = r0; r < r1; ++r) {
+                    int32_t nz = 0;
+                    for (int64_t k = 0; k < d; ++k) nz += (fn.re[r * d + k] != 0.0 || fn.im[r * d + k] != 0.0);
+                    cs.rp[r + 1] = nz;
+                }
+            });
+            for (int64_t r = 0; r < d; ++r) cs.rp[r + 1] += cs.rp[r];
+            cs.ci.resize(cs.rp[d]);
+            cs.vr.resize(cs.rp[d]);
+            cs.vi.resize(cs.rp[d]);
+            run([&](int64_t r0, int64_t r1) {
+                for (int64_t r = r0; r < r1; ++r) {
+                    int32_t z = cs.rp[r];
+                    for (int64_t k = 0; k < d; ++k) {
+                        const double a = fn.re[r * d + k], b = fn.im[r * d + k];
+                        if (a == 0.0 && b == 0.0) continue;
+                        cs.ci[z] = static_cast<int32_t>(k);
+                        cs.vr[z] = a;
+                        cs.vi[z] = b;
+                        ++z;
+                    }
+                }
+            });
             bytes += 16 * cs.vr.size() + 4 * (cs.rp.size() + cs.ci.size()) + 64;
         }
         if (bytes > 0) {
