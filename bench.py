@@ -239,13 +239,32 @@ class ClockSampler:
                 parts = [p.strip() for p in line.split(",")]
                 if len(parts) >= 9 and parts[1].isdigit():
                     rows.append(parts)
+        note = None
+        if not rows:
+            # a timed region shorter than the 200 ms sampling period: one query right after it
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=20)
+                for line in out.stdout.splitlines():
+                    parts = [p.strip() for p in line.split(",")]
+                    if len(parts) >= 9 and parts[1].isdigit():
+                        rows.append(parts)
+                note = "timed region shorter than the sampling period: sampled right after it"
+            except Exception:
+                pass
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         sm = [int(r[1]) for r in rows]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][2]), "reasons": reasons,
-                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3] not in ("", "[N/A]"))}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][2]), "reasons": reasons,
+               "samples": len(rows)}
+        powers = [float(r[3]) for r in rows if r[3] not in ("", "[N/A]")]
+        if powers:
+            out["power_w_max"] = max(powers)
+        if note:
+            out["note"] = note
+        return out
 
 
 # --------------------------------------------------------------- our arm
