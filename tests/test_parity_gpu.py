@@ -573,3 +573,26 @@ def test_qft14_row_shard_matches_dft(sim):
     den = torch.sqrt((dr ** 2 + di ** 2).sum()).item()
     plan.close()
     assert num / den <= TOL, num / den
+
+
+def test_hbm_limit_plans_fall_back_to_two_planes(sim):
+    """QFT-16 (65536^2): two 3-plane V buffers (206 GB) do not fit a B200, so the
+    plan keeps re/im planes only (in-register 3M sums) and generates every
+    operator instead of materialising (memory_estimate / guard:
+    unitary_backend.cpp:156-192)."""
+    import torch
+
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+
+    free, _ = torch.cuda.mem_get_info()
+    if free < 150e9:
+        pytest.skip("needs ~140 GB of free HBM")
+    c, reg = q.make_named_circuit("qft", 16)
+    plan = sim.plan(native.flatten(c, reg))
+    assert plan.info.v_planes == 2 and plan.info.gemm_tile == 4
+    assert plan.info.n_launches == 2 + plan.info.n_gemms  # no K1t launches
+    plan.close()
+    c, reg = q.make_named_circuit("qft", 17)
+    with pytest.raises(q.ResourceError, match="refuses 17 qubits"):
+        sim.simulate_full_state(c, reg)
