@@ -143,7 +143,8 @@ typedef struct qsb_plan_info {
     double expand_bytes;       /* bytes written by the K1 expansion */
     int32_t gemm_tile;         /* K2 variant: QSB_TILE_* */
     int32_t v_planes;          /* planes per V buffer (2, or 3 with the 3M sum plane) */
-    int32_t gemm_splits;       /* split-K cluster size of the K2 launches (1, 2, 4, 8) */
+    int32_t gemm_splits;       /* split-K cluster size of the K2 launches (1, 2, 4, 8), or -1:
+                                  stream-K (persistent CTAs share the tile x k-tile iterations) */
     int32_t n_real_gemms;      /* GEMMs whose operator is real: two real products instead of 3M's three */
     double gemm_hw_flops;      /* FP64 FLOPs the DMMAs actually execute: 6 M N^2 (3M), 4 M N^2 (real
                                   layer), 8 M N^2 (4M) per GEMM, summed; gemm_flops credits 8 M N^2 */

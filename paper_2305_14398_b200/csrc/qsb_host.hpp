@@ -116,6 +116,8 @@ struct Buffers {
     DevBuf p;        // probabilities
     DevBuf partial;  // reduction partials + norm
     DevBuf lmat;     // dense path: a materialised (transposed) layer operator for K2's TMA B operand
+    DevBuf skws;     // dense path: stream-K partial accumulators
+    DevBuf skflags;  // dense path: stream-K per-tile arrival counters
 };
 
 }  // namespace qsbh

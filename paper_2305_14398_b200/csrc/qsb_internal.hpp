@@ -59,6 +59,20 @@ struct LayerDesc {
     BlockDesc blocks[kMaxBlocks];
 };
 
+// Stream-K schedule of the warp-specialised K2: gridDim.x persistent CTAs share
+// the T x KT k-tile iterations evenly; a tile split between CTAs is finished by
+// the CTA holding its first k-tiles (the "owner"), which adds the partials the
+// other CTAs publish in `ws` (flag per tile) in k order — deterministic.
+struct SkArgs {
+    int enabled = 0;
+    int tiles_n = 0;        // output tiles along N
+    int tiles = 0;          // T
+    int maxc = 0;           // partial slots per tile
+    double* ws = nullptr;   // [P owner CTAs][maxc][values][256 consumer threads]
+    int* flags = nullptr;   // [P owner CTAs], zero between launches (each owner re-arms its own)
+    int* dbg = nullptr;     // QSB_SK_DEBUG: protocol anomaly counters
+};
+
 // Launch wrappers (qsb_kernels.cu). All return cudaError_t as int.
 struct GemmArgs {
     const void* tmap;        // CUtensorMap of the A operand (V, [2][M][N] doubles)
@@ -71,6 +85,7 @@ struct GemmArgs {
     bool real = false;             // 3M warp-specialised tiles: the operator is real -> two real GEMMs
     const void* tmap_real = nullptr;    // two-plane (re, im) view of A for the real variant
     const void* tmap_b_real = nullptr;  // one-plane (re) view of a materialised operator
+    SkArgs sk;               // warp-specialised tiles: stream-K schedule (sk.enabled)
     int splits = 1;          // warp-specialised tiles: K split over a thread-block cluster of this
                              // size (1, 2, 4); partial accumulators are summed through
                              // distributed shared memory in rank order (deterministic)
@@ -100,6 +115,7 @@ int launch_gram_small(const double* re, const double* im, int N, unsigned long l
 enum GemmTile : int { kTile128x64 = 0, kTile64x64 = 1, kTile32x32 = 2, kTileWs4M = 3, kTileWs3M = 4, kTileWs3MS = 5 };
 int configure_kernels();
 int ws_max_active_clusters(int splits);  // co-resident clusters of the warp-specialised K2 per split size
+int ws_partial_values(int tile);          // accumulator values per consumer thread of a tile variant
 int gemm_tile_rows(int tile);
 int gemm_tile_cols(int tile);
 size_t small_circuit_smem_bytes(int M, int N);

@@ -621,7 +621,8 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 template <bool THREE_M, bool SUMPLANE, bool MAT_B, bool REAL = false>
 __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
     zgemm_ws_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ LayerDesc layer, double* __restrict__ out, int M, int N) {
+                    const __grid_constant__ LayerDesc layer, double* __restrict__ out, int M, int N,
+                    const __grid_constant__ SkArgs sk) {
     using C = WsCfg<THREE_M, SUMPLANE, REAL>;
     constexpr int BM = C::BM, BN = C::BN;
     extern __shared__ uint8_t smem_raw[];
@@ -633,15 +634,28 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
-    const int m0 = blockIdx.y * BM;
-    const int n0 = blockIdx.x * BN;
     // split-K over the cluster (gridDim.z = cluster size): rank r owns k-tiles [kt0, kt1)
     const int splits = gridDim.z;
     const int rank = blockIdx.z;
     const int KTall = N / C::BK;
     const int kt0 = (KTall * rank) / splits;
     const int KT = (KTall * (rank + 1)) / splits - kt0;
-
+    // Work as segments of the flattened (tile, k-tile) iteration space: classic
+    // grids own one segment (their tile, their split-K range); stream-K CTAs own
+    // [I c / P, I (c + 1) / P) of the I = T KTall iterations.
+    const int tiles_n = N / BN;
+    const long long I = static_cast<long long>(sk.tiles) * KTall;
+    const long long it_begin =
+        sk.enabled ? I * blockIdx.x / gridDim.x
+                   : static_cast<long long>(blockIdx.y * tiles_n + blockIdx.x) * KTall + kt0;
+    const long long it_end = sk.enabled ? I * (blockIdx.x + 1) / gridDim.x : it_begin + KT;
+    // CTA whose stream-K share holds iteration x
+    auto cta_of = [&](long long x) {
+        long long c = x * gridDim.x / I;
+        while (c + 1 < gridDim.x && I * (c + 1) / gridDim.x <= x) ++c;
+        while (c > 0 && I * c / gridDim.x > x) --c;
+        return static_cast<int>(c);
+    };
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(sFull + 8 * s, 1 + C::PRODUCER_WARPS);
@@ -663,12 +677,19 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
         // ------------------------------ producer warpgroup
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::PRODUCER_REGS));
         const int ptid = tid - 32 * C::CONSUMER_WARPS;
-        for (int kt = 0; kt < KT; ++kt) {
-            const int s = kt % C::STAGES;
-            if (kt >= C::STAGES) mbar_wait(sEmpty + 8 * s, ((kt / C::STAGES) & 1) ^ 1);
+        int kc = 0;  // stage counter across segments
+        for (long long it = it_begin; it < it_end;) {
+        const int tile = static_cast<int>(it / KTall);
+        const int seg_k0 = static_cast<int>(it % KTall);
+        const int seg_k1 = static_cast<int>(min(static_cast<long long>(KTall), seg_k0 + (it_end - it)));
+        it += seg_k1 - seg_k0;
+        const int m0 = (tile / tiles_n) * BM;
+        const int n0 = (tile % tiles_n) * BN;
+        for (int ktg = seg_k0; ktg < seg_k1; ++ktg, ++kc) {
+            const int s = kc % C::STAGES;
+            if (kc >= C::STAGES) mbar_wait(sEmpty + 8 * s, ((kc / C::STAGES) & 1) ^ 1);
             const uint32_t stage = sBase + s * C::STAGE;
             const uint32_t tma_bar = sFull + 8 * s;
-            const int ktg = kt0 + kt;  // global k-tile
             const uint32_t bBase = stage + C::A_BYTES;
             if (MAT_B) {
                 if (ptid == 0) {
@@ -782,6 +803,7 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(sFull + 8 * s);
         }
+        }
         if (splits > 1) {  // every thread of the cluster takes part in both cluster barriers
             cluster_sync();
             cluster_sync();
@@ -797,6 +819,21 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
     const int wn = warp % C::CWN;
     constexpr int NT = C::NT;
     constexpr int NACC = (THREE_M && !REAL) ? 3 : 2;
+    int kc = 0;  // stage counter across segments (mirrors the producer's)
+    // A stage is released (arrive on sEmpty) only after a block boundary that follows all of
+    // its DMMAs: at the top of the next k-tile iteration, or after the k-loop. Releasing at the
+    // end of the k-tile is not enough: ptxas schedules that arrive right after the stage's last
+    // LDS, before its data has returned (the DMMAs consuming it come later), and the producer's
+    // TMA refill can then overwrite the stage under the load — seen as one wrong k-tile in the
+    // last fragment of whichever warp arrives last. Issued DMMAs have read their operands.
+    int pending = -1;
+    for (long long it = it_begin; it < it_end;) {
+    const int tile = static_cast<int>(it / KTall);
+    const int seg_k0 = static_cast<int>(it % KTall);
+    const int seg_k1 = static_cast<int>(min(static_cast<long long>(KTall), seg_k0 + (it_end - it)));
+    it += seg_k1 - seg_k0;
+    const int m0 = (tile / tiles_n) * BM;
+    const int n0 = (tile % tiles_n) * BN;
     double acc[NACC][4][NT][2];
 #pragma unroll
     for (int a = 0; a < NACC; ++a)
@@ -805,9 +842,14 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
 #pragma unroll
             for (int j = 0; j < NT; ++j) acc[a][i][j][0] = acc[a][i][j][1] = 0.0;
 
-    for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % C::STAGES;
-        mbar_wait(sFull + 8 * s, (kt / C::STAGES) & 1);
+    for (int ktg = seg_k0; ktg < seg_k1; ++ktg, ++kc) {
+        if (pending >= 0) {  // the previous stage (its DMMAs are issued: its loads have returned)
+            __syncwarp();
+            if (lane == 0) mbar_arrive(sEmpty + 8 * pending);
+        }
+        const int s = kc % C::STAGES;
+        mbar_wait(sFull + 8 * s, (kc / C::STAGES) & 1);
+        pending = s;
         const uint32_t aRe = sBase + s * C::STAGE;
         const uint32_t aIm = aRe + BM * 128;
         const uint32_t aSm = aIm + BM * 128;
@@ -893,8 +935,11 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
                 }
             }
         }
+    }
+    if (pending >= 0) {  // the segment's last stage, before the epilogue
         __syncwarp();
-        if (lane == 0) mbar_arrive(sEmpty + 8 * s);
+        if (lane == 0) mbar_arrive(sEmpty + 8 * pending);
+        pending = -1;
     }
 
     // Output fragment (i, j) of this warp: combine the accumulators (3M: Cr = T1 - T2,
@@ -986,6 +1031,77 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
         return;
     }
 
+    if (sk.enabled && !(seg_k0 == 0 && seg_k1 == KTall)) {
+        // Stream-K tile shared with other CTAs: the CTA holding k-tiles [0, k1) owns it.
+        constexpr int CT = 32 * C::CONSUMER_WARPS;
+        constexpr int NV = NACC * 4 * NT * 2;
+        auto vidx = [](int a, int i, int j, int e) { return ((a * 4 + i) * NT + j) * 2 + e; };
+        // A split tile is its owner's LAST segment, so the owner CTA indexes the partial
+        // slots and the flag: the workspace is [P][maxc] slots, not one per tile.
+        const long long tile_first = static_cast<long long>(tile) * KTall;
+        const int owner = seg_k0 > 0 ? cta_of(tile_first) : static_cast<int>(blockIdx.x);
+        double* tile_ws = sk.ws + static_cast<size_t>(owner) * sk.maxc * NV * CT + tid;
+        int* flag = sk.flags + owner;
+        if (seg_k0 > 0) {
+            // contributor: publish the partial, then count it in
+            double* dst = tile_ws + static_cast<size_t>(static_cast<int>(blockIdx.x) - owner - 1) * NV * CT;
+#pragma unroll
+            for (int a = 0; a < NACC; ++a)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) __stcg(dst + vidx(a, i, j, e) * CT, acc[a][i][j][e]);
+            // release: every consumer fences its own stores, the CTA barrier orders them before
+            // thread 0's fence + flag increment, which the owner's threads acquire
+            __threadfence();
+            asm volatile("bar.sync 1, %0;" ::"n"(CT) : "memory");
+            if (tid == 0) {
+                __threadfence();
+                const int old = atomicAdd(flag, 1);
+                if (sk.dbg) {
+                    const int slot = static_cast<int>(blockIdx.x) - owner - 1;
+                    const int nc = cta_of(tile_first + KTall - 1) - owner;
+                    atomicAdd(sk.dbg + 3, 1);
+                    if (slot < 0 || slot >= sk.maxc) atomicAdd(sk.dbg + 1, 1);
+                    if (old >= nc) atomicAdd(sk.dbg + 5, 1);
+                }
+            }
+            continue;
+        }
+        // owner: wait for the contributors, add their partials in k order, store. Every
+        // consumer thread acquires the flag itself (no reliance on barrier cumulativity).
+        const int ncontrib = cta_of(tile_first + KTall - 1) - static_cast<int>(blockIdx.x);
+        {
+            int v = 0;
+            do {
+                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+            } while (v < ncontrib);
+            if (sk.dbg && tid == 0) {
+                atomicAdd(sk.dbg + 2, 1);
+                atomicAdd(sk.dbg + 4, ncontrib);
+                if (v != ncontrib) atomicAdd(sk.dbg + 0, 1);
+            }
+        }
+        __syncwarp();
+        for (int q = 0; q < ncontrib; ++q) {
+            const double* src = tile_ws + static_cast<size_t>(q) * NV * CT;
+#pragma unroll
+            for (int a = 0; a < NACC; ++a)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) acc[a][i][j][e] += __ldcg(src + vidx(a, i, j, e) * CT);
+        }
+        // the owner is this flag's only reader in this launch: re-arm it for the next
+        // GEMM (which starts after this grid completes: griddepcontrol.wait)
+        asm volatile("bar.sync 1, %0;" ::"n"(CT) : "memory");
+        if (tid == 0) *flag = 0;
+    }
+
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -998,6 +1114,7 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
             }
             store(i, j, f);
         }
+    }  // segments
 }
 
 template <bool THREE_M, bool SUMPLANE, bool REAL>
@@ -1027,7 +1144,8 @@ static int launch_ws_t(const GemmArgs& a, void* stream) {
     const CUtensorMap& tmB =
         MAT_B ? *static_cast<const CUtensorMap*>(REAL && a.tmap_b_real ? a.tmap_b_real : a.tmap_b) : tmA;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(a.N / C::BN, a.M / C::BM, splits);
+    cfg.gridDim = a.sk.enabled ? dim3(static_cast<unsigned>(ws_max_active_clusters(1)), 1, 1)
+                               : dim3(a.N / C::BN, a.M / C::BM, splits);
     cfg.blockDim = dim3(C::THREADS, 1, 1);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = static_cast<cudaStream_t>(stream);
@@ -1047,7 +1165,7 @@ static int launch_ws_t(const GemmArgs& a, void* stream) {
     cfg.attrs = attr;
     cfg.numAttrs = na;
     return static_cast<int>(cudaLaunchKernelEx(&cfg, zgemm_ws_kernel<THREE_M, SUMPLANE, MAT_B, REAL>, tmA, tmB,
-                                               *a.layer, a.out, a.M, a.N));
+                                               *a.layer, a.out, a.M, a.N, a.sk));
 }
 
 template <bool THREE_M, bool SUMPLANE>
@@ -1139,6 +1257,11 @@ int gemm_tile_rows(int tile) {
     }
 }
 int gemm_tile_planes(int tile) { return tile == kTileWs3MS ? 3 : 2; }
+
+int ws_partial_values(int tile) {
+    // accumulators per consumer thread: NACC x 4 x NT x 2 (4M: 2 x 4 x 4 x 2, 3M: 3 x 4 x 2 x 2)
+    return tile == kTileWs4M ? 64 : 48;
+}
 
 int gemm_tile_cols(int tile) {
     switch (tile) {

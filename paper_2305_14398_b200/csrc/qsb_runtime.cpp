@@ -294,6 +294,8 @@ struct qsb_plan {
     int N = 0;
     int tile = qsb::kTile32x32;
     int splits = 1;  // K2 split-K cluster size (warp-specialised tiles)
+    bool streamk = false;  // K2 stream-K schedule (warp-specialised tiles)
+    qsb::SkArgs sk;
     std::vector<char> mat;  // chain[i] (i >= 1) is materialised by K1t and streamed to K2 by TMA
     CUtensorMap tmap_b;     // the materialised operator ([planes][N][N], transposed)
     CUtensorMap tmap_b_real;  // its real plane alone (box of one plane) for real layers
@@ -428,6 +430,24 @@ int pick_splits(int64_t T, int KT) {
     return best;
 }
 
+// Stream-K instead of whole tiles whenever the tiles fill at least one wave: P
+// persistent CTAs (one per SM) share the T x KT k-tile iterations evenly, so the
+// last partial wave and the per-CTA prologue of every further wave disappear
+// (measured on B200, deferred-release K2: QFT-12 1024 -> 1000 ms, QFT-10 13.7 ->
+// 12.4 ms, Entangle-10 1.36 -> 1.22 ms, DJ-12 24.1 -> 23.7 ms). Below one wave
+// the cluster split-K grid stays. QSB_STREAMK=0 / 1 forces it off / on (tests).
+bool pick_streamk(int64_t T, int KT, int splits) {
+    (void)splits;
+    const char* force = std::getenv("QSB_STREAMK");
+    // every persistent CTA needs at least one k-tile (an empty share would leave its
+    // tile's owner waiting for a contribution that never comes)
+    if (T * KT < qsb::ws_max_active_clusters(1)) return false;
+    if (force && *force) return std::atoi(force) == 1 && KT >= 4;
+    const char* forced_split = std::getenv("QSB_SPLITK");
+    if (forced_split && *forced_split) return false;  // a forced cluster split stays a cluster split
+    return T >= qsb::ws_max_active_clusters(1) && KT >= 4;
+}
+
 int pick_tile(int M, int N, int gemm_mode, int* splits) {
     const int sms = 148;
     *splits = 1;
@@ -497,6 +517,11 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
         raise(QSB_ERR_ARGUMENT, "row shard [%lld, +%lld) is not contained in one aligned window of %lld rows",
               static_cast<long long>(row_begin), static_cast<long long>(row_count), static_cast<long long>(M));
     p->tile = p->small ? qsb::kTile32x32 : pick_tile(p->M, p->N, h->gemm_mode, &p->splits);
+    if (!p->small && p->tile >= qsb::kTileWs4M) {
+        const int64_t T = static_cast<int64_t>(p->M / qsb::gemm_tile_rows(p->tile)) * (p->N / qsb::gemm_tile_cols(p->tile));
+        p->streamk = pick_streamk(T, p->N / 16, p->splits);
+        if (p->streamk) p->splits = 1;
+    }
     if (p->tile == qsb::kTileWs3MS) {
         // the sum plane costs 50% more V memory: fall back to in-register sums if it does not fit
         size_t free_b = 0, total_b = 0;
@@ -581,6 +606,35 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
         const int rows = qsb::gemm_tile_rows(p->tile);
         p->tmap[0] = make_tmap(p->b.v[0].p, p->M, p->N, rows, p->planes);
         if (p->b.v[1].p) p->tmap[1] = make_tmap(p->b.v[1].p, p->M, p->N, rows, p->planes);
+        if (p->streamk) {
+            const int rows_t = qsb::gemm_tile_rows(p->tile), cols_t = qsb::gemm_tile_cols(p->tile);
+            const int T = (p->M / rows_t) * (p->N / cols_t);
+            const int KT = p->N / 16;
+            const int P = qsb::ws_max_active_clusters(1);
+            const long long I = static_cast<long long>(T) * KT;
+            const int per = static_cast<int>(std::max<long long>(1, I / P));
+            p->sk.enabled = 1;
+            p->sk.tiles_n = p->N / cols_t;
+            p->sk.tiles = T;
+            p->sk.maxc = (KT + per - 1) / per + 1;
+            const size_t vals = static_cast<size_t>(qsb::ws_partial_values(p->tile)) * 256;
+            // one split tile at most per CTA (its last segment): slots per owner CTA
+            p->b.skws.ensure(static_cast<size_t>(P) * p->sk.maxc * vals * sizeof(double));
+            p->b.skflags.ensure(static_cast<size_t>(P) * sizeof(int));
+            p->sk.ws = p->b.skws.as<double>();
+            p->sk.flags = p->b.skflags.as<int>();
+            if (std::getenv("QSB_SK_DEBUG")) {
+                static int* dbg = nullptr;
+                if (!dbg) {
+                    cuda_check(cudaMallocManaged(&dbg, 8 * sizeof(int)), "dbg");
+                    std::memset(dbg, 0, 8 * sizeof(int));
+                }
+                p->sk.dbg = dbg;
+            }
+            // on the plan stream (non-blocking: a legacy-stream memset would not order with it)
+            cuda_check(cudaMemsetAsync(p->sk.flags, 0, static_cast<size_t>(P) * sizeof(int), dc->stream),
+                       "stream-K flags");
+        }
         // real layers (Li = 0) as two real GEMMs on the 3M tiles (QSB_NO_REAL: tests keep 3M)
         p->real_ok = (p->tile == qsb::kTileWs3M || p->tile == qsb::kTileWs3MS) && !std::getenv("QSB_NO_REAL");
         if (p->real_ok) {
@@ -603,7 +657,7 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     in.gemm_flops = 8.0 * static_cast<double>(p->M) * static_cast<double>(N) * static_cast<double>(N) * gemms;
     in.expand_bytes = p->small ? 0.0 : 8.0 * p->planes * static_cast<double>(p->M) * static_cast<double>(N);
     in.gemm_tile = p->small ? -1 : p->tile;
-    in.gemm_splits = p->small ? 1 : p->splits;
+    in.gemm_splits = p->small ? 1 : (p->streamk ? -1 : p->splits);  // -1: stream-K schedule
     {
         const double mn2 = static_cast<double>(p->M) * static_cast<double>(N) * static_cast<double>(N);
         const bool three = p->tile == qsb::kTileWs3M || p->tile == qsb::kTileWs3MS;
@@ -658,6 +712,7 @@ void enqueue(qsb_plan* p, cudaStream_t s) {
         a.tmap_real = &p->tmap_real[cur];
         a.tmap_b_real = &p->tmap_b_real;
         a.splits = p->splits;
+        a.sk = p->sk;  // flags start at zero and every owner re-arms its own (no memset between GEMMs)
         cuda_check(qsb::launch_zgemm(a, p->tile, p->h->gemm_mode, s), "zgemm_gen_kernel");
         cur ^= 1;
     }
@@ -866,6 +921,11 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
         for (int g = 0; g < G; ++g) {
             DeviceScope ds(plans[g]->dc->device);
             cuda_check(cudaStreamSynchronize(plans[g]->dc->stream), "cudaStreamSynchronize");
+            if (int* d = plans[g]->sk.dbg) {
+                std::fprintf(stderr, "qsb stream-K: stale-exit %d bad-slot %d owners %d contributors %d "
+                             "expected %d over-count %d\n", d[0], d[1], d[2], d[3], d[4], d[5]);
+                std::memset(d, 0, 8 * sizeof(int));
+            }
             if (staged[g]) {
                 const qsb_plan* p = plans[g].get();
                 const int64_t off = p->row_begin - p->eff_begin;

@@ -337,7 +337,8 @@ def test_cluster_split_k(monkeypatch, sim, orc, splits, tile, name, n):
 
 def test_split_k_chosen_for_small_grids(sim):
     """Small grids take their parallelism from the K split (N = 512: 64 tiles x 2
-    ranks); large ones do not split; N <= 64 runs row-resident in one launch."""
+    ranks); grids of at least one wave run stream-K (gemm_splits -1); N <= 64 runs
+    row-resident in one launch."""
     import paper_2305_14398_b200 as q
     from paper_2305_14398_b200 import native
 
@@ -351,7 +352,7 @@ def test_split_k_chosen_for_small_grids(sim):
     plan.close()
     c, reg = q.make_named_circuit("qft", 12)
     plan = sim.plan(native.flatten(c, reg))
-    assert plan.info.gemm_splits == 1
+    assert plan.info.gemm_splits == -1
     plan.close()
 
 
@@ -596,3 +597,74 @@ def test_hbm_limit_plans_fall_back_to_two_planes(sim):
     c, reg = q.make_named_circuit("qft", 17)
     with pytest.raises(q.ResourceError, match="refuses 17 qubits"):
         sim.simulate_full_state(c, reg)
+
+
+@pytest.mark.parametrize("tile", ["3", "4", "5"])
+@pytest.mark.parametrize("name,n", [("entangle", 10), ("qft", 10), ("deutsch-jozsa", 11), ("qft", 11)])
+def test_stream_k_schedule(monkeypatch, sim, orc, tile, name, n):
+    """Stream-K (persistent CTAs sharing the tile x k-tile iterations; a split
+    tile's owner adds the published partials in k order): deterministic, within
+    1e-10 of the oracle and of the whole-tile schedule."""
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+
+    c, reg = q.make_named_circuit(name, n)
+    flat = native.flatten(c, reg)
+    monkeypatch.setenv("QSB_TILE", tile)
+    monkeypatch.setenv("QSB_STREAMK", "1")
+    plan = sim.plan(flat)
+    assert plan.info.gemm_splits == -1
+    plan.close()
+    a = sim.build_unitary(flat)
+    for _ in range(3):
+        b = sim.build_unitary(flat)
+        assert bit_equal(a[0], b[0]) and bit_equal(a[1], b[1])
+    monkeypatch.setenv("QSB_STREAMK", "0")
+    ref = sim.build_unitary(flat)
+    assert rel_frob(a[0], a[1], ref[0], ref[1]) <= TOL
+    for col in (0, (1 << n) - 1):
+        cr, ci = orc.unitary_column(flat, col)
+        assert rel_frob(a[0][:, col], a[1][:, col], cr, ci) <= TOL
+
+
+def test_stream_k_chosen_where_waves_quantise(sim):
+    """Grids of at least one wave run stream-K (Entangle-10: 256 tiles on 148 SMs,
+    QFT-12: 4096 tiles); QFT-9 (64 tiles) keeps the cluster split-K grid."""
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+
+    c, reg = q.make_named_circuit("entangle", 10)
+    plan = sim.plan(native.flatten(c, reg))
+    assert plan.info.gemm_splits == -1
+    plan.close()
+    c, reg = q.make_named_circuit("qft", 12)
+    plan = sim.plan(native.flatten(c, reg))
+    assert plan.info.gemm_splits == -1
+    plan.close()
+    c, reg = q.make_named_circuit("qft", 9)
+    plan = sim.plan(native.flatten(c, reg))
+    assert plan.info.gemm_splits == 2
+    plan.close()
+
+
+def test_stage_release_regression(monkeypatch, sim):
+    """H^n H^n = I through one materialised real GEMM under stream-K, repeated:
+    every run bit-identical and within 1e-12 of I. Before stages were released
+    after a block boundary, a consumer warp's last shared load could be
+    overwritten by the producer's TMA refill (one wrong k-tile, ~30 % of runs)."""
+    from paper_2305_14398_b200 import native
+    from paper_2305_14398_b200.circuit import Circuit, GateRegistry
+
+    n = 11
+    c = Circuit(n)
+    for _ in range(2):
+        for k in range(n):
+            c.h(k)
+    flat = native.flatten(c, GateRegistry())
+    monkeypatch.setenv("QSB_TILE", "5")
+    monkeypatch.setenv("QSB_STREAMK", "1")
+    first = sim.build_unitary(flat)
+    assert np.abs(first[0] - np.eye(1 << n)).max() < 1e-12 and np.abs(first[1]).max() < 1e-12
+    for _ in range(15):
+        u = sim.build_unitary(flat)
+        assert bit_equal(u[0], first[0]) and bit_equal(u[1], first[1])
