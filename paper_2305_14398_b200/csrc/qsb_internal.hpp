@@ -59,6 +59,19 @@ struct LayerDesc {
     BlockDesc blocks[kMaxBlocks];
 };
 
+// The one-launch small path (N <= 64, n <= 6) uploads and stages this compact
+// copy of each layer: the same fields, room for n blocks instead of kMaxBlocks.
+constexpr int kSmallMaxBlocks = 6;
+struct SmallLayerDesc {
+    uint32_t idmask;
+    int32_t nblocks;
+    int32_t real;
+    uint32_t zmask;
+    int32_t monomial;
+    int32_t pad;
+    BlockDesc blocks[kSmallMaxBlocks];
+};
+
 // Stream-K schedule of the warp-specialised K2: gridDim.x persistent CTAs share
 // the T x KT k-tile iterations evenly; a tile split between CTAs is finished by
 // the CTA holding its first k-tiles (the "owner"), which adds the partials the
@@ -98,7 +111,7 @@ int launch_zgemm(const GemmArgs& a, int tile, int gemm_mode, void* stream);
 // K1t: transposed operator planes for a materialised B (planes 2: re, im; 3: + re+im)
 int launch_expand_t(const LayerDesc& layer, int N, double* out, int planes, void* stream);
 int gemm_tile_b_planes(int tile);
-int launch_small_circuit(const LayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, int N,
+int launch_small_circuit(const SmallLayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, int N,
                          const double* x, double* v, double* psi, void* stream);
 int launch_matvec(const double* v, int M, int N, const double* x, double* psi, void* stream);
 int launch_probabilities(const double* psi, int64_t dim, double* p, double* partial, int partial_cap,

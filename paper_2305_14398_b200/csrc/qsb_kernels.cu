@@ -78,9 +78,12 @@ __device__ __forceinline__ void block_entry(const BlockDesc& b, uint32_t r, uint
 }
 
 // Entry (r, c) of the layer operator.
-__device__ __forceinline__ void layer_entry(const LayerDesc& d, uint32_t r, uint32_t c, double& vr,
+template <class Desc>  // LayerDesc, or the small path's SmallLayerDesc
+__device__ __forceinline__ void layer_entry(const Desc& d, uint32_t r, uint32_t c, double& vr,
                                             double& vi) {
-    if ((r ^ c) & d.idmask) {
+    // zmask = identity bits + controlled blocks' non-target bits: the entry is an exact
+    // zero unless r and c agree there (the fold would give a signed zero; == ignores the sign)
+    if ((r ^ c) & d.zmask) {
         vr = 0.0;
         vi = 0.0;
         return;
@@ -1320,7 +1323,7 @@ size_t small_circuit_smem_bytes(int M, int N) {
 // constants and fully unrolled inner loops. x == nullptr means psi0 = |0...0>:
 // psi = V[:, 0] (the reference's matvec with e_0 adds only exact zeros to V[i][0]).
 template <int N>
-__global__ void __launch_bounds__(1024) small_circuit_kernel(const LayerDesc* __restrict__ layers, int nlayers,
+__global__ void __launch_bounds__(1024) small_circuit_kernel(const SmallLayerDesc* __restrict__ layers, int nlayers,
                                                             uint32_t row_begin, int M,
                                                             const double* __restrict__ x,
                                                             double* __restrict__ v_out,
@@ -1330,9 +1333,9 @@ __global__ void __launch_bounds__(1024) small_circuit_kernel(const LayerDesc* __
     extern __shared__ double sm[];
     // Layer descriptors are staged in shared memory one ahead (cp.async), so the
     // generator's field reads never chase pointers through global memory.
-    __shared__ __align__(16) LayerDesc desc[2];
-    constexpr int DESC_WORDS = static_cast<int>(sizeof(LayerDesc) / 8);
-    static_assert(sizeof(LayerDesc) % 8 == 0, "LayerDesc is copied in 8-byte words");
+    __shared__ __align__(16) SmallLayerDesc desc[2];
+    constexpr int DESC_WORDS = static_cast<int>(sizeof(SmallLayerDesc) / 8);
+    static_assert(sizeof(SmallLayerDesc) % 8 == 0, "SmallLayerDesc is copied in 8-byte words");
     const int R = M / gridDim.x;
     const int cta_row = blockIdx.x * R;
     row_begin += static_cast<uint32_t>(cta_row);
@@ -1365,7 +1368,7 @@ __global__ void __launch_bounds__(1024) small_circuit_kernel(const LayerDesc* __
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();  // desc[l & 1] has landed; every thread is done with desc[(l - 1) & 1]
         if (l + 1 < nlayers) fetch(l + 1, (l + 1) & 1);
-        const LayerDesc& d = desc[l & 1];
+        const SmallLayerDesc& d = desc[l & 1];
         const double* vr = sm + (2 * cur) * MN;
         const double* vi = vr + MN;
         double* tr = sm + (2 * (cur ^ 1)) * MN;
@@ -1429,11 +1432,143 @@ __global__ void __launch_bounds__(1024) small_circuit_kernel(const LayerDesc* __
     }
 }
 
+// 8 <= N <= 64: the whole chain on the FP64 tensor cores, 8 rows of V per CTA.
+// The operators of a batch of layers are generated together into shared memory
+// (every entry independent: one generation latency per batch, not per layer),
+// transposed, LT[n][k]; then each layer is V <- V L with DMMA m8n8k4 (4M):
+// warp w owns output columns [8w, 8w + 8) and walks k in steps of 4 on two
+// accumulator sets (even / odd steps). Row stride S = N + 4 doubles makes every
+// fragment load two wavefronts (the minimum for 32 doubles). Operator entries are
+// the bit-exact layer_entry values; only the summation order of products differs
+// from the reference's k-sequential loop (within the 1e-10 contract).
+constexpr size_t kSmallSmemMax = 227 * 1024;
+
 template <int N>
-static int launch_small_t(const LayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, const double* x, double* v,
+__host__ __device__ constexpr int small_stride() { return N + 4; }
+
+template <int N>
+__host__ __device__ constexpr size_t small_v_bytes() {
+    return sizeof(double) * 4 * 8 * static_cast<size_t>(small_stride<N>());  // V, V' (re, im), 8 rows
+}
+
+template <int N>
+__host__ __device__ constexpr size_t small_op_bytes() {
+    // LT re, im + the layer's descriptor (generation reads it from shared memory)
+    return sizeof(double) * 2 * N * static_cast<size_t>(small_stride<N>()) + sizeof(SmallLayerDesc);
+}
+
+template <int N>
+__global__ void __launch_bounds__(1024) small_dmma_kernel(const SmallLayerDesc* __restrict__ layers, int nlayers,
+                                                        int batch, uint32_t row_begin, int M,
+                                                        const double* __restrict__ x,
+                                                        double* __restrict__ v_out, double* __restrict__ psi) {
+    static_assert(N >= 8 && N <= 64, "DMMA small path: 8 <= N <= 64");
+    extern __shared__ __align__(16) double sm[];
+    constexpr int S = small_stride<N>();
+    constexpr int VP = 8 * S;          // one plane of V
+    constexpr int OP = N * S;          // one plane of an operator
+    const int cta_row = blockIdx.x * 8;
+    row_begin += static_cast<uint32_t>(cta_row);
+    const int out_plane = M * N;
+    v_out += static_cast<size_t>(cta_row) * N;
+    psi += cta_row;
+    double* ops = sm + 4 * VP;        // [batch][re | im][N][S]
+    SmallLayerDesc* descs = reinterpret_cast<SmallLayerDesc*>(ops + static_cast<size_t>(batch) * 2 * OP);  // [batch]
+    static_assert(sizeof(SmallLayerDesc) % 8 == 0, "descriptors are staged in 8-byte words");
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, t = lane & 3;
+    for (int e = tid; e < 8 * N; e += blockDim.x) {
+        const int i = e / N, j = e % N;
+        layer_entry(layers[0], row_begin + i, j, sm[i * S + j], sm[VP + i * S + j]);
+    }
+    int cur = 0;
+    for (int l0 = 1; l0 < nlayers; l0 += batch) {
+        const int nb = min(batch, nlayers - l0);
+        __syncthreads();  // the previous batch's operators are consumed (and V0 is written)
+        {
+            constexpr int W = static_cast<int>(sizeof(SmallLayerDesc) / 8);
+            const unsigned long long* src = reinterpret_cast<const unsigned long long*>(layers + l0);
+            unsigned long long* dst = reinterpret_cast<unsigned long long*>(descs);
+            for (int w = tid; w < nb * W; w += blockDim.x) dst[w] = __ldg(src + w);
+        }
+        __syncthreads();
+        for (int e = tid; e < nb * N * N; e += blockDim.x) {
+            const int b = e / (N * N), kn = e % (N * N);
+            const int k = kn / N, n = kn % N;
+            double* o = ops + static_cast<size_t>(b) * 2 * OP + n * S + k;
+            layer_entry(descs[b], static_cast<uint32_t>(k), static_cast<uint32_t>(n), o[0], o[OP]);
+        }
+        __syncthreads();
+        for (int b = 0; b < nb; ++b) {
+            if (warp < N / 8) {
+                const double* ltr = ops + static_cast<size_t>(b) * 2 * OP + (8 * warp + g) * S + t;
+                const double* lti = ltr + OP;
+                const double* vr = sm + (2 * cur) * VP + g * S + t;
+                const double* vi = vr + VP;
+                double cr0[2] = {0.0, 0.0}, ci0[2] = {0.0, 0.0}, cr1[2] = {0.0, 0.0}, ci1[2] = {0.0, 0.0};
+#pragma unroll
+                for (int ks = 0; ks < N / 4; ++ks) {
+                    const double ar = vr[4 * ks], ai = vi[4 * ks];
+                    const double br = ltr[4 * ks], bi = lti[4 * ks];
+                    if (ks & 1) {
+                        dmma(cr1, ar, br);
+                        dmma(cr1, ai, neg(bi));
+                        dmma(ci1, ar, bi);
+                        dmma(ci1, ai, br);
+                    } else {
+                        dmma(cr0, ar, br);
+                        dmma(cr0, ai, neg(bi));
+                        dmma(ci0, ar, bi);
+                        dmma(ci0, ai, br);
+                    }
+                }
+                double* tr = sm + (2 * (cur ^ 1)) * VP + g * S + 8 * warp + 2 * t;
+                *reinterpret_cast<double2*>(tr) = make_double2(cr0[0] + cr1[0], cr0[1] + cr1[1]);
+                *reinterpret_cast<double2*>(tr + VP) = make_double2(ci0[0] + ci1[0], ci0[1] + ci1[1]);
+            }
+            cur ^= 1;
+            __syncthreads();
+        }
+    }
+    __syncthreads();
+    const double* vr = sm + (2 * cur) * VP;
+    const double* vi = vr + VP;
+    for (int e = tid; e < 8 * N; e += blockDim.x) {
+        const int i = e / N, j = e % N;
+        v_out[e] = vr[i * S + j];
+        v_out[out_plane + e] = vi[i * S + j];
+    }
+    for (int i = tid; i < 8; i += blockDim.x) {
+        if (x == nullptr) {
+            psi[i] = vr[i * S];
+            psi[M + i] = vi[i * S];
+            continue;
+        }
+        double sr = 0.0, si = 0.0;
+        for (int k = 0; k < N; ++k) {
+            const double a_r = vr[i * S + k], a_i = vi[i * S + k];
+            sr += a_r * x[k] - a_i * x[N + k];
+            si += a_r * x[N + k] + a_i * x[k];
+        }
+        psi[i] = sr;
+        psi[M + i] = si;
+    }
+}
+
+template <int N>
+static int launch_small_t(const SmallLayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, const double* x, double* v,
                           double* psi, cudaStream_t st) {
     // rows per CTA: 8 from N = 32 (several SMs), all of them below
     const int R = (N >= 32 && M % 8 == 0) ? 8 : M;
+    if (N >= 8 && N <= 64 && M % 8 == 0 && !std::getenv("QSB_SMALL_FMA")) {
+        constexpr int NT = (N >= 8 && N <= 64) ? N : 8;
+        int batch = static_cast<int>((kSmallSmemMax - small_v_bytes<NT>()) / small_op_bytes<NT>());
+        batch = std::max(1, std::min(batch, std::max(1, nlayers - 1)));
+        const size_t smem = small_v_bytes<NT>() + static_cast<size_t>(batch) * small_op_bytes<NT>();
+        small_dmma_kernel<NT><<<M / 8, 1024, smem, st>>>(d_layers, nlayers, batch, row_begin, M, x, v, psi);
+        return static_cast<int>(cudaGetLastError());
+    }
     const size_t smem = small_circuit_smem_bytes(R, N);
     int threads = R * N;
     if (threads > 1024) threads = 1024;
@@ -1442,7 +1577,7 @@ static int launch_small_t(const LayerDesc* d_layers, int nlayers, uint32_t row_b
     return static_cast<int>(cudaGetLastError());
 }
 
-int launch_small_circuit(const LayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, int N,
+int launch_small_circuit(const SmallLayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, int N,
                          const double* x, double* v, double* psi, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (N) {
@@ -1452,8 +1587,6 @@ int launch_small_circuit(const LayerDesc* d_layers, int nlayers, uint32_t row_be
     case 16: return launch_small_t<16>(d_layers, nlayers, row_begin, M, x, v, psi, st);
     case 32: return launch_small_t<32>(d_layers, nlayers, row_begin, M, x, v, psi, st);
     case 64: return launch_small_t<64>(d_layers, nlayers, row_begin, M, x, v, psi, st);
-    case 128: return launch_small_t<128>(d_layers, nlayers, row_begin, M, x, v, psi, st);
-    case 256: return launch_small_t<256>(d_layers, nlayers, row_begin, M, x, v, psi, st);
     default: return static_cast<int>(cudaErrorInvalidValue);
     }
 }
@@ -1553,6 +1686,12 @@ int launch_probabilities(const double* psi, int64_t dim, double* p, double* part
     return static_cast<int>(cudaGetLastError());
 }
 
+template <int N>
+static int configure_small_t() {
+    return static_cast<int>(cudaFuncSetAttribute(small_dmma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(kSmallSmemMax)));
+}
+
 // Kernel attributes, set once per device before any launch or graph capture.
 int configure_kernels() {
     int e;
@@ -1563,6 +1702,9 @@ int configure_kernels() {
     if ((e = configure_ws_t<true, false>())) return e;
     if ((e = configure_ws_t<true, true>())) return e;
     query_ws_clusters();
+    if ((e = configure_small_t<8>()) || (e = configure_small_t<16>()) || (e = configure_small_t<32>()) ||
+        (e = configure_small_t<64>()))
+        return e;
     if ((e = static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel<32>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024))))
         return e;
@@ -1570,13 +1712,7 @@ int configure_kernels() {
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    static_cast<int>(small_circuit_smem_bytes(8, 64))))))
         return e;
-    if ((e = static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel<128>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   static_cast<int>(small_circuit_smem_bytes(8, 128))))))
-        return e;
-    return static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel<256>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(small_circuit_smem_bytes(8, 256))));
+    return 0;
 }
 
 }  // namespace qsb

@@ -307,6 +307,8 @@ struct qsb_plan {
     bool borrowed = false;
     CUtensorMap tmap[2];
     int final_buf = 0;
+    const void* small_layers_dev = nullptr;  // one-shot small plans: descriptors read in place from pinned staging
+    double* psi_dev_out = nullptr;            // ... and psi written straight into pinned staging
     bool x_is_e0 = true;  // psi0 = |0...0>: the one-CTA path reads psi as column 0
     cudaGraphExec_t graph = nullptr;
     bool timing = false;
@@ -478,12 +480,16 @@ int pick_tile(int M, int N, int gemm_mode, int* splits) {
 // Build a plan; the caller holds the handle mutex when borrow_cache is set.
 std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circuit* c, int64_t row_begin,
                                     int64_t row_count, bool borrow_cache) {
+    static const bool trace = std::getenv("QSB_TRACE") != nullptr;
+    auto tnow = [] { return std::chrono::steady_clock::now(); };
+    const auto t0 = tnow();
     validate_circuit_shape(c);
     check_guard(c, h->guard);
     auto p = std::make_unique<qsb_plan>();
     p->h = h;
     p->dc = dc;
     p->cc = compile(c);
+    const auto t1 = tnow();
     const int n = c->n_qubits;
     const int64_t N = int64_t{1} << n;
     if (row_count < 0 || row_begin < 0 || row_begin + row_count > N)
@@ -542,7 +548,9 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     if (!p->small && p->chain.size() > 1) p->b.v[1].ensure(p->planes * plane_bytes);
     p->b.psi.ensure(2 * static_cast<size_t>(M) * 8);
     p->b.x.ensure(2 * static_cast<size_t>(N) * 8);
+    const auto t2 = tnow();
     upload_tables(p.get(), c);
+    const auto t3 = tnow();
     // re-derive the chain with patched table pointers
     p->chain.clear();
     for (auto it = p->cc.app.rbegin(); it != p->cc.app.rend(); ++it)
@@ -597,11 +605,37 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
                    "init psi0");
     p->x_is_e0 = true;
     if (p->small) {
-        const size_t bytes = sizeof(qsb::LayerDesc) * p->chain.size();
+        // compact descriptors (n <= 6 blocks each) written straight into pinned staging
+        static_assert(qsb::kSmallMaxBlocks >= 6, "the small path covers n <= 6");
+        const size_t bytes = sizeof(qsb::SmallLayerDesc) * p->chain.size();
         p->b.layers.ensure(bytes);
-        void* st = dc->stage(bytes);
-        std::memcpy(st, p->chain.data(), bytes);
-        cuda_check(cudaMemcpyAsync(p->b.layers.p, st, bytes, cudaMemcpyHostToDevice, dc->stream), "upload layers");
+        auto* st = static_cast<qsb::SmallLayerDesc*>(dc->stage(bytes));
+        for (size_t i = 0; i < p->chain.size(); ++i) {
+            const qsb::LayerDesc& d = p->chain[i];
+            qsb::SmallLayerDesc& o = st[i];
+            o.idmask = d.idmask;
+            o.nblocks = d.nblocks;
+            o.real = d.real;
+            o.zmask = d.zmask;
+            o.monomial = d.monomial;
+            o.pad = 0;
+            std::memcpy(o.blocks, d.blocks, sizeof(qsb::BlockDesc) * static_cast<size_t>(d.nblocks));
+        }
+        // A one-shot call (run_full) lets the kernel read the pinned staging in place
+        // (mapped host memory): no copy call. Plans that outlive the call upload.
+        void* mapped = nullptr;
+        if (borrow_cache && cudaHostGetDevicePointer(&mapped, st, 0) == cudaSuccess) {
+            p->small_layers_dev = mapped;
+        } else {
+            cudaGetLastError();
+            cuda_check(cudaMemcpyAsync(p->b.layers.p, st, bytes, cudaMemcpyHostToDevice, dc->stream), "upload layers");
+        }
+        if (trace) {
+            const auto t4 = tnow();
+            auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+            std::fprintf(stderr, "qsb plan: compile %.1f us, buffers %.1f us, tables %.1f us, layers %.1f us\n",
+                         us(t0, t1), us(t1, t2), us(t2, t3), us(t3, t4));
+        }
     } else {
         const int rows = qsb::gemm_tile_rows(p->tile);
         p->tmap[0] = make_tmap(p->b.v[0].p, p->M, p->N, rows, p->planes);
@@ -687,9 +721,12 @@ void release_plan(std::unique_ptr<qsb_plan>& p) {
 void enqueue(qsb_plan* p, cudaStream_t s) {
     const uint32_t rb = static_cast<uint32_t>(p->eff_begin);
     if (p->small) {
-        cuda_check(qsb::launch_small_circuit(p->b.layers.as<qsb::LayerDesc>(), static_cast<int>(p->chain.size()), rb,
+        const auto* layers = p->small_layers_dev ? static_cast<const qsb::SmallLayerDesc*>(p->small_layers_dev)
+                                                 : p->b.layers.as<qsb::SmallLayerDesc>();
+        cuda_check(qsb::launch_small_circuit(layers, static_cast<int>(p->chain.size()), rb,
                                              p->M, p->N, p->x_is_e0 ? nullptr : p->b.x.as<double>(),
-                                             p->b.v[0].as<double>(), p->b.psi.as<double>(), s),
+                                             p->b.v[0].as<double>(),
+                                             p->psi_dev_out ? p->psi_dev_out : p->b.psi.as<double>(), s),
                    "small_circuit_kernel");
         p->final_buf = 0;
         return;
@@ -895,9 +932,21 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
                 cuda_check(cudaMemcpyAsync(p->b.x.as<double>() + N, psi0_im, N * 8, cudaMemcpyHostToDevice, s),
                            "upload psi0");
             }
+            double* mapped_psi = nullptr;
+            if (psi_re && p->small) {
+                // the one-CTA kernel writes psi straight into pinned staging (mapped): no copy call
+                staged[g] = static_cast<double*>(p->dc->stage_out(2 * static_cast<size_t>(p->M) * 8));
+                void* d = nullptr;
+                if (cudaHostGetDevicePointer(&d, staged[g], 0) == cudaSuccess)
+                    mapped_psi = p->psi_dev_out = static_cast<double*>(d);
+                else
+                    cudaGetLastError();
+            }
             execute(p, s, false);
             const int64_t off = p->row_begin - p->eff_begin;
-            if (psi_re && p->M <= 65536) {
+            if (mapped_psi) {
+                // written by the kernel; read after the stream synchronisation below
+            } else if (psi_re && p->M <= 65536) {
                 // one copy of both psi planes into pinned staging; scattered on the host after the sync
                 staged[g] = static_cast<double*>(p->dc->stage_out(2 * static_cast<size_t>(p->M) * 8));
                 cuda_check(cudaMemcpyAsync(staged[g], p->b.psi.p, 2 * static_cast<size_t>(p->M) * 8,
