@@ -1493,11 +1493,38 @@ __global__ void __launch_bounds__(1024) small_dmma_kernel(const SmallLayerDesc* 
             for (int w = tid; w < nb * W; w += blockDim.x) dst[w] = __ldg(src + w);
         }
         __syncthreads();
-        for (int e = tid; e < nb * N * N; e += blockDim.x) {
-            const int b = e / (N * N), kn = e % (N * N);
-            const int k = kn / N, n = kn % N;
-            double* o = ops + static_cast<size_t>(b) * 2 * OP + n * S + k;
-            layer_entry(descs[b], static_cast<uint32_t>(k), static_cast<uint32_t>(n), o[0], o[OP]);
+        // Zero the batch's operator planes, then evaluate only the candidate entries:
+        // (k, c) can be nonzero only where k and c agree on the layer's zmask, i.e.
+        // c = (k & zmask) | (any combination of the free bits) — N 2^f of N^2 entries
+        // (f = 1 for a gate or a controlled gate). A group of threads per layer.
+        {
+            double2* z = reinterpret_cast<double2*>(ops);
+            const int nz = nb * OP;  // double2 words of nb x 2 planes
+            for (int w = tid; w < nz; w += blockDim.x) z[w] = make_double2(0.0, 0.0);
+        }
+        __syncthreads();
+        {
+            const int gsz = static_cast<int>(blockDim.x) / nb;
+            const int grp = tid / gsz, gl = tid - grp * gsz;
+            if (grp < nb) {
+                const SmallLayerDesc& d = descs[grp];
+                const uint32_t fmask = ~d.zmask & static_cast<uint32_t>(N - 1);
+                const int f = __popc(fmask);
+                double* o = ops + static_cast<size_t>(grp) * 2 * OP;
+                for (int idx = gl; idx < (N << f); idx += gsz) {
+                    const uint32_t k = static_cast<uint32_t>(idx) >> f;
+                    uint32_t sub = static_cast<uint32_t>(idx) & ((1u << f) - 1u);
+                    uint32_t c = k & ~fmask, fb = fmask;
+                    while (fb) {  // deposit sub's bits at fmask's positions
+                        const uint32_t lb = fb & (0u - fb);
+                        if (sub & 1u) c |= lb;
+                        sub >>= 1;
+                        fb ^= lb;
+                    }
+                    double* e = o + c * S + k;
+                    layer_entry(d, k, c, e[0], e[OP]);
+                }
+            }
         }
         __syncthreads();
         for (int b = 0; b < nb; ++b) {
