@@ -81,6 +81,7 @@ struct SkArgs {
     int tiles_n = 0;        // output tiles along N
     int tiles = 0;          // T
     int maxc = 0;           // partial slots per tile
+    int dp_waves = 0;       // whole-tile data-parallel waves before the stream-K range
     double* ws = nullptr;   // [P owner CTAs][maxc][values][256 consumer threads]
     int* flags = nullptr;   // [P owner CTAs], zero between launches (each owner re-arms its own)
     int* dbg = nullptr;     // QSB_SK_DEBUG: protocol anomaly counters

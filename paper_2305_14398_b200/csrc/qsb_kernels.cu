@@ -643,15 +643,35 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
     const int KTall = N / C::BK;
     const int kt0 = (KTall * rank) / splits;
     const int KT = (KTall * (rank + 1)) / splits - kt0;
-    // Work as segments of the flattened (tile, k-tile) iteration space: classic
-    // grids own one segment (their tile, their split-K range); stream-K CTAs own
-    // [I c / P, I (c + 1) / P) of the I = T KTall iterations.
+    // Work as segments: classic grids own one segment (their tile, their split-K
+    // range). Stream-K grids (P = gridDim.x persistent CTAs) first run sk.dp_waves
+    // data-parallel waves — CTA c takes whole tile w P + c in wave w, so the CTAs
+    // running together share A row blocks in L2 — then own [I c / P, I (c + 1) / P)
+    // of the I = (T - W P) KTall iterations of the remaining tiles (stream-K).
     const int tiles_n = N / BN;
-    const long long I = static_cast<long long>(sk.tiles) * KTall;
+    const int W = sk.enabled ? sk.dp_waves : 0;
+    const int tile_base = W * static_cast<int>(gridDim.x);
+    const long long I = static_cast<long long>(sk.tiles - tile_base) * KTall;
     const long long it_begin =
         sk.enabled ? I * blockIdx.x / gridDim.x
                    : static_cast<long long>(blockIdx.y * tiles_n + blockIdx.x) * KTall + kt0;
     const long long it_end = sk.enabled ? I * (blockIdx.x + 1) / gridDim.x : it_begin + KT;
+    // Next segment of this CTA: data-parallel waves, then the (stream-K) range.
+    auto next_segment = [&](int& seg, long long& it, int& tile, int& k0, int& k1) -> bool {
+        if (seg < W) {
+            tile = seg * static_cast<int>(gridDim.x) + static_cast<int>(blockIdx.x);
+            k0 = 0;
+            k1 = KTall;
+            ++seg;
+            return true;
+        }
+        if (it >= it_end) return false;
+        tile = tile_base + static_cast<int>(it / KTall);
+        k0 = static_cast<int>(it % KTall);
+        k1 = static_cast<int>(min(static_cast<long long>(KTall), k0 + (it_end - it)));
+        it += k1 - k0;
+        return true;
+    };
     // CTA whose stream-K share holds iteration x
     auto cta_of = [&](long long x) {
         long long c = x * gridDim.x / I;
@@ -681,11 +701,9 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::PRODUCER_REGS));
         const int ptid = tid - 32 * C::CONSUMER_WARPS;
         int kc = 0;  // stage counter across segments
-        for (long long it = it_begin; it < it_end;) {
-        const int tile = static_cast<int>(it / KTall);
-        const int seg_k0 = static_cast<int>(it % KTall);
-        const int seg_k1 = static_cast<int>(min(static_cast<long long>(KTall), seg_k0 + (it_end - it)));
-        it += seg_k1 - seg_k0;
+        int seg = 0, tile, seg_k0, seg_k1;
+        long long it = it_begin;
+        while (next_segment(seg, it, tile, seg_k0, seg_k1)) {
         const int m0 = (tile / tiles_n) * BM;
         const int n0 = (tile % tiles_n) * BN;
         for (int ktg = seg_k0; ktg < seg_k1; ++ktg, ++kc) {
@@ -830,11 +848,9 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
     // TMA refill can then overwrite the stage under the load — seen as one wrong k-tile in the
     // last fragment of whichever warp arrives last. Issued DMMAs have read their operands.
     int pending = -1;
-    for (long long it = it_begin; it < it_end;) {
-    const int tile = static_cast<int>(it / KTall);
-    const int seg_k0 = static_cast<int>(it % KTall);
-    const int seg_k1 = static_cast<int>(min(static_cast<long long>(KTall), seg_k0 + (it_end - it)));
-    it += seg_k1 - seg_k0;
+    int seg = 0, tile, seg_k0, seg_k1;
+    long long it = it_begin;
+    while (next_segment(seg, it, tile, seg_k0, seg_k1)) {
     const int m0 = (tile / tiles_n) * BM;
     const int n0 = (tile % tiles_n) * BN;
     double acc[NACC][4][NT][2];
@@ -1041,7 +1057,7 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
         auto vidx = [](int a, int i, int j, int e) { return ((a * 4 + i) * NT + j) * 2 + e; };
         // A split tile is its owner's LAST segment, so the owner CTA indexes the partial
         // slots and the flag: the workspace is [P][maxc] slots, not one per tile.
-        const long long tile_first = static_cast<long long>(tile) * KTall;
+        const long long tile_first = static_cast<long long>(tile - tile_base) * KTall;  // stream-K space
         const int owner = seg_k0 > 0 ? cta_of(tile_first) : static_cast<int>(blockIdx.x);
         double* tile_ws = sk.ws + static_cast<size_t>(owner) * sk.maxc * NV * CT + tid;
         int* flag = sk.flags + owner;

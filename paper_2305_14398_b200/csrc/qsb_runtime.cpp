@@ -645,12 +645,22 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
             const int T = (p->M / rows_t) * (p->N / cols_t);
             const int KT = p->N / 16;
             const int P = qsb::ws_max_active_clusters(1);
-            const long long I = static_cast<long long>(T) * KT;
+            // QSB_SK_DP=1: data-parallel waves first, the last one to two waves' worth of
+            // tiles stream-K. The CTAs of a wave share A row blocks in L2, so DRAM traffic
+            // drops to the algorithmic 0.78 GB per QFT-12 launch (from 25.8 GB: each CTA's
+            // contiguous tile range re-reads its row block) — yet the circuit runs 2 %
+            // slower (1025 vs 1004 ms, r73): the K2 stays FP64-tensor bound either way, so
+            // all-stream-K is the default.
+            int W = 0;
+            if (const char* e = std::getenv("QSB_SK_DP"))
+                if (*e && std::atoi(e) == 1) W = T % P == 0 ? T / P : std::max(0, T / P - 1);
+            const long long I = static_cast<long long>(T - W * P) * KT;
             const int per = static_cast<int>(std::max<long long>(1, I / P));
+            p->sk.dp_waves = W;
             p->sk.enabled = 1;
             p->sk.tiles_n = p->N / cols_t;
             p->sk.tiles = T;
-            p->sk.maxc = (KT + per - 1) / per + 1;
+            p->sk.maxc = I > 0 ? (KT + per - 1) / per + 1 : 1;
             const size_t vals = static_cast<size_t>(qsb::ws_partial_values(p->tile)) * 256;
             // one split tile at most per CTA (its last segment): slots per owner CTA
             p->b.skws.ensure(static_cast<size_t>(P) * p->sk.maxc * vals * sizeof(double));
