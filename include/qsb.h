@@ -122,8 +122,14 @@ typedef struct qsb_options {
 
 enum {
     QSB_FLAG_NO_GRAPH = 1,        /* do not capture plan execution in a CUDA graph */
-    QSB_FLAG_MATERIALIZE = 2      /* materialise each layer operator with K1 and run the
+    QSB_FLAG_MATERIALIZE = 2,     /* materialise each layer operator with K1 and run the
                                      GEMM on it instead of generating tiles in shared memory */
+    QSB_FLAG_COLUMN_BLOCKS = 4    /* shard U by column blocks instead of row blocks:
+                                     U[:, cols] <- S_k U[:, cols] in application order, the
+                                     reference's association; a plan's "rows" are then the columns
+                                     [row_begin, row_begin + row_count) of U, its unitary buffer
+                                     holds U[:, cols]^T and its state buffer the full-length share
+                                     U[:, cols] psi0[cols] (2^n entries per plane) */
 };
 
 typedef struct qsb_handle qsb_handle;

@@ -112,8 +112,15 @@ int launch_zgemm(const GemmArgs& a, int tile, int gemm_mode, void* stream);
 // K1t: transposed operator planes for a materialised B (planes 2: re, im; 3: + re+im)
 int launch_expand_t(const LayerDesc& layer, int N, double* out, int planes, void* stream);
 int gemm_tile_b_planes(int tile);
-int launch_small_circuit(const SmallLayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, int N,
-                         const double* x, double* v, double* psi, void* stream);
+// transpose = 1: column blocks (operands L^T, V = U[:, cols]^T)
+int launch_small_circuit(const SmallLayerDesc* d_layers, int nlayers, int transpose, uint32_t row_begin, int M,
+                         int N, const double* x, double* v, double* psi, void* stream);
+// rows [col_begin, col_begin + M) of L^T (the first layer of a column block)
+int launch_expand_cols(const LayerDesc& layer, uint32_t col_begin, int M, int N, double* out, int planes,
+                       void* stream);
+// psi[k] = sum_{i in [i0, i0 + count)} V[i][k] x[col0 + i - i0] (column blocks; psi has N entries)
+int launch_matvec_t(const double* v, int M, int N, int i0, int count, int col0, const double* x, double* psi,
+                    void* stream);
 int launch_matvec(const double* v, int M, int N, const double* x, double* psi, void* stream);
 int launch_probabilities(const double* psi, int64_t dim, double* p, double* partial, int partial_cap,
                          double* norm, void* stream);

@@ -314,6 +314,9 @@ __device__ __forceinline__ void gen_batch(const LayerDesc& d, const TilePrefix& 
 // K1: expansion
 // ----------------------------------------------------------------------------
 
+// TRANSPOSE: rows [row_begin, row_begin + M) of L^T, i.e. out[i][j] = L(j, row_begin + i)
+// (column blocks: V starts as the first layer's columns).
+template <bool TRANSPOSE>
 __global__ void __launch_bounds__(256) expand_kernel(const __grid_constant__ LayerDesc d,
                                                      uint32_t row_begin, int M, int N,
                                                      double* __restrict__ out, int planes) {
@@ -325,8 +328,13 @@ __global__ void __launch_bounds__(256) expand_kernel(const __grid_constant__ Lay
         const uint32_t row = static_cast<uint32_t>(p / half_n);
         const uint32_t col = static_cast<uint32_t>(p % half_n) * 2;
         double r0, i0, r1, i1;
-        layer_entry(d, row_begin + row, col, r0, i0);
-        layer_entry(d, row_begin + row, col + 1, r1, i1);
+        if (TRANSPOSE) {
+            layer_entry(d, col, row_begin + row, r0, i0);
+            layer_entry(d, col + 1, row_begin + row, r1, i1);
+        } else {
+            layer_entry(d, row_begin + row, col, r0, i0);
+            layer_entry(d, row_begin + row, col + 1, r1, i1);
+        }
         reinterpret_cast<double2*>(out)[p] = make_double2(r0, r1);
         reinterpret_cast<double2*>(out + plane)[p] = make_double2(i0, i1);
         if (planes == 3)
@@ -340,7 +348,17 @@ int launch_expand(const LayerDesc& layer, uint32_t row_begin, int M, int N, doub
     int blocks = static_cast<int>((pairs + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
-    expand_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(layer, row_begin, M, N, out, planes);
+    expand_kernel<false><<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(layer, row_begin, M, N, out, planes);
+    return static_cast<int>(cudaGetLastError());
+}
+
+int launch_expand_cols(const LayerDesc& layer, uint32_t col_begin, int M, int N, double* out, int planes,
+                       void* stream) {
+    const size_t pairs = static_cast<size_t>(M) * N / 2;
+    int blocks = static_cast<int>((pairs + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks < 1) blocks = 1;
+    expand_kernel<true><<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(layer, col_begin, M, N, out, planes);
     return static_cast<int>(cudaGetLastError());
 }
 
@@ -1340,7 +1358,7 @@ size_t small_circuit_smem_bytes(int M, int N) {
 // psi = V[:, 0] (the reference's matvec with e_0 adds only exact zeros to V[i][0]).
 template <int N>
 __global__ void __launch_bounds__(1024) small_circuit_kernel(const SmallLayerDesc* __restrict__ layers, int nlayers,
-                                                            uint32_t row_begin, int M,
+                                                            int transpose, uint32_t row_begin, int M,
                                                             const double* __restrict__ x,
                                                             double* __restrict__ v_out,
                                                             double* __restrict__ psi) {
@@ -1378,7 +1396,10 @@ __global__ void __launch_bounds__(1024) small_circuit_kernel(const SmallLayerDes
         asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-    for (int e = tid; e < MN; e += blockDim.x) layer_entry(desc[0], row_begin + e / N, e % N, sm[e], sm[MN + e]);
+    for (int e = tid; e < MN; e += blockDim.x) {
+        const uint32_t r = row_begin + e / N, c = e % N;
+        layer_entry(desc[0], transpose ? c : r, transpose ? r : c, sm[e], sm[MN + e]);
+    }
     int cur = 0;  // V in planes [2 cur, 2 cur + 1] of sm
     for (int l = 1; l < nlayers; ++l) {
         asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -1394,8 +1415,10 @@ __global__ void __launch_bounds__(1024) small_circuit_kernel(const SmallLayerDes
         for (int q = 0; q < MAXQ; ++q) accr[q] = acci[q] = 0.0;
         for (int k0 = 0; k0 < N; k0 += KC) {
             if (k0 > 0) __syncthreads();  // the previous chunk is consumed
-            for (int e = tid; e < KC * N; e += blockDim.x)
-                layer_entry(d, static_cast<uint32_t>(k0 + e / N), static_cast<uint32_t>(e % N), lr[e], li[e]);
+            for (int e = tid; e < KC * N; e += blockDim.x) {
+                const uint32_t r = static_cast<uint32_t>(k0 + e / N), c = static_cast<uint32_t>(e % N);
+                layer_entry(d, transpose ? c : r, transpose ? r : c, lr[e], li[e]);
+            }
             __syncthreads();
 #pragma unroll
             for (int q = 0; q < MAXQ; ++q) {
@@ -1475,7 +1498,7 @@ __host__ __device__ constexpr size_t small_op_bytes() {
 
 template <int N>
 __global__ void __launch_bounds__(1024) small_dmma_kernel(const SmallLayerDesc* __restrict__ layers, int nlayers,
-                                                        int batch, uint32_t row_begin, int M,
+                                                        int batch, int transpose, uint32_t row_begin, int M,
                                                         const double* __restrict__ x,
                                                         double* __restrict__ v_out, double* __restrict__ psi) {
     static_assert(N >= 8 && N <= 64, "DMMA small path: 8 <= N <= 64");
@@ -1496,7 +1519,8 @@ __global__ void __launch_bounds__(1024) small_dmma_kernel(const SmallLayerDesc* 
     const int g = lane >> 2, t = lane & 3;
     for (int e = tid; e < 8 * N; e += blockDim.x) {
         const int i = e / N, j = e % N;
-        layer_entry(layers[0], row_begin + i, j, sm[i * S + j], sm[VP + i * S + j]);
+        const uint32_t r = row_begin + i, c = j;
+        layer_entry(layers[0], transpose ? c : r, transpose ? r : c, sm[i * S + j], sm[VP + i * S + j]);
     }
     int cur = 0;
     for (int l0 = 1; l0 < nlayers; l0 += batch) {
@@ -1538,7 +1562,8 @@ __global__ void __launch_bounds__(1024) small_dmma_kernel(const SmallLayerDesc* 
                         fb ^= lb;
                     }
                     double* e = o + c * S + k;
-                    layer_entry(d, k, c, e[0], e[OP]);
+                    // the operand's entry (k, c): L(k, c), or L(c, k) for column blocks (operand L^T)
+                    layer_entry(d, transpose ? c : k, transpose ? k : c, e[0], e[OP]);
                 }
             }
         }
@@ -1600,8 +1625,8 @@ __global__ void __launch_bounds__(1024) small_dmma_kernel(const SmallLayerDesc* 
 }
 
 template <int N>
-static int launch_small_t(const SmallLayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, const double* x, double* v,
-                          double* psi, cudaStream_t st) {
+static int launch_small_t(const SmallLayerDesc* d_layers, int nlayers, int transpose, uint32_t row_begin, int M,
+                          const double* x, double* v, double* psi, cudaStream_t st) {
     // rows per CTA: 8 from N = 32 (several SMs), all of them below
     const int R = (N >= 32 && M % 8 == 0) ? 8 : M;
     if (N >= 8 && N <= 64 && M % 8 == 0 && !std::getenv("QSB_SMALL_FMA")) {
@@ -1609,27 +1634,27 @@ static int launch_small_t(const SmallLayerDesc* d_layers, int nlayers, uint32_t 
         int batch = static_cast<int>((kSmallSmemMax - small_v_bytes<NT>()) / small_op_bytes<NT>());
         batch = std::max(1, std::min(batch, std::max(1, nlayers - 1)));
         const size_t smem = small_v_bytes<NT>() + static_cast<size_t>(batch) * small_op_bytes<NT>();
-        small_dmma_kernel<NT><<<M / 8, 1024, smem, st>>>(d_layers, nlayers, batch, row_begin, M, x, v, psi);
+        small_dmma_kernel<NT><<<M / 8, 1024, smem, st>>>(d_layers, nlayers, batch, transpose, row_begin, M, x, v, psi);
         return static_cast<int>(cudaGetLastError());
     }
     const size_t smem = small_circuit_smem_bytes(R, N);
     int threads = R * N;
     if (threads > 1024) threads = 1024;
     threads = (threads + 31) / 32 * 32;
-    small_circuit_kernel<N><<<M / R, threads, smem, st>>>(d_layers, nlayers, row_begin, M, x, v, psi);
+    small_circuit_kernel<N><<<M / R, threads, smem, st>>>(d_layers, nlayers, transpose, row_begin, M, x, v, psi);
     return static_cast<int>(cudaGetLastError());
 }
 
-int launch_small_circuit(const SmallLayerDesc* d_layers, int nlayers, uint32_t row_begin, int M, int N,
-                         const double* x, double* v, double* psi, void* stream) {
+int launch_small_circuit(const SmallLayerDesc* d_layers, int nlayers, int transpose, uint32_t row_begin, int M,
+                         int N, const double* x, double* v, double* psi, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (N) {
-    case 2: return launch_small_t<2>(d_layers, nlayers, row_begin, M, x, v, psi, st);
-    case 4: return launch_small_t<4>(d_layers, nlayers, row_begin, M, x, v, psi, st);
-    case 8: return launch_small_t<8>(d_layers, nlayers, row_begin, M, x, v, psi, st);
-    case 16: return launch_small_t<16>(d_layers, nlayers, row_begin, M, x, v, psi, st);
-    case 32: return launch_small_t<32>(d_layers, nlayers, row_begin, M, x, v, psi, st);
-    case 64: return launch_small_t<64>(d_layers, nlayers, row_begin, M, x, v, psi, st);
+    case 2: return launch_small_t<2>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
+    case 4: return launch_small_t<4>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
+    case 8: return launch_small_t<8>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
+    case 16: return launch_small_t<16>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
+    case 32: return launch_small_t<32>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
+    case 64: return launch_small_t<64>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
     default: return static_cast<int>(cudaErrorInvalidValue);
     }
 }
@@ -1666,6 +1691,34 @@ __global__ void __launch_bounds__(256) matvec_kernel(const double* __restrict__ 
             psi[M + row] = si;
         }
     }
+}
+
+// Column blocks: V holds U[:, cols]^T (rows i <-> columns col0 + i of U), so the
+// shard's share of psi = U psi0 is psi[k] = sum_i V[i][k] x[col0 + i] over the rows
+// [i0, i0 + count) of the shard; one thread per k (coalesced over k), i ascending.
+__global__ void __launch_bounds__(256) matvec_t_kernel(const double* __restrict__ v, int M, int N, int i0, int count,
+                                                       int col0, const double* __restrict__ x,
+                                                       double* __restrict__ psi) {
+    const size_t plane = static_cast<size_t>(M) * N;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+        double sr = 0.0, si = 0.0;
+        for (int i = i0; i < i0 + count; ++i) {
+            const double ar = v[static_cast<size_t>(i) * N + k], ai = v[plane + static_cast<size_t>(i) * N + k];
+            const double xr = x[col0 + i - i0], xi = x[N + col0 + i - i0];
+            sr += ar * xr - ai * xi;
+            si += ar * xi + ai * xr;
+        }
+        psi[k] = sr;
+        psi[N + k] = si;
+    }
+}
+
+int launch_matvec_t(const double* v, int M, int N, int i0, int count, int col0, const double* x, double* psi,
+                    void* stream) {
+    int blocks = (N + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    matvec_t_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(v, M, N, i0, count, col0, x, psi);
+    return static_cast<int>(cudaGetLastError());
 }
 
 int launch_matvec(const double* v, int M, int N, const double* x, double* psi, void* stream) {

@@ -307,6 +307,7 @@ struct qsb_plan {
     bool borrowed = false;
     CUtensorMap tmap[2];
     int final_buf = 0;
+    bool columns = false;  // QSB_FLAG_COLUMN_BLOCKS: V = U[:, cols]^T, operands L^T in application order
     const void* small_layers_dev = nullptr;  // one-shot small plans: descriptors read in place from pinned staging
     double* psi_dev_out = nullptr;            // ... and psi written straight into pinned staging
     bool x_is_e0 = true;  // psi0 = |0...0>: the one-CTA path reads psi as column 0
@@ -500,12 +501,24 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     p->row_begin = row_begin;
     p->row_count = row_count;
     // Row-form chain: reverse application order; instruction-only layers are exact identities.
-    for (auto it = p->cc.app.rbegin(); it != p->cc.app.rend(); ++it) {
-        if (it->nblocks == 0)
-            ++p->n_identity;
+    // Column blocks: U[:, cols] <- S_k U[:, cols] in application order, run as
+    // V <- V L^T on V = U[:, cols]^T — the reference's own association (U_k = S_k U_{k-1}).
+    p->columns = (h->flags & QSB_FLAG_COLUMN_BLOCKS) != 0;
+    auto rebuild_chain = [&] {
+        p->chain.clear();
+        p->n_identity = 0;
+        auto take = [&](const qsb::LayerDesc& d) {
+            if (d.nblocks == 0)
+                ++p->n_identity;
+            else
+                p->chain.push_back(d);
+        };
+        if (p->columns)
+            for (const auto& d : p->cc.app) take(d);
         else
-            p->chain.push_back(*it);
-    }
+            for (auto it = p->cc.app.rbegin(); it != p->cc.app.rend(); ++it) take(*it);
+    };
+    rebuild_chain();
     p->small = N <= 64;  // measured: row-resident CUDA-core chains lose to K2 from N = 128 (r39)
     int64_t M = row_count;
     if (!p->small) {
@@ -546,15 +559,13 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     const size_t plane_bytes = static_cast<size_t>(M) * N * 8;
     p->b.v[0].ensure(p->planes * plane_bytes);
     if (!p->small && p->chain.size() > 1) p->b.v[1].ensure(p->planes * plane_bytes);
-    p->b.psi.ensure(2 * static_cast<size_t>(M) * 8);
+    p->b.psi.ensure(2 * static_cast<size_t>(p->columns ? N : M) * 8);  // column blocks: a full-length partial psi
     p->b.x.ensure(2 * static_cast<size_t>(N) * 8);
     const auto t2 = tnow();
     upload_tables(p.get(), c);
     const auto t3 = tnow();
     // re-derive the chain with patched table pointers
-    p->chain.clear();
-    for (auto it = p->cc.app.rbegin(); it != p->cc.app.rend(); ++it)
-        if (it->nblocks != 0) p->chain.push_back(*it);
+    rebuild_chain();
     for (auto& d : p->chain) set_monomial(d);
     // Dense, non-monomial layers whose generation would put several FP64 products
     // per element on the producer warps (they queue behind DMMA on the shared FP64
@@ -567,7 +578,9 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
         for (size_t i = 1; i < p->chain.size(); ++i) {
             const qsb::LayerDesc& d = p->chain[i];
             bool m;
-            if (force >= 0) {
+            if (p->columns) {
+                m = true;  // the operand is L^T: materialised (K1 rows of L are its transposed planes)
+            } else if (force >= 0) {
                 m = force == 1;
             } else if (h->flags & QSB_FLAG_MATERIALIZE) {
                 m = true;
@@ -576,7 +589,11 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
                 for (int b = 0; b < d.nblocks; ++b)
                     if (d.blocks[b].shift < 6) low += d.blocks[b].kind == qsb::kBlockGate ? 1 : 4;
                 const double frac = std::ldexp(1.0, -__builtin_popcount(d.zmask >> 6));
-                m = !d.monomial && frac * low >= 1.0;
+                // complex layers too (QFT's controlled phases): generating their three B planes
+                // (re, im, re + im) puts DADDs on the producer's FP64 pipe next to the DMMAs;
+                // the K1t pass costs less than it saves (QFT-12 1004 -> 992 ms, QFT-11 109.0 ->
+                // 105.9 ms, QFT-10 12.50 -> 12.30 ms; real layers keep the generator: r74)
+                m = (!d.monomial && frac * low >= 1.0) || !d.real;
             }
             p->mat[i] = m ? 1 : 0;
             any = any || m;
@@ -592,6 +609,10 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
                                       qsb::gemm_tile_cols(p->tile), bp);
                 p->tmap_b_real = make_tmap(p->b.lmat.p, static_cast<int>(N), static_cast<int>(N),
                                            qsb::gemm_tile_cols(p->tile), 1);
+            } else if (p->columns) {
+                char mb[64];
+                format_bytes(bytes, mb, sizeof mb);
+                raise(QSB_ERR_RESOURCE, "column blocks need a %s operator buffer next to V; it does not fit", mb);
             } else {
                 std::fill(p->mat.begin(), p->mat.end(), 0);  // does not fit next to V: generate instead
             }
@@ -600,7 +621,7 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     if (p->chain.empty()) p->chain.push_back(identity_layer(n));
     // psi0 = |0...0> (zero_state, state.cpp:37-47), written on the device (the
     // one-CTA path reads psi as column 0 and never touches x for |0...0>)
-    if (!p->small)
+    if (!p->small || p->columns)
         cuda_check(qsb::sv_launch_init_identity(p->b.x.as<double>(), p->b.x.as<double>() + N, N, 1, 0, dc->stream),
                    "init psi0");
     p->x_is_e0 = true;
@@ -733,23 +754,37 @@ void enqueue(qsb_plan* p, cudaStream_t s) {
     if (p->small) {
         const auto* layers = p->small_layers_dev ? static_cast<const qsb::SmallLayerDesc*>(p->small_layers_dev)
                                                  : p->b.layers.as<qsb::SmallLayerDesc>();
-        cuda_check(qsb::launch_small_circuit(layers, static_cast<int>(p->chain.size()), rb,
+        cuda_check(qsb::launch_small_circuit(layers, static_cast<int>(p->chain.size()), p->columns ? 1 : 0, rb,
                                              p->M, p->N, p->x_is_e0 ? nullptr : p->b.x.as<double>(),
                                              p->b.v[0].as<double>(),
                                              p->psi_dev_out ? p->psi_dev_out : p->b.psi.as<double>(), s),
                    "small_circuit_kernel");
+        if (p->columns)  // the kernel's row-form psi is replaced by this shard's share of U psi0
+            cuda_check(qsb::launch_matvec_t(p->b.v[0].as<double>(), p->M, p->N,
+                                            static_cast<int>(p->row_begin - p->eff_begin),
+                                            static_cast<int>(p->row_count), static_cast<int>(p->row_begin),
+                                            p->b.x.as<double>(), p->b.psi.as<double>(), s),
+                       "matvec_t_kernel");
         p->final_buf = 0;
         return;
     }
     const bool ev = p->timing && p->timed_run;
     if (ev) cuda_check(cudaEventRecord(p->ev[0], s), "event");
-    cuda_check(qsb::launch_expand(p->chain[0], rb, p->M, p->N, p->b.v[0].as<double>(), p->planes, s),
-               "expand_kernel");
+    if (p->columns)
+        cuda_check(qsb::launch_expand_cols(p->chain[0], rb, p->M, p->N, p->b.v[0].as<double>(), p->planes, s),
+                   "expand_kernel");
+    else
+        cuda_check(qsb::launch_expand(p->chain[0], rb, p->M, p->N, p->b.v[0].as<double>(), p->planes, s),
+                   "expand_kernel");
     if (ev) cuda_check(cudaEventRecord(p->ev[1], s), "event");
     int cur = 0;
     for (size_t i = 1; i < p->chain.size(); ++i) {
         const bool mat = p->mat[i] != 0;
-        if (mat)
+        if (mat && p->columns)  // operand L^T: its transposed planes are the rows of L
+            cuda_check(qsb::launch_expand(p->chain[i], 0, p->N, p->N, p->b.lmat.as<double>(),
+                                          qsb::gemm_tile_b_planes(p->tile), s),
+                       "expand_kernel");
+        else if (mat)
             cuda_check(qsb::launch_expand_t(p->chain[i], p->N, p->b.lmat.as<double>(),
                                             qsb::gemm_tile_b_planes(p->tile), s),
                        "expand_t_kernel");
@@ -764,8 +799,15 @@ void enqueue(qsb_plan* p, cudaStream_t s) {
         cur ^= 1;
     }
     if (ev) cuda_check(cudaEventRecord(p->ev[2], s), "event");
-    cuda_check(qsb::launch_matvec(p->b.v[cur].as<double>(), p->M, p->N, p->b.x.as<double>(), p->b.psi.as<double>(), s),
-               "matvec_kernel");
+    if (p->columns)
+        cuda_check(qsb::launch_matvec_t(p->b.v[cur].as<double>(), p->M, p->N,
+                                        static_cast<int>(p->row_begin - p->eff_begin), static_cast<int>(p->row_count),
+                                        static_cast<int>(p->row_begin), p->b.x.as<double>(), p->b.psi.as<double>(), s),
+                   "matvec_t_kernel");
+    else
+        cuda_check(qsb::launch_matvec(p->b.v[cur].as<double>(), p->M, p->N, p->b.x.as<double>(),
+                                      p->b.psi.as<double>(), s),
+                   "matvec_kernel");
     if (ev) cuda_check(cudaEventRecord(p->ev[3], s), "event");
     p->final_buf = cur;
 }
@@ -922,6 +964,7 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
     const int64_t rows = N / G;
     std::vector<std::unique_ptr<qsb_plan>> plans(G);
     std::vector<double*> staged(G, nullptr);
+    std::vector<std::vector<double>> vt(G);  // column blocks: V = U[:, cols]^T on the host
     auto release_all = [&] {
         for (auto& p : plans) release_plan(p);
     };
@@ -943,7 +986,10 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
                            "upload psi0");
             }
             double* mapped_psi = nullptr;
-            if (psi_re && p->small) {
+            if (psi_re && p->columns) {
+                // column blocks: every shard returns a full-length share of psi, summed below
+                staged[g] = static_cast<double*>(p->dc->stage_out(2 * static_cast<size_t>(N) * 8));
+            } else if (psi_re && p->small) {
                 // the one-CTA kernel writes psi straight into pinned staging (mapped): no copy call
                 staged[g] = static_cast<double*>(p->dc->stage_out(2 * static_cast<size_t>(p->M) * 8));
                 void* d = nullptr;
@@ -954,7 +1000,11 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
             }
             execute(p, s, false);
             const int64_t off = p->row_begin - p->eff_begin;
-            if (mapped_psi) {
+            if (p->columns) {
+                if (psi_re)
+                    cuda_check(cudaMemcpyAsync(staged[g], p->b.psi.p, 2 * static_cast<size_t>(N) * 8,
+                                               cudaMemcpyDeviceToHost, s), "download psi");
+            } else if (mapped_psi) {
                 // written by the kernel; read after the stream synchronisation below
             } else if (psi_re && p->M <= 65536) {
                 // one copy of both psi planes into pinned staging; scattered on the host after the sync
@@ -967,7 +1017,16 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
                 cuda_check(cudaMemcpyAsync(psi_im + p->row_begin, p->b.psi.as<double>() + p->M + off, rows * 8,
                                            cudaMemcpyDeviceToHost, s), "download psi");
             }
-            if (u_re) {
+            if (u_re && p->columns) {
+                // V = U[:, cols]^T: its rows land as columns of U (transposed on the host after the sync)
+                const double* v = p->b.v[p->final_buf].as<double>();
+                const size_t plane = static_cast<size_t>(p->M) * N;
+                vt[g].resize(2 * static_cast<size_t>(rows) * N);
+                cuda_check(cudaMemcpyAsync(vt[g].data(), v + off * N, rows * N * 8, cudaMemcpyDeviceToHost, s),
+                           "download U");
+                cuda_check(cudaMemcpyAsync(vt[g].data() + static_cast<size_t>(rows) * N, v + plane + off * N,
+                                           rows * N * 8, cudaMemcpyDeviceToHost, s), "download U");
+            } else if (u_re) {
                 const double* v = p->b.v[p->final_buf].as<double>();
                 const size_t plane = static_cast<size_t>(p->M) * N;
                 cuda_check(cudaMemcpyAsync(u_re + p->row_begin * N, v + off * N, rows * N * 8,
@@ -985,11 +1044,27 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
                              "expected %d over-count %d\n", d[0], d[1], d[2], d[3], d[4], d[5]);
                 std::memset(d, 0, 8 * sizeof(int));
             }
-            if (staged[g]) {
-                const qsb_plan* p = plans[g].get();
+            const qsb_plan* p = plans[g].get();
+            if (staged[g] && p->columns) {
+                // shares summed in shard order (deterministic); shard 0 initialises
+                for (int64_t k = 0; k < N; ++k) {
+                    psi_re[k] = g == 0 ? staged[g][k] : psi_re[k] + staged[g][k];
+                    psi_im[k] = g == 0 ? staged[g][N + k] : psi_im[k] + staged[g][N + k];
+                }
+            } else if (staged[g]) {
                 const int64_t off = p->row_begin - p->eff_begin;
                 std::memcpy(psi_re + p->row_begin, staged[g] + off, rows * 8);
                 std::memcpy(psi_im + p->row_begin, staged[g] + p->M + off, rows * 8);
+            }
+            if (!vt[g].empty()) {
+                const double* vr = vt[g].data();
+                const double* vi = vr + static_cast<size_t>(rows) * N;
+                for (int64_t i = 0; i < rows; ++i)
+                    for (int64_t k = 0; k < N; ++k) {
+                        u_re[k * N + p->row_begin + i] = vr[i * N + k];
+                        u_im[k * N + p->row_begin + i] = vi[i * N + k];
+                    }
+                std::vector<double>().swap(vt[g]);
             }
         }
         if (trace) {
@@ -1254,6 +1329,11 @@ qsb_status qsb_plan_unitary_device(const qsb_plan* plan, const double** re, cons
 qsb_status qsb_plan_state_device(const qsb_plan* plan, const double** re, const double** im) {
     return guarded([&] {
         if (!plan || !re || !im) raise(QSB_ERR_ARGUMENT, "null argument");
+        if (plan->columns) {  // the full-length share U[:, cols] psi0[cols]
+            *re = plan->b.psi.as<double>();
+            *im = plan->b.psi.as<double>() + plan->N;
+            return;
+        }
         *re = psi_rows(plan);
         *im = psi_rows(plan) + plan->M;
     });
@@ -1264,6 +1344,13 @@ qsb_status qsb_plan_copy_state(const qsb_plan* plan, double* dst_re, double* dst
         if (!plan || !dst_re || !dst_im) raise(QSB_ERR_ARGUMENT, "null argument");
         DeviceScope ds(plan->dc->device);
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->dc->stream;
+        if (plan->columns) {
+            const size_t bytes = static_cast<size_t>(plan->N) * 8;
+            cuda_check(cudaMemcpyAsync(dst_re, plan->b.psi.p, bytes, cudaMemcpyDefault, s), "copy psi");
+            cuda_check(cudaMemcpyAsync(dst_im, plan->b.psi.as<double>() + plan->N, bytes, cudaMemcpyDefault, s),
+                       "copy psi");
+            return;
+        }
         const size_t bytes = static_cast<size_t>(plan->row_count) * 8;
         cuda_check(cudaMemcpyAsync(dst_re, psi_rows(plan), bytes, cudaMemcpyDefault, s), "copy psi");
         cuda_check(cudaMemcpyAsync(dst_im, psi_rows(plan) + plan->M, bytes, cudaMemcpyDefault, s), "copy psi");

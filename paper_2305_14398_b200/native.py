@@ -29,7 +29,7 @@ assert OP_DTYPE.itemsize == 104
 
 OP_GATE, OP_CONTROL, OP_FUNCTION, OP_INSTRUCTION = 0, 1, 2, 3
 GEMM_AUTO, GEMM_4M, GEMM_3M = 0, 1, 2
-FLAG_NO_GRAPH, FLAG_MATERIALIZE = 1, 2
+FLAG_NO_GRAPH, FLAG_MATERIALIZE, FLAG_COLUMN_BLOCKS = 1, 2, 4
 TILE_NAMES = {0: "zgemm_gen_kernel<128,64> (4M)", 1: "zgemm_gen_kernel<64,64> (4M)", 2: "zgemm_gen_kernel<32,32> (4M)",
               3: "zgemm_ws_kernel<4M>", 4: "zgemm_ws_kernel<3M>", 5: "zgemm_ws_kernel<3M, sum plane>"}
 

@@ -11,7 +11,8 @@ from paper_2305_14398_b200.simulator import B200UnitarySimulator  # noqa: E402
 
 import os
 from paper_2305_14398_b200 import native as _n
-sim = B200UnitarySimulator(gemm_mode={'4m': _n.GEMM_4M, '3m': _n.GEMM_3M}.get(os.environ.get('QSB_GEMM', ''), _n.GEMM_AUTO))
+sim = B200UnitarySimulator(gemm_mode={'4m': _n.GEMM_4M, '3m': _n.GEMM_3M}.get(os.environ.get('QSB_GEMM', ''), _n.GEMM_AUTO),
+                           flags=int(os.environ.get('QSB_FLAGS', '0')))
 for spec in sys.argv[1:] or ["qft:10", "qft:12"]:
     name, n = spec.split(":")
     c, reg = q.make_named_circuit(name, int(n))
