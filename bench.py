@@ -360,12 +360,15 @@ def run_ours(args):
     job_tflops = float(tot.item()) / (ms_max * 1e-3) / 1e12
 
     # ---- e2e through the public API with host buffers ----
+    # (the device-timed plan is closed first: an open plan holds the handle's
+    # buffer cache, and the host call would allocate its own V buffers every step)
+    if plan is not None:
+        plan.close()
+        plan = None
     if vr > 1:
         e2e_ms, h2d, d2h = None, 0, 0  # the projection times one shard, not a full circuit
     else:
         e2e_ms, h2d, d2h = e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr)
-    if plan is not None:
-        plan.close()
 
     if rank == 0:
         clocks = clk.summary()

@@ -59,9 +59,9 @@ struct LayerDesc {
     BlockDesc blocks[kMaxBlocks];
 };
 
-// The one-launch small path (N <= 64, n <= 6) uploads and stages this compact
-// copy of each layer: the same fields, room for n blocks instead of kMaxBlocks.
-constexpr int kSmallMaxBlocks = 6;
+// The one-launch paths (K2s: N <= 64; K2m: N = 128, 256) upload and stage this
+// compact copy of each layer: the same fields, room for n <= 8 blocks instead of kMaxBlocks.
+constexpr int kSmallMaxBlocks = 8;
 struct SmallLayerDesc {
     uint32_t idmask;
     int32_t nblocks;

@@ -1645,9 +1645,265 @@ static int launch_small_t(const SmallLayerDesc* d_layers, int nlayers, int trans
     return static_cast<int>(cudaGetLastError());
 }
 
+// K2m: the one-launch chain for N = 128 and 256 (n = 7, 8). Per layer, a K2
+// GEMM of this size is ~15 us of fixed cost (launch, prologue, split-K
+// reduction) for < 1 us of DMMA work. Here the whole chain runs in one launch:
+// a cluster of CS CTAs owns 8 rows of V; CTA r of the cluster computes output
+// columns [r N/CS, (r+1) N/CS) of every layer, generating only those columns of
+// the operator (transposed, in shared memory, candidate entries only, in KCH
+// k chunks when the columns do not fit whole), K split
+// over KSPLIT warp groups whose partials are added in fixed order, and stores
+// its 8 x N/CS block of V' into the V' buffer of every CTA of the cluster
+// (st.shared::cluster); one cluster barrier per layer hands the full rows over.
+// The next layer's descriptor is fetched into registers during the DMMAs.
+template <int N, int CS, int KSPLIT, int KCH>
+struct MidCfg {
+    static constexpr int NC = N / CS;               // output columns per CTA
+    static constexpr int KC = N / KCH;              // k rows of the operator per generated chunk
+    static constexpr int SK = KC + 4;               // operator column stride
+    static constexpr int CB = NC / 8;               // 8-column DMMA blocks per CTA
+    static constexpr int WARPS = CB * KSPLIT;
+    static constexpr int THREADS = 32 * WARPS;
+    static constexpr int S = N + 4;                 // row stride (bank-conflict-free fragments)
+    static constexpr int VP = 8 * S;                // one plane of V
+    static constexpr int OP = NC * SK;              // one plane of the operator chunk's columns
+    static constexpr int KS = KC / 4 / KSPLIT;      // m8n8k4 steps per warp per chunk
+    static constexpr size_t RED = static_cast<size_t>(KSPLIT - 1) * CB * 32 * 4;  // partials
+    static constexpr size_t BASE = sizeof(double) * (4 * VP + 2 * OP + RED);  // + descriptor slots
+    static constexpr size_t SMEM = BASE + 2 * sizeof(SmallLayerDesc);          // with a 2-slot ring
+    static_assert(THREADS <= 1024 && SMEM <= kSmallSmemMax, "K2m configuration does not fit one SM");
+    static_assert(KC % (4 * KSPLIT) == 0 && NC % 8 == 0, "K2m tiling");
+};
+
+__device__ __forceinline__ void st_cluster_v2(uint32_t local_addr, uint32_t rank, double a, double b) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(rank));
+    asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(remote), "d"(a), "d"(b) : "memory");
+}
+
+template <int N, int CS, int KSPLIT, int KCH>
+__global__ void __launch_bounds__(MidCfg<N, CS, KSPLIT, KCH>::THREADS, 1)
+    mid_dmma_kernel(const SmallLayerDesc* __restrict__ layers, int nlayers, int all_staged, int transpose,
+                    uint32_t row_begin, int M, const double* __restrict__ x, double* __restrict__ v_out,
+                    double* __restrict__ psi) {
+    using C = MidCfg<N, CS, KSPLIT, KCH>;
+    constexpr int S = C::S, VP = C::VP, OP = C::OP, NC = C::NC, KC = C::KC, SK = C::SK;
+    constexpr int DW = static_cast<int>(sizeof(SmallLayerDesc) / 8);
+    static_assert(sizeof(SmallLayerDesc) % 8 == 0, "descriptors move in 8-byte words");
+    extern __shared__ __align__(16) double sm[];
+    double* ops = sm + 4 * VP;                       // [re | im][NC][S], transposed: (column, k)
+    double* red = ops + 2 * OP;                      // [KSPLIT-1][CB][32 lanes][4]
+    // descriptor slots: every layer's (all_staged: read once, up front — short chains,
+    // where a per-layer fetch would sit on the critical path), or a 2-slot ring
+    SmallLayerDesc* descs = reinterpret_cast<SmallLayerDesc*>(red + C::RED);
+    const int rank = blockIdx.x;                     // cluster (CS, 1, 1) spans gridDim.x
+    const int c0 = rank * NC;
+    const int cta_row = blockIdx.y * 8;
+    row_begin += static_cast<uint32_t>(cta_row);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int cb = warp % C::CB, kp = warp / C::CB;
+    const unsigned long long* lsrc = reinterpret_cast<const unsigned long long*>(layers);
+    // V0 = the first operand's rows (every CTA holds full rows); descriptor 1 staged
+    for (int e = tid; e < 8 * N; e += C::THREADS) {
+        const int i = e / N, j = e % N;
+        const uint32_t r = row_begin + i, c = j;
+        layer_entry(layers[0], transpose ? c : r, transpose ? r : c, sm[i * S + j], sm[VP + i * S + j]);
+    }
+    if (all_staged) {
+        unsigned long long* dst = reinterpret_cast<unsigned long long*>(descs);
+        for (int w = tid; w < nlayers * DW; w += C::THREADS) dst[w] = __ldg(lsrc + w);
+    } else if (nlayers > 1 && tid < DW) {
+        reinterpret_cast<unsigned long long*>(descs + 1)[tid] = __ldg(lsrc + DW + tid);
+    }
+    {
+        double2* z = reinterpret_cast<double2*>(ops);
+        for (int w = tid; w < OP; w += C::THREADS) z[w] = make_double2(0.0, 0.0);  // 2 planes
+    }
+    cluster_sync();  // every CTA of the cluster runs before any remote store
+    // The operator buffer is all zeros between chunks: a chunk writes its candidate
+    // entries, and after its DMMAs clears just those again (or the whole buffer
+    // when the candidates outnumber it) — no full memset per chunk.
+    auto candidates = [&](const SmallLayerDesc& d, uint32_t fmask, int f, uint32_t k0, bool clear) {
+        // candidate entries of this CTA's columns: k agrees with c on zmask (and lies in the chunk)
+        for (int idx = tid; idx < (NC << f); idx += C::THREADS) {
+            const int cl = idx >> f;
+            const uint32_t c = static_cast<uint32_t>(c0 + cl);
+            uint32_t sub = static_cast<uint32_t>(idx) & ((1u << f) - 1u);
+            uint32_t k = c & ~fmask, fb = fmask;
+            while (fb) {
+                const uint32_t lb = fb & (0u - fb);
+                if (sub & 1u) k |= lb;
+                sub >>= 1;
+                fb ^= lb;
+            }
+            if (KCH > 1 && k - k0 >= static_cast<uint32_t>(KC)) continue;
+            double* e = ops + cl * SK + (k - k0);
+            if (clear) {
+                e[0] = 0.0;
+                e[OP] = 0.0;
+            } else {
+                layer_entry(d, transpose ? c : k, transpose ? k : c, e[0], e[OP]);
+            }
+        }
+    };
+    auto wipe = [&](const SmallLayerDesc& d, uint32_t fmask, int f, uint32_t k0) {
+        if ((NC << f) > OP / 2) {
+            double2* z = reinterpret_cast<double2*>(ops);
+            for (int w = tid; w < OP; w += C::THREADS) z[w] = make_double2(0.0, 0.0);
+        } else {
+            candidates(d, fmask, f, k0, true);
+        }
+    };
+    int cur = 0;
+    for (int l = 1; l < nlayers; ++l) {
+        const SmallLayerDesc& d = descs[all_staged ? l : (l & 1)];
+        unsigned long long next = 0;  // descriptor l + 1, in flight during this layer
+        if (!all_staged && l + 1 < nlayers && tid < DW) next = __ldg(lsrc + static_cast<size_t>(l + 1) * DW + tid);
+        double cr0[2] = {0.0, 0.0}, ci0[2] = {0.0, 0.0}, cr1[2] = {0.0, 0.0}, ci1[2] = {0.0, 0.0};
+        const uint32_t fmask = ~d.zmask & static_cast<uint32_t>(N - 1);
+        const int f = __popc(fmask);
+#pragma unroll 1
+        for (int ch = 0; ch < KCH; ++ch) {
+            const uint32_t k0 = static_cast<uint32_t>(ch * KC);
+            if (ch > 0) {
+                __syncthreads();  // the previous chunk's operator is consumed
+                wipe(d, fmask, f, k0 - KC);
+                __syncthreads();
+            }
+            candidates(d, fmask, f, k0, false);
+            __syncthreads();
+            const int kl = kp * C::KS;  // this warp's k steps within the chunk
+            const double* ltr = ops + (8 * cb + g) * SK + t + 4 * kl;
+            const double* lti = ltr + OP;
+            const double* vr = sm + (2 * cur) * VP + g * S + t + static_cast<int>(k0) + 4 * kl;
+            const double* vi = vr + VP;
+            if (d.real) {  // exact zero imaginary plane: the products with it add signed zeros
+#pragma unroll
+                for (int ks = 0; ks < C::KS; ++ks) {
+                    const double br = ltr[4 * ks];
+                    dmma((ks & 1) ? cr1 : cr0, vr[4 * ks], br);
+                    dmma((ks & 1) ? ci1 : ci0, vi[4 * ks], br);
+                }
+            } else {
+#pragma unroll
+                for (int ks = 0; ks < C::KS; ++ks) {
+                    const double ar = vr[4 * ks], ai = vi[4 * ks];
+                    const double br = ltr[4 * ks], bi = lti[4 * ks];
+                    dmma((ks & 1) ? cr1 : cr0, ar, br);
+                    dmma((ks & 1) ? cr1 : cr0, ai, neg(bi));
+                    dmma((ks & 1) ? ci1 : ci0, ar, bi);
+                    dmma((ks & 1) ? ci1 : ci0, ai, br);
+                }
+            }
+        }
+        double o[4] = {cr0[0] + cr1[0], cr0[1] + cr1[1], ci0[0] + ci1[0], ci0[1] + ci1[1]};
+        if (KSPLIT > 1 && kp > 0) {
+            double* r = red + ((static_cast<size_t>(kp - 1) * C::CB + cb) * 32 + lane) * 4;
+            *reinterpret_cast<double4*>(r) = make_double4(o[0], o[1], o[2], o[3]);
+        }
+        __syncthreads();  // every DMMA of the layer is done: partials visible, operator free
+        wipe(d, fmask, f, static_cast<uint32_t>((KCH - 1) * KC));
+        if (KSPLIT > 1) {
+            if (kp == 0) {
+#pragma unroll
+                for (int q = 1; q < KSPLIT; ++q) {  // fixed k order: deterministic
+                    const double4 p = *reinterpret_cast<const double4*>(
+                        red + ((static_cast<size_t>(q - 1) * C::CB + cb) * 32 + lane) * 4);
+                    o[0] += p.x;
+                    o[1] += p.y;
+                    o[2] += p.z;
+                    o[3] += p.w;
+                }
+            }
+        }
+        if (kp == 0) {
+            double* tr = sm + (2 * (cur ^ 1)) * VP + g * S + c0 + 8 * cb + 2 * t;
+            const uint32_t ar = static_cast<uint32_t>(__cvta_generic_to_shared(tr));
+            const uint32_t ai = static_cast<uint32_t>(__cvta_generic_to_shared(tr + VP));
+#pragma unroll
+            for (int q = 0; q < CS; ++q) {
+                st_cluster_v2(ar, static_cast<uint32_t>(q), o[0], o[1]);
+                st_cluster_v2(ai, static_cast<uint32_t>(q), o[2], o[3]);
+            }
+        }
+        if (!all_staged && l + 1 < nlayers && tid < DW)
+            reinterpret_cast<unsigned long long*>(descs + ((l + 1) & 1))[tid] = next;
+        cluster_sync();  // V' rows complete in every CTA; ops and descs[l & 1] free
+        cur ^= 1;
+    }
+    const double* vr = sm + (2 * cur) * VP;
+    const double* vi = vr + VP;
+    const int out_plane = M * N;
+    for (int e = tid; e < 8 * NC; e += C::THREADS) {
+        const int i = e / NC, j = c0 + e % NC;
+        v_out[static_cast<size_t>(cta_row + i) * N + j] = vr[i * S + j];
+        v_out[out_plane + static_cast<size_t>(cta_row + i) * N + j] = vi[i * S + j];
+    }
+    if (rank == 0) {
+        for (int i = tid; i < 8; i += C::THREADS) {
+            if (x == nullptr) {
+                psi[cta_row + i] = vr[i * S];
+                psi[M + cta_row + i] = vi[i * S];
+                continue;
+            }
+            double sr = 0.0, si = 0.0;
+            for (int k = 0; k < N; ++k) {
+                const double a_r = vr[i * S + k], a_i = vi[i * S + k];
+                sr += a_r * x[k] - a_i * x[N + k];
+                si += a_r * x[N + k] + a_i * x[k];
+            }
+            psi[cta_row + i] = sr;
+            psi[M + cta_row + i] = si;
+        }
+    }
+}
+
+template <int N, int CS, int KSPLIT, int KCH>
+static int launch_mid_t(const SmallLayerDesc* d_layers, int nlayers, int transpose, uint32_t row_begin, int M,
+                        const double* x, double* v, double* psi, cudaStream_t st) {
+    using C = MidCfg<N, CS, KSPLIT, KCH>;
+    if (M % 8 != 0) return static_cast<int>(cudaErrorInvalidValue);
+    const int all_staged = C::BASE + sizeof(SmallLayerDesc) * static_cast<size_t>(nlayers) <= kSmallSmemMax;
+    static_assert(C::THREADS * 8 >= static_cast<int>(sizeof(SmallLayerDesc)), "ring: one word per thread");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CS, M / 8, 1);
+    cfg.blockDim = dim3(C::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = all_staged ? C::BASE + sizeof(SmallLayerDesc) * std::max(nlayers, 2) : C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, mid_dmma_kernel<N, CS, KSPLIT, KCH>, d_layers, nlayers, all_staged,
+                                               transpose, row_begin, M, x, v, psi));
+}
+
+// N = 128: clusters of 4 (32 columns per CTA, K over 8 warp groups), 16 row blocks.
+// N = 256: clusters of 4 (64 columns per CTA, K over 4 warp groups, operator in
+// two k chunks), 32 row blocks: 128 CTAs, one wave.
+#define QSB_MID_128 128, 4, 8, 1
+#define QSB_MID_256 256, 4, 4, 2
+// N = 64: clusters of 2, K over 8 warp groups (2 m8n8k4 steps each). Measured
+// against K2s (r76): QFT-6 57.9 -> 57.5 us, DJ-6 22.7 -> 14.5 us; for N <= 32
+// K2s's batched generation wins (QFT-4 8.4 vs 16.5 us) and stays.
+#define QSB_MID_64 64, 2, 8, 1
+
 int launch_small_circuit(const SmallLayerDesc* d_layers, int nlayers, int transpose, uint32_t row_begin, int M,
                          int N, const double* x, double* v, double* psi, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    switch (N) {
+    case 128: return launch_mid_t<QSB_MID_128>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
+    case 256: return launch_mid_t<QSB_MID_256>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
+    default: break;
+    }
+    const bool classic = std::getenv("QSB_SMALL_CLASSIC") != nullptr;  // K2s instead of K2m
+    if (!classic) {
+        if (N == 64) return launch_mid_t<QSB_MID_64>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
+    }
     switch (N) {
     case 2: return launch_small_t<2>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
     case 4: return launch_small_t<4>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
@@ -1788,6 +2044,13 @@ static int configure_small_t() {
                                                  static_cast<int>(kSmallSmemMax)));
 }
 
+template <int N, int CS, int KSPLIT, int KCH>
+static int configure_mid_t() {
+    return static_cast<int>(cudaFuncSetAttribute(mid_dmma_kernel<N, CS, KSPLIT, KCH>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(kSmallSmemMax)));
+}
+
 // Kernel attributes, set once per device before any launch or graph capture.
 int configure_kernels() {
     int e;
@@ -1800,6 +2063,9 @@ int configure_kernels() {
     query_ws_clusters();
     if ((e = configure_small_t<8>()) || (e = configure_small_t<16>()) || (e = configure_small_t<32>()) ||
         (e = configure_small_t<64>()))
+        return e;
+    if ((e = configure_mid_t<QSB_MID_64>()) || (e = configure_mid_t<QSB_MID_128>()) ||
+        (e = configure_mid_t<QSB_MID_256>()))
         return e;
     if ((e = static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel<32>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024))))

@@ -519,7 +519,17 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
             for (auto it = p->cc.app.rbegin(); it != p->cc.app.rend(); ++it) take(*it);
     };
     rebuild_chain();
-    p->small = N <= 64;  // measured: row-resident CUDA-core chains lose to K2 from N = 128 (r39)
+    // one-launch chains: K2s (N <= 64) and the cluster kernel K2m (N = 128, 256), whose
+    // per-layer cost is far below a K2 launch's fixed cost at these sizes
+    p->small = N <= 64 || (N <= 256 && !std::getenv("QSB_NO_MID") && !std::getenv("QSB_TILE"));
+    if (p->small && N == 256) {
+        // K2m generates each CTA's operator columns itself (every cluster repeats it):
+        // a dense non-monomial layer (DJ's H on every qubit: 2^8 candidates per column,
+        // an 8-block fold each) costs more there than K2's one materialisation (DJ-8
+        // 44 us on K2, 89 us on K2m; r75). Such chains keep the GEMM path at N = 256.
+        for (const auto& d : p->chain)
+            if (!d.monomial && __builtin_popcount(~d.zmask & static_cast<uint32_t>(N - 1)) >= 7) p->small = false;
+    }
     int64_t M = row_count;
     if (!p->small) {
         // The tiled kernels need at least 32 rows and power-of-two shards; widen
@@ -627,7 +637,7 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     p->x_is_e0 = true;
     if (p->small) {
         // compact descriptors (n <= 6 blocks each) written straight into pinned staging
-        static_assert(qsb::kSmallMaxBlocks >= 6, "the small path covers n <= 6");
+        static_assert(qsb::kSmallMaxBlocks >= 8, "the one-launch paths cover n <= 8");
         const size_t bytes = sizeof(qsb::SmallLayerDesc) * p->chain.size();
         p->b.layers.ensure(bytes);
         auto* st = static_cast<qsb::SmallLayerDesc*>(dc->stage(bytes));
@@ -645,7 +655,8 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
         // A one-shot call (run_full) lets the kernel read the pinned staging in place
         // (mapped host memory): no copy call. Plans that outlive the call upload.
         void* mapped = nullptr;
-        if (borrow_cache && cudaHostGetDevicePointer(&mapped, st, 0) == cudaSuccess) {
+        // (K2s only: K2m fetches one descriptor per layer on its critical path.)
+        if (borrow_cache && N <= 64 && cudaHostGetDevicePointer(&mapped, st, 0) == cudaSuccess) {
             p->small_layers_dev = mapped;
         } else {
             cudaGetLastError();
