@@ -1882,7 +1882,8 @@ static int launch_mid_t(const SmallLayerDesc* d_layers, int nlayers, int transpo
                                                transpose, row_begin, M, x, v, psi));
 }
 
-// N = 128: clusters of 4 (32 columns per CTA, K over 8 warp groups), 16 row blocks.
+// N = 128: clusters of 4 (32 columns per CTA, K over 8 warp groups), 16 row blocks
+// (clusters of 8 with K over 16 groups measured slower: QFT-7 103 -> 178 us, r79).
 // N = 256: clusters of 4 (64 columns per CTA, K over 4 warp groups, operator in
 // two k chunks), 32 row blocks: 128 CTAs, one wave.
 #define QSB_MID_128 128, 4, 8, 1

@@ -683,7 +683,7 @@ def test_column_blocks(orc, G):
     rows = B200UnitarySimulator()
     cols = B200UnitarySimulator(flags=native.FLAG_COLUMN_BLOCKS, devices=[0] * G if G > 1 else None)
     rng = np.random.default_rng(808)
-    for name, n in [("qft", 4), ("qft", 6), ("entangle", 8), ("deutsch-jozsa", 9), ("qft", 10)]:
+    for name, n in [("qft", 4), ("qft", 6), ("qft", 7), ("entangle", 8), ("deutsch-jozsa", 9), ("qft", 10)]:
         c, reg = q.make_named_circuit(name, n)
         flat = native.flatten(c, reg)
         N = 1 << n
