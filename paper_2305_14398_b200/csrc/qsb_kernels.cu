@@ -1656,7 +1656,7 @@ static int launch_small_t(const SmallLayerDesc* d_layers, int nlayers, int trans
 // its 8 x N/CS block of V' into the V' buffer of every CTA of the cluster
 // (st.shared::cluster); one cluster barrier per layer hands the full rows over.
 // The next layer's descriptor is fetched into registers during the DMMAs.
-template <int N, int CS, int KSPLIT, int KCH>
+template <int N, int CS, int KSPLIT, int KCH, bool DBUF = false>
 struct MidCfg {
     static constexpr int NC = N / CS;               // output columns per CTA
     static constexpr int KC = N / KCH;              // k rows of the operator per generated chunk
@@ -1669,10 +1669,12 @@ struct MidCfg {
     static constexpr int OP = NC * SK;              // one plane of the operator chunk's columns
     static constexpr int KS = KC / 4 / KSPLIT;      // m8n8k4 steps per warp per chunk
     static constexpr size_t RED = static_cast<size_t>(KSPLIT - 1) * CB * 32 * 4;  // partials
-    static constexpr size_t BASE = sizeof(double) * (4 * VP + 2 * OP + RED);  // + descriptor slots
+    static constexpr int NOPS = DBUF ? 2 : 1;       // operator buffers (DBUF: next layer's made early)
+    static constexpr size_t BASE = sizeof(double) * (4 * VP + NOPS * 2 * OP + RED);  // + descriptor slots
     static constexpr size_t SMEM = BASE + 2 * sizeof(SmallLayerDesc);          // with a 2-slot ring
     static_assert(THREADS <= 1024 && SMEM <= kSmallSmemMax, "K2m configuration does not fit one SM");
     static_assert(KC % (4 * KSPLIT) == 0 && NC % 8 == 0, "K2m tiling");
+    static_assert(!DBUF || KCH == 1, "double-buffered operators: whole columns");
 };
 
 __device__ __forceinline__ void st_cluster_v2(uint32_t local_addr, uint32_t rank, double a, double b) {
@@ -1681,18 +1683,18 @@ __device__ __forceinline__ void st_cluster_v2(uint32_t local_addr, uint32_t rank
     asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(remote), "d"(a), "d"(b) : "memory");
 }
 
-template <int N, int CS, int KSPLIT, int KCH>
-__global__ void __launch_bounds__(MidCfg<N, CS, KSPLIT, KCH>::THREADS, 1)
+template <int N, int CS, int KSPLIT, int KCH, bool DBUF>
+__global__ void __launch_bounds__(MidCfg<N, CS, KSPLIT, KCH, DBUF>::THREADS, 1)
     mid_dmma_kernel(const SmallLayerDesc* __restrict__ layers, int nlayers, int all_staged, int transpose,
                     uint32_t row_begin, int M, const double* __restrict__ x, double* __restrict__ v_out,
                     double* __restrict__ psi) {
-    using C = MidCfg<N, CS, KSPLIT, KCH>;
+    using C = MidCfg<N, CS, KSPLIT, KCH, DBUF>;
     constexpr int S = C::S, VP = C::VP, OP = C::OP, NC = C::NC, KC = C::KC, SK = C::SK;
     constexpr int DW = static_cast<int>(sizeof(SmallLayerDesc) / 8);
     static_assert(sizeof(SmallLayerDesc) % 8 == 0, "descriptors move in 8-byte words");
     extern __shared__ __align__(16) double sm[];
-    double* ops = sm + 4 * VP;                       // [re | im][NC][S], transposed: (column, k)
-    double* red = ops + 2 * OP;                      // [KSPLIT-1][CB][32 lanes][4]
+    double* ops = sm + 4 * VP;                       // [NOPS][re | im][NC][SK], transposed: (column, k)
+    double* red = ops + C::NOPS * 2 * OP;            // [KSPLIT-1][CB][32 lanes][4]
     // descriptor slots: every layer's (all_staged: read once, up front — short chains,
     // where a per-layer fetch would sit on the critical path), or a 2-slot ring
     SmallLayerDesc* descs = reinterpret_cast<SmallLayerDesc*>(red + C::RED);
@@ -1718,13 +1720,12 @@ __global__ void __launch_bounds__(MidCfg<N, CS, KSPLIT, KCH>::THREADS, 1)
     }
     {
         double2* z = reinterpret_cast<double2*>(ops);
-        for (int w = tid; w < OP; w += C::THREADS) z[w] = make_double2(0.0, 0.0);  // 2 planes
+        for (int w = tid; w < C::NOPS * OP; w += C::THREADS) z[w] = make_double2(0.0, 0.0);  // 2 planes each
     }
-    cluster_sync();  // every CTA of the cluster runs before any remote store
     // The operator buffer is all zeros between chunks: a chunk writes its candidate
     // entries, and after its DMMAs clears just those again (or the whole buffer
     // when the candidates outnumber it) — no full memset per chunk.
-    auto candidates = [&](const SmallLayerDesc& d, uint32_t fmask, int f, uint32_t k0, bool clear) {
+    auto candidates = [&](const SmallLayerDesc& d, uint32_t fmask, int f, uint32_t k0, bool clear, double* ob) {
         // candidate entries of this CTA's columns: k agrees with c on zmask (and lies in the chunk)
         for (int idx = tid; idx < (NC << f); idx += C::THREADS) {
             const int cl = idx >> f;
@@ -1738,7 +1739,7 @@ __global__ void __launch_bounds__(MidCfg<N, CS, KSPLIT, KCH>::THREADS, 1)
                 fb ^= lb;
             }
             if (KCH > 1 && k - k0 >= static_cast<uint32_t>(KC)) continue;
-            double* e = ops + cl * SK + (k - k0);
+            double* e = ob + cl * SK + (k - k0);
             if (clear) {
                 e[0] = 0.0;
                 e[OP] = 0.0;
@@ -1747,14 +1748,23 @@ __global__ void __launch_bounds__(MidCfg<N, CS, KSPLIT, KCH>::THREADS, 1)
             }
         }
     };
-    auto wipe = [&](const SmallLayerDesc& d, uint32_t fmask, int f, uint32_t k0) {
+    auto wipe = [&](const SmallLayerDesc& d, uint32_t fmask, int f, uint32_t k0, double* ob) {
         if ((NC << f) > OP / 2) {
-            double2* z = reinterpret_cast<double2*>(ops);
+            double2* z = reinterpret_cast<double2*>(ob);
             for (int w = tid; w < OP; w += C::THREADS) z[w] = make_double2(0.0, 0.0);
         } else {
-            candidates(d, fmask, f, k0, true);
+            candidates(d, fmask, f, k0, true, ob);
         }
     };
+    auto free_bits = [](const SmallLayerDesc& d) { return ~d.zmask & static_cast<uint32_t>(N - 1); };
+    if (DBUF) {  // every descriptor is staged: layer 1's operator is made before the loop
+        __syncthreads();
+        if (nlayers > 1) {
+            const uint32_t fm = free_bits(descs[1]);
+            candidates(descs[1], fm, __popc(fm), 0, false, ops + 2 * OP);
+        }
+    }
+    cluster_sync();  // every CTA of the cluster runs before any remote store
     int cur = 0;
     for (int l = 1; l < nlayers; ++l) {
         const SmallLayerDesc& d = descs[all_staged ? l : (l & 1)];
@@ -1763,18 +1773,21 @@ __global__ void __launch_bounds__(MidCfg<N, CS, KSPLIT, KCH>::THREADS, 1)
         double cr0[2] = {0.0, 0.0}, ci0[2] = {0.0, 0.0}, cr1[2] = {0.0, 0.0}, ci1[2] = {0.0, 0.0};
         const uint32_t fmask = ~d.zmask & static_cast<uint32_t>(N - 1);
         const int f = __popc(fmask);
+        double* ob = DBUF ? ops + (l & 1) * 2 * OP : ops;  // this layer's operator
 #pragma unroll 1
         for (int ch = 0; ch < KCH; ++ch) {
             const uint32_t k0 = static_cast<uint32_t>(ch * KC);
-            if (ch > 0) {
-                __syncthreads();  // the previous chunk's operator is consumed
-                wipe(d, fmask, f, k0 - KC);
+            if (!DBUF) {  // (DBUF: made during the previous layer's store phase)
+                if (ch > 0) {
+                    __syncthreads();  // the previous chunk's operator is consumed
+                    wipe(d, fmask, f, k0 - KC, ob);
+                    __syncthreads();
+                }
+                candidates(d, fmask, f, k0, false, ob);
                 __syncthreads();
             }
-            candidates(d, fmask, f, k0, false);
-            __syncthreads();
             const int kl = kp * C::KS;  // this warp's k steps within the chunk
-            const double* ltr = ops + (8 * cb + g) * SK + t + 4 * kl;
+            const double* ltr = ob + (8 * cb + g) * SK + t + 4 * kl;
             const double* lti = ltr + OP;
             const double* vr = sm + (2 * cur) * VP + g * S + t + static_cast<int>(k0) + 4 * kl;
             const double* vi = vr + VP;
@@ -1803,7 +1816,11 @@ __global__ void __launch_bounds__(MidCfg<N, CS, KSPLIT, KCH>::THREADS, 1)
             *reinterpret_cast<double4*>(r) = make_double4(o[0], o[1], o[2], o[3]);
         }
         __syncthreads();  // every DMMA of the layer is done: partials visible, operator free
-        wipe(d, fmask, f, static_cast<uint32_t>((KCH - 1) * KC));
+        wipe(d, fmask, f, static_cast<uint32_t>((KCH - 1) * KC), ob);
+        if (DBUF && l + 1 < nlayers) {  // the next layer's operator, into the other buffer
+            const uint32_t fm = free_bits(descs[l + 1]);
+            candidates(descs[l + 1], fm, __popc(fm), 0, false, ops + ((l + 1) & 1) * 2 * OP);
+        }
         if (KSPLIT > 1) {
             if (kp == 0) {
 #pragma unroll
@@ -1859,13 +1876,14 @@ __global__ void __launch_bounds__(MidCfg<N, CS, KSPLIT, KCH>::THREADS, 1)
     }
 }
 
-template <int N, int CS, int KSPLIT, int KCH>
+template <int N, int CS, int KSPLIT, int KCH, bool DBUF = false>
 static int launch_mid_t(const SmallLayerDesc* d_layers, int nlayers, int transpose, uint32_t row_begin, int M,
                         const double* x, double* v, double* psi, cudaStream_t st) {
-    using C = MidCfg<N, CS, KSPLIT, KCH>;
+    using C = MidCfg<N, CS, KSPLIT, KCH, DBUF>;
     if (M % 8 != 0) return static_cast<int>(cudaErrorInvalidValue);
     const int all_staged = C::BASE + sizeof(SmallLayerDesc) * static_cast<size_t>(nlayers) <= kSmallSmemMax;
     static_assert(C::THREADS * 8 >= static_cast<int>(sizeof(SmallLayerDesc)), "ring: one word per thread");
+    if (DBUF && !all_staged) return static_cast<int>(cudaErrorInvalidValue);  // caller checks mid_dbuf_fits
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CS, M / 8, 1);
     cfg.blockDim = dim3(C::THREADS, 1, 1);
@@ -1878,7 +1896,7 @@ static int launch_mid_t(const SmallLayerDesc* d_layers, int nlayers, int transpo
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return static_cast<int>(cudaLaunchKernelEx(&cfg, mid_dmma_kernel<N, CS, KSPLIT, KCH>, d_layers, nlayers, all_staged,
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, mid_dmma_kernel<N, CS, KSPLIT, KCH, DBUF>, d_layers, nlayers, all_staged,
                                                transpose, row_begin, M, x, v, psi));
 }
 
@@ -1893,16 +1911,31 @@ static int launch_mid_t(const SmallLayerDesc* d_layers, int nlayers, int transpo
 // K2s's batched generation wins (QFT-4 8.4 vs 16.5 us) and stays.
 #define QSB_MID_64 64, 2, 8, 1
 
+// Double-buffered operators (the next layer's generated while this layer's
+// partials are reduced and stored: one barrier per layer less) need every
+// descriptor staged next to two operator buffers. QSB_MID_NODBUF turns it off.
+static bool mid_dbuf(int nlayers, size_t base) {
+    return !std::getenv("QSB_MID_NODBUF") &&
+           base + sizeof(SmallLayerDesc) * static_cast<size_t>(std::max(nlayers, 2)) <= kSmallSmemMax;
+}
+
 int launch_small_circuit(const SmallLayerDesc* d_layers, int nlayers, int transpose, uint32_t row_begin, int M,
                          int N, const double* x, double* v, double* psi, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (N) {
-    case 128: return launch_mid_t<QSB_MID_128>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
+    case 128:
+        if (mid_dbuf(nlayers, MidCfg<128, 4, 8, 1, true>::BASE))
+            return launch_mid_t<128, 4, 8, 1, true>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
+        if (mid_dbuf(nlayers, MidCfg<128, 4, 4, 1, true>::BASE))
+            return launch_mid_t<128, 4, 4, 1, true>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
+        return launch_mid_t<QSB_MID_128>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
     case 256: return launch_mid_t<QSB_MID_256>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
     default: break;
     }
     const bool classic = std::getenv("QSB_SMALL_CLASSIC") != nullptr;  // K2s instead of K2m
     if (!classic) {
+        if (N == 64 && mid_dbuf(nlayers, MidCfg<64, 2, 8, 1, true>::BASE))
+            return launch_mid_t<64, 2, 8, 1, true>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
         if (N == 64) return launch_mid_t<QSB_MID_64>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
     }
     switch (N) {
@@ -2045,9 +2078,9 @@ static int configure_small_t() {
                                                  static_cast<int>(kSmallSmemMax)));
 }
 
-template <int N, int CS, int KSPLIT, int KCH>
+template <int N, int CS, int KSPLIT, int KCH, bool DBUF = false>
 static int configure_mid_t() {
-    return static_cast<int>(cudaFuncSetAttribute(mid_dmma_kernel<N, CS, KSPLIT, KCH>,
+    return static_cast<int>(cudaFuncSetAttribute(mid_dmma_kernel<N, CS, KSPLIT, KCH, DBUF>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  static_cast<int>(kSmallSmemMax)));
 }
@@ -2066,7 +2099,8 @@ int configure_kernels() {
         (e = configure_small_t<64>()))
         return e;
     if ((e = configure_mid_t<QSB_MID_64>()) || (e = configure_mid_t<QSB_MID_128>()) ||
-        (e = configure_mid_t<QSB_MID_256>()))
+        (e = configure_mid_t<QSB_MID_256>()) || (e = configure_mid_t<64, 2, 8, 1, true>()) ||
+        (e = configure_mid_t<128, 4, 8, 1, true>()) || (e = configure_mid_t<128, 4, 4, 1, true>()))
         return e;
     if ((e = static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel<32>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024))))

@@ -762,7 +762,7 @@ def test_mid_cluster_chain_random_golden(golden, sim):
     assert seen >= 60
 
 
-@pytest.mark.parametrize("n", [5, 6])
+@pytest.mark.parametrize("n", [5, 6, 7])
 def test_small_k2m_matches_row_resident(monkeypatch, sim, orc, n):
     """N = 64 runs K2m (clusters of 2 CTAs, K over 8 warp groups; N = 32 keeps
     K2s); the K2s row-resident kernel (QSB_SMALL_CLASSIC) stays selectable. Both
@@ -789,7 +789,10 @@ def test_small_k2m_matches_row_resident(monkeypatch, sim, orc, n):
         assert rel_frob(ur, ui, orr, ori) <= TOL
         re, im = orc.unitary_simulate(flat, guard=n)
         assert rel_frob(out.re, out.im, re, im) <= TOL
-        monkeypatch.setenv("QSB_SMALL_CLASSIC", "1")
-        kr, ki = sim.build_unitary(flat)
-        monkeypatch.delenv("QSB_SMALL_CLASSIC")
-        assert rel_frob(ur, ui, kr, ki) <= TOL
+        # the other paths: K2s (N <= 64) or the K2 chain (N = 128), and K2m without
+        # double-buffered operators
+        for env in ("QSB_SMALL_CLASSIC" if n <= 6 else "QSB_NO_MID", "QSB_MID_NODBUF"):
+            monkeypatch.setenv(env, "1")
+            kr, ki = sim.build_unitary(flat)
+            monkeypatch.delenv(env)
+            assert rel_frob(ur, ui, kr, ki) <= TOL, env
