@@ -112,9 +112,11 @@ int launch_zgemm(const GemmArgs& a, int tile, int gemm_mode, void* stream);
 // K1t: transposed operator planes for a materialised B (planes 2: re, im; 3: + re+im)
 int launch_expand_t(const LayerDesc& layer, int N, double* out, int planes, void* stream);
 int gemm_tile_b_planes(int tile);
-// transpose = 1: column blocks (operands L^T, V = U[:, cols]^T)
-int launch_small_circuit(const SmallLayerDesc* d_layers, int nlayers, int transpose, uint32_t row_begin, int M,
-                         int N, const double* x, double* v, double* psi, void* stream);
+// transpose = 1: column blocks (operands L^T, V = U[:, cols]^T). max_free_bits: the
+// largest number of free index bits (f) of any layer after the first — 2^f candidate
+// entries per operator column, i.e. how much generation work a layer can need.
+int launch_small_circuit(const SmallLayerDesc* d_layers, int nlayers, int max_free_bits, int transpose,
+                         uint32_t row_begin, int M, int N, const double* x, double* v, double* psi, void* stream);
 // rows [col_begin, col_begin + M) of L^T (the first layer of a column block)
 int launch_expand_cols(const LayerDesc& layer, uint32_t col_begin, int M, int N, double* out, int planes,
                        void* stream);

@@ -1919,17 +1919,27 @@ static bool mid_dbuf(int nlayers, size_t base) {
            base + sizeof(SmallLayerDesc) * static_cast<size_t>(std::max(nlayers, 2)) <= kSmallSmemMax;
 }
 
-int launch_small_circuit(const SmallLayerDesc* d_layers, int nlayers, int transpose, uint32_t row_begin, int M,
-                         int N, const double* x, double* v, double* psi, void* stream) {
+int launch_small_circuit(const SmallLayerDesc* d_layers, int nlayers, int max_free_bits, int transpose,
+                         uint32_t row_begin, int M, int N, const double* x, double* v, double* psi, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // K2m thread count: DMMA-bound layers run best with few warps (short barriers, small
+    // reductions; r82: QFT-8 303 -> 262 us with K over 1 group instead of 4, QFT-7
+    // 82 -> 76.5 us with 2 instead of 4), while layers with many candidate entries per
+    // operator column (DJ's H on every qubit) need every thread for their generation
+    // (DJ-7 22.6 us with 8 groups, 36.9 with 2).
+    const bool dense = max_free_bits >= 4;
     switch (N) {
     case 128:
+        if (!dense && mid_dbuf(nlayers, MidCfg<128, 4, 2, 1, true>::BASE))
+            return launch_mid_t<128, 4, 2, 1, true>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
         if (mid_dbuf(nlayers, MidCfg<128, 4, 8, 1, true>::BASE))
             return launch_mid_t<128, 4, 8, 1, true>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
         if (mid_dbuf(nlayers, MidCfg<128, 4, 4, 1, true>::BASE))
             return launch_mid_t<128, 4, 4, 1, true>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
         return launch_mid_t<QSB_MID_128>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
-    case 256: return launch_mid_t<QSB_MID_256>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
+    case 256:
+        if (!dense) return launch_mid_t<256, 4, 1, 2>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
+        return launch_mid_t<QSB_MID_256>(d_layers, nlayers, transpose, row_begin, M, x, v, psi, st);
     default: break;
     }
     const bool classic = std::getenv("QSB_SMALL_CLASSIC") != nullptr;  // K2s instead of K2m
@@ -2100,7 +2110,8 @@ int configure_kernels() {
         return e;
     if ((e = configure_mid_t<QSB_MID_64>()) || (e = configure_mid_t<QSB_MID_128>()) ||
         (e = configure_mid_t<QSB_MID_256>()) || (e = configure_mid_t<64, 2, 8, 1, true>()) ||
-        (e = configure_mid_t<128, 4, 8, 1, true>()) || (e = configure_mid_t<128, 4, 4, 1, true>()))
+        (e = configure_mid_t<128, 4, 8, 1, true>()) || (e = configure_mid_t<128, 4, 4, 1, true>()) ||
+        (e = configure_mid_t<256, 4, 1, 2>()) || (e = configure_mid_t<128, 4, 2, 1, true>()))
         return e;
     if ((e = static_cast<int>(cudaFuncSetAttribute(small_circuit_kernel<32>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024))))

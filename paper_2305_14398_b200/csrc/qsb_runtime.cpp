@@ -765,7 +765,10 @@ void enqueue(qsb_plan* p, cudaStream_t s) {
     if (p->small) {
         const auto* layers = p->small_layers_dev ? static_cast<const qsb::SmallLayerDesc*>(p->small_layers_dev)
                                                  : p->b.layers.as<qsb::SmallLayerDesc>();
-        cuda_check(qsb::launch_small_circuit(layers, static_cast<int>(p->chain.size()), p->columns ? 1 : 0, rb,
+        int max_f = 0;
+        for (size_t i = 1; i < p->chain.size(); ++i)
+            max_f = std::max(max_f, __builtin_popcount(~p->chain[i].zmask & static_cast<uint32_t>(p->N - 1)));
+        cuda_check(qsb::launch_small_circuit(layers, static_cast<int>(p->chain.size()), max_f, p->columns ? 1 : 0, rb,
                                              p->M, p->N, p->x_is_e0 ? nullptr : p->b.x.as<double>(),
                                              p->b.v[0].as<double>(),
                                              p->psi_dev_out ? p->psi_dev_out : p->b.psi.as<double>(), s),
