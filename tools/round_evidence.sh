@@ -1,7 +1,7 @@
 #!/bin/bash
-# Round evidence after K2m: GPU tests, smoke, bench lines + launch list, reference arm,
+# Round evidence: GPU tests, smoke, bench lines + launch list, reference arm,
 # one ncu --set full capture of K2m (QFT-8), and the qubit sweep.
-TAG=${1:-r77}
+TAG=${1:-r84}
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest.log 2>&1; echo "exit $?" >> gpurun_out/${TAG}_pytest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/${TAG}_smoke.log
