@@ -205,10 +205,10 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, tag: str = "bench"):
         self.device = device
         self.proc = None
-        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_bench_{device}.csv")
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{tag}_{device}.csv")
 
     def __enter__(self):
         try:
@@ -365,10 +365,13 @@ def run_ours(args):
     if plan is not None:
         plan.close()
         plan = None
+    e2e_clocks = None
     if vr > 1:
         e2e_ms, h2d, d2h = None, 0, 0  # the projection times one shard, not a full circuit
     else:
-        e2e_ms, h2d, d2h = e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr)
+        with ClockSampler(local, "e2e") as eclk:
+            e2e_ms, h2d, d2h = e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr)
+        e2e_clocks = eclk.summary()
 
     if rank == 0:
         clocks = clk.summary()
@@ -401,7 +404,8 @@ def run_ours(args):
                                         "profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no FP64 entry"},
             "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "qsb_simulate_full_state (C ABI)" if world == 1 else
-                           "qsb_plan_create/execute + NCCL all-gather + D2H"},
+                           "qsb_plan_create/execute + NCCL all-gather + D2H",
+                    "clocks": e2e_clocks},
             "gpu_launches": (info.n_launches if info else 0) * args.steps,
             "clocks": clocks,
         }
