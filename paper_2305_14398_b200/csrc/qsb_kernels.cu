@@ -1645,8 +1645,8 @@ static int launch_small_t(const SmallLayerDesc* d_layers, int nlayers, int trans
     return static_cast<int>(cudaGetLastError());
 }
 
-// K2m: the one-launch chain for N = 128 and 256 (n = 7, 8). Per layer, a K2
-// GEMM of this size is ~15 us of fixed cost (launch, prologue, split-K
+// K2m: the one-launch chain for N = 64, 128 and 256 (n = 6, 7, 8). Per layer, a
+// K2 GEMM of this size is ~15 us of fixed cost (launch, prologue, split-K
 // reduction) for < 1 us of DMMA work. Here the whole chain runs in one launch:
 // a cluster of CS CTAs owns 8 rows of V; CTA r of the cluster computes output
 // columns [r N/CS, (r+1) N/CS) of every layer, generating only those columns of
@@ -1655,7 +1655,10 @@ static int launch_small_t(const SmallLayerDesc* d_layers, int nlayers, int trans
 // over KSPLIT warp groups whose partials are added in fixed order, and stores
 // its 8 x N/CS block of V' into the V' buffer of every CTA of the cluster
 // (st.shared::cluster); one cluster barrier per layer hands the full rows over.
-// The next layer's descriptor is fetched into registers during the DMMAs.
+// Descriptors are staged in shared memory up front when they fit, else the next
+// one is fetched into registers during the DMMAs. DBUF (whole columns, every
+// descriptor staged): two operator buffers, the next layer's generated while
+// this layer's partials are reduced and stored.
 template <int N, int CS, int KSPLIT, int KCH, bool DBUF = false>
 struct MidCfg {
     static constexpr int NC = N / CS;               // output columns per CTA
@@ -1900,10 +1903,11 @@ static int launch_mid_t(const SmallLayerDesc* d_layers, int nlayers, int transpo
                                                transpose, row_begin, M, x, v, psi));
 }
 
-// N = 128: clusters of 4 (32 columns per CTA, K over 8 warp groups), 16 row blocks
-// (clusters of 8 with K over 16 groups measured slower: QFT-7 103 -> 178 us, r79).
-// N = 256: clusters of 4 (64 columns per CTA, K over 4 warp groups, operator in
-// two k chunks), 32 row blocks: 128 CTAs, one wave.
+// Fallback configurations (launch_small_circuit picks DBUF / fewer-warp variants
+// first). N = 128: clusters of 4 (32 columns per CTA, K over 8 warp groups), 16
+// row blocks (clusters of 8 with K over 16 groups measured slower: QFT-7 103 ->
+// 178 us, r79). N = 256: clusters of 4 (64 columns per CTA, K over 4 warp groups,
+// operator in two k chunks), 32 row blocks: 128 CTAs, one wave.
 #define QSB_MID_128 128, 4, 8, 1
 #define QSB_MID_256 256, 4, 4, 2
 // N = 64: clusters of 2, K over 8 warp groups (2 m8n8k4 steps each). Measured
