@@ -59,6 +59,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--gemm-mode", default="auto", choices=["auto", "4m", "3m"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU check of the multi-rank plumbing: the same launch (re-exec under torchrun for "
+                         "--gpus N), rank-count checks, row_shard and the psi all-gather over gloo, with every "
+                         "rank contributing index-valued rows instead of computed ones (no kernels)")
     ap.add_argument("--virtual-ranks", type=int, default=1,
                     help="with one GPU: time only rank 0's row block of a G-way shard (the work each of G "
                          "GPUs does, with no communication but the final psi all-gather) and report it "
@@ -169,31 +173,64 @@ def cpu_sample_circuit(name: str, n: int, repeats: int = 1):
                              "steps": n_steps, "extra_layers": extra}}
 
 
+def model_validation(workload: str):
+    """Measured error of the extrapolation model against full reference runs on a
+    GPU box's host (tools/cpu_pin.py -> profiles/cpu_pin.json)."""
+    path = os.path.join(ROOT, "profiles", "cpu_pin.json")
+    try:
+        with open(path) as f:
+            pins = json.load(f)
+    except Exception:
+        return None
+    rows = pins.get("runs", [])
+    errs = [abs(r["model_error"]) for r in rows]
+    out = {"source": "profiles/cpu_pin.json (tools/cpu_pin.py: full reference unitary-parallel "
+                     "simulate_full_state vs the model, same host cores)",
+           "workloads": {r["workload"]: round(r["model_error"], 4) for r in rows},
+           "max_abs_error": max(errs) if errs else None}
+    if workload in out["workloads"]:
+        out["this_workload_error"] = out["workloads"][workload]
+    return out
+
+
 def run_reference(args):
+    """The reference's own CPU path (oracle/_ref: the unmodified reference library)
+    on this host's cores. n <= 8: the whole simulate_full_state, timed --steps
+    times after --warmup runs. Larger n: one timed sample of the model's components
+    (one single-layer step_unitary, a parallel and a serial matmul row slab),
+    extrapolated ONCE to the circuit (extrapolated: true) — the model's error
+    against full reference runs is stated from profiles/cpu_pin.json."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     name, n = WORKLOADS[args.workload]
-    for _ in range(args.warmup):
-        cpu_sample(args.workload)
-    vals = []
     t0 = time.perf_counter()
-    last = None
-    for _ in range(args.steps):
+    if n <= 8:
+        for _ in range(args.warmup):
+            cpu_sample(args.workload)
+        runs = [cpu_sample(args.workload) for _ in range(args.steps)]
+        value = statistics.mean(r["value"] for r in runs)
+        last = runs[-1]
+        extrapolated, timed = False, len(runs)
+    else:
         last = cpu_sample(args.workload)
-        vals.append(last["value"])
+        value = last["value"]
+        extrapolated, timed = True, 1
     wall = time.perf_counter() - t0
-    value = statistics.mean(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "ms", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "deterministic circuit (synthetic)",
         "config": {"workload": args.workload, "circuit": name, "qubits": n, "parallelism": "host threads"},
         "cpu_baseline": {"value": value, "unit": "ms", "cores": last["cores"], "kind": last["kind"],
-                         "sample": last["sample"]},
+                         "sample": last["sample"], "extrapolated": extrapolated, "samples_timed": timed,
+                         "model_validation": model_validation(args.workload) if extrapolated else None},
         "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "extrapolated": extrapolated,
         "wall_s": wall,
     }
+    if "components_s" in last:
+        line["cpu_baseline"]["components_s"] = last["components_s"]
     print(json.dumps(line), flush=True)
     return 0
 
@@ -279,8 +316,15 @@ def run_ours(args):
     from paper_2305_14398_b200.simulator import B200UnitarySimulator
 
     rank, world, local = dist_env()
+    if world != max(1, args.gpus):
+        raise SystemExit(f"bench: --gpus {args.gpus} but {world} rank(s)")
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"bench: rank {rank} has LOCAL_RANK {local} but only {torch.cuda.device_count()} GPU(s)")
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator ranks are visible in the log
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if dist.get_world_size() != args.gpus:
+            raise SystemExit(f"bench: process group has {dist.get_world_size()} ranks, --gpus {args.gpus}")
     torch.cuda.set_device(local)
     name, n = WORKLOADS[args.workload]
     N = 1 << n
@@ -344,8 +388,21 @@ def run_ours(args):
     gemm_flops_step = info.gemm_flops if info else 0.0
     n_gemms = info.n_gemms if info else 0
     mean_gemm_ms = (sum(gemm_ms) / len(gemm_ms) / n_gemms) if (gemm_ms and n_gemms) else None
-    per_launch_flops = gemm_flops_step / n_gemms if n_gemms else 0.0
-    achieved = per_launch_flops / (mean_gemm_ms * 1e-3) / 1e12 if mean_gemm_ms else None
+    per_launch_flops = gemm_flops_step / n_gemms if n_gemms else 0.0  # credited 8 M N^2
+    hw_per_launch = info.gemm_hw_flops / n_gemms if n_gemms else 0.0  # what the DMMAs execute
+    achieved = hw_per_launch / (mean_gemm_ms * 1e-3) / 1e12 if mean_gemm_ms else None
+    credited = per_launch_flops / (mean_gemm_ms * 1e-3) / 1e12 if mean_gemm_ms else None
+    # per-kind breakdown: one more execute (after the timed region) with an event pair
+    # around every K2 launch — those events serialise the chained launches, so this
+    # run explains the timed one rather than replacing it
+    per_kind = None
+    if timed:
+        plan.set_timing(2)
+        plan.execute(s_ptr)
+        torch.cuda.synchronize()
+        g_ms, g_kind = plan.gemm_times()
+        plan.set_timing(0)
+        per_kind = k2_breakdown(g_ms, g_kind, per_launch_flops)
     traffic = None
     prof_json = os.path.join(ROOT, "profiles", "k2_traffic.json")
     if os.path.exists(prof_json):
@@ -354,10 +411,11 @@ def run_ours(args):
             if tr:
                 traffic = tr.get("dram_bytes_per_launch")
     chain_tflops = gemm_flops_step / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
-    tot = torch.tensor([gemm_flops_step], dtype=torch.float64, device="cuda")
+    tot = torch.tensor([gemm_flops_step, info.gemm_hw_flops if info else 0.0], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tot)
-    job_tflops = float(tot.item()) / (ms_max * 1e-3) / 1e12
+    job_tflops = float(tot[0].item()) / (ms_max * 1e-3) / 1e12  # credited 8N^3 per GEMM
+    job_hw_tflops = float(tot[1].item()) / (ms_max * 1e-3) / 1e12  # executed DMMA FLOPs
 
     # ---- e2e through the public API with host buffers ----
     # (the device-timed plan is closed first: an open plan holds the handle's
@@ -387,20 +445,29 @@ def run_ours(args):
                        "gemm_mode": args.gemm_mode,
                        "gemm_splitk": info.gemm_splits if info else None,
                        "l2": ("inputs larger than L2" if flush is None else "L2 flushed between steps")},
-            "tflops": job_tflops,
-            "fp64_peak_frac": job_tflops / (FP64_DMMA_PEAK_TFLOPS * world),
+            # whole job, every rank's GEMMs over the max-over-ranks circuit time
+            "tflops": job_hw_tflops,
+            "fp64_peak_frac": job_hw_tflops / (FP64_DMMA_PEAK_TFLOPS * world),
+            "credited_tflops": job_tflops,
+            "credited_fp64_peak_frac": job_tflops / (FP64_DMMA_PEAK_TFLOPS * world),
             "roofline": {"bound": "tensor", "kernel": (native.TILE_NAMES.get(info.gemm_tile, "small_circuit_kernel") + " (K2)") if info else None,
                          "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": (achieved / FP64_DMMA_PEAK_TFLOPS) if achieved else None,
-                         # hardware FLOPs the DMMAs execute: 6N^3 (3M), 4N^3 (real layer), 8N^3 (4M)
-                         # per GEMM, against the credited 8N^3 above
-                         "hw_frac": (achieved * (info.gemm_hw_flops / info.gemm_flops)
-                                     / FP64_DMMA_PEAK_TFLOPS) if achieved and info.gemm_flops else None,
+                         "flops_counted": "FP64 FLOPs the DMMAs execute per launch: 6MN^2 (3M complex layer), "
+                                          "4MN^2 (real layer: two real products), 8MN^2 (4M); mean over the "
+                                          "timed chain, K1t expansions included in the launch time",
+                         "hw_frac": (achieved / FP64_DMMA_PEAK_TFLOPS) if achieved else None,
+                         "credited_achieved": credited,
+                         "credited_frac": (credited / FP64_DMMA_PEAK_TFLOPS) if credited else None,
+                         "credited_note": "8MN^2 per GEMM (ZGEMM convention, SURVEY 8(d)); above 1 because 3M "
+                                          "and real layers execute fewer FLOPs than they are credited",
+                         "per_kind": per_kind,
                          "real_gemms": info.n_real_gemms if info else None,
                          "traffic": traffic,
-                         "algorithmic_flops_per_launch": per_launch_flops,
+                         "algorithmic_flops_per_launch": hw_per_launch,
                          "mean_launch_ms": mean_gemm_ms,
-                         "peak_source": "measured FP64 DMMA peak (tools/microbench/fp64_peak.cu, "
+                         "peak_source": "builder-measured FP64 DMMA peak of this pool's B200 (register-only "
+                                        "mma.sync.m8n8k4.f64 loop, tools/microbench/fp64_peak.cu, "
                                         "profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no FP64 entry"},
             "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "qsb_simulate_full_state (C ABI)" if world == 1 else
@@ -414,18 +481,44 @@ def run_ours(args):
             line["config"]["parallelism"] = f"row block 0 of {vr} (one shard on one GPU)"
             line["projection"] = {
                 "n_gpus": vr, "ms_per_circuit": ms_max,
-                "tflops_aggregate": job_tflops * vr,
-                "fp64_peak_frac_aggregate": job_tflops / FP64_DMMA_PEAK_TFLOPS,
+                "tflops_aggregate": job_hw_tflops * vr,
+                "fp64_peak_frac_aggregate": job_hw_tflops / FP64_DMMA_PEAK_TFLOPS,
+                "credited_tflops_aggregate": job_tflops * vr,
                 "method": f"rows [0, N/{vr}) of U timed alone on one B200: every rank does identical, "
                           "independent work (row blocks, operators regenerated locally); excludes the "
                           f"NCCL all-gather of psi ({16 * N // vr} bytes per rank)"}
         if world == 1 and vr == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_sample(args.workload)
+            cb = cpu_sample(args.workload)
+            cb["extrapolated"] = "components_s" in cb
+            if cb["extrapolated"]:
+                cb["model_validation"] = model_validation(args.workload)
+            line["cpu_baseline"] = cb
         print(json.dumps(line), flush=True)
     sim.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def k2_breakdown(ms, kinds, credited_per_launch):
+    """Per-kind K2 roofline from one mode-2 execute: kind bit 0 = real layer (two real
+    products, 4MN^2), bit 1 = operand materialised by K1t, bit 2 = 4M (8MN^2), else 3M (6MN^2)."""
+    groups = {}
+    for t, k in zip(ms, kinds):
+        arith = "4M" if k & 4 else ("real" if k & 1 else "3M")
+        key = f"{arith}{' materialised' if k & 2 else ' generated'}"
+        hw = credited_per_launch * (1.0 if k & 4 else (0.5 if k & 1 else 0.75))
+        g = groups.setdefault(key, {"launches": 0, "ms": 0.0, "hw_flops_per_launch": hw})
+        g["launches"] += 1
+        g["ms"] += t
+    out = {}
+    for key, g in groups.items():
+        mean = g["ms"] / g["launches"]
+        tf = g["hw_flops_per_launch"] / (mean * 1e-3) / 1e12
+        out[key] = {"launches": g["launches"], "mean_ms": mean, "hw_flops_per_launch": g["hw_flops_per_launch"],
+                    "achieved_tflops": tf, "frac": tf / FP64_DMMA_PEAK_TFLOPS,
+                    "credited_frac": credited_per_launch / (mean * 1e-3) / 1e12 / FP64_DMMA_PEAK_TFLOPS}
+    return out
 
 
 def e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr):
@@ -589,8 +682,75 @@ def run_sv(args):
     return 0
 
 
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def ensure_ranks(args) -> int:
+    """--gpus N is honoured or the run fails: under torchrun the world size must
+    equal N; a plain `python bench.py --gpus N` (N > 1) re-executes itself under
+    torch.distributed.run with one process per GPU, after checking that N GPUs
+    are visible. Returns 0 to continue in this process (never returns after exec)."""
+    rank, world, _ = dist_env()
+    if world > 1:
+        if world != args.gpus:
+            print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), flush=True)
+            sys.exit(2)
+        return 0
+    if args.gpus <= 1 or args.impl == "reference":
+        return 0
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus and not args.dry_run:
+        print(json.dumps({"error": f"--gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}",
+                          "n_gpus": have}), flush=True)
+        sys.exit(2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+    return 0
+
+
+def run_dry(args):
+    """--dry-run: the N > 1 plumbing on CPU over gloo (tests/test_sharding_gloo.py)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_14398_b200.sharding import gather_rows, row_shard
+
+    rank, world, _ = dist_env()
+    if world != max(1, args.gpus):
+        raise SystemExit(f"bench: --gpus {args.gpus} but {world} rank(s)")
+    if world > 1:
+        dist.init_process_group("gloo")
+    _, n = WORKLOADS[args.workload]
+    N = 1 << n
+    begin, count = row_shard(N, world, rank)
+    rows = torch.arange(begin, begin + count, dtype=torch.float64)
+    if world > 1:
+        re, im = gather_rows(rows, -rows, N, world)
+    else:
+        re, im = rows, -rows
+    want = torch.arange(N, dtype=torch.float64)
+    ok = bool(torch.equal(re, want) and torch.equal(im, -want))
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "workload": args.workload, "rows_per_rank": count,
+                          "gathered_ok": ok, "backend": dist.get_backend() if world > 1 else None}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0 if ok else 1
+
+
 def main():
     args = parse()
+    ensure_ranks(args)
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.backend != "dense":

@@ -124,12 +124,18 @@ enum {
     QSB_FLAG_NO_GRAPH = 1,        /* do not capture plan execution in a CUDA graph */
     QSB_FLAG_MATERIALIZE = 2,     /* materialise each layer operator with K1 and run the
                                      GEMM on it instead of generating tiles in shared memory */
-    QSB_FLAG_COLUMN_BLOCKS = 4    /* shard U by column blocks instead of row blocks:
+    QSB_FLAG_COLUMN_BLOCKS = 4,   /* shard U by column blocks instead of row blocks:
                                      U[:, cols] <- S_k U[:, cols] in application order, the
                                      reference's association; a plan's "rows" are then the columns
                                      [row_begin, row_begin + row_count) of U, its unitary buffer
                                      holds U[:, cols]^T and its state buffer the full-length share
                                      U[:, cols] psi0[cols] (2^n entries per plane) */
+    QSB_FLAG_NCCL_GATHER = 8      /* host-API calls all-gather the shards' psi rows over NCCL into a
+                                     device-resident psi on every device even when the handle has a
+                                     single device (a one-rank communicator; tests). With several
+                                     DISTINCT devices the NCCL all-gather is always used; repeated
+                                     device ids (virtual shards) cannot form a communicator and copy
+                                     each shard's rows to the host instead */
 };
 
 typedef struct qsb_handle qsb_handle;
@@ -226,12 +232,26 @@ qsb_status qsb_plan_destroy(qsb_plan* plan);
 qsb_status qsb_plan_get_info(const qsb_plan* plan, qsb_plan_info* info);
 
 /* Run the whole chain on `stream` (a cudaStream_t; NULL = the handle's stream):
- * V = rows of U, then psi_rows = V * psi0 (psi0 = |0...0> unless set). Async. */
+ * V = rows of U, then psi_rows = V * psi0 (psi0 = |0...0> unless set). Async.
+ * Plans on ONE device must not execute concurrently on different streams: a
+ * stream-K GEMM is a persistent grid sized to the SM count whose tile owners
+ * wait on other CTAs of the same grid, so two of them sharing the SMs can both
+ * be partly resident and wait forever (the host-API calls use one stream per
+ * physical device for this reason). */
 qsb_status qsb_plan_execute(qsb_plan* plan, void* stream);
 
 /* Record CUDA events around the K1 / K2 / K3 phases of every execute (disables
- * the plan's CUDA graph); read them back with qsb_plan_last_timing. */
+ * the plan's CUDA graph); read them back with qsb_plan_last_timing. enable = 2
+ * also brackets every K2 launch with its own event pair (qsb_plan_gemm_times);
+ * those events sit between chained launches and serialise them, so mode 2 is
+ * for a per-kind breakdown, not for timing the chain. */
 qsb_status qsb_plan_set_timing(qsb_plan* plan, int32_t enable);
+
+/* Per-K2-launch durations (ms) of the last mode-2 execute, in chain order, and
+ * each launch's kind: bit 0 = real layer (two real products), bit 1 = operand
+ * materialised by K1t, bit 2 = 4M arithmetic (else 3M). Fills min(cap, count)
+ * entries; *count = GEMMs per execute. ms / kinds may be NULL. */
+qsb_status qsb_plan_gemm_times(qsb_plan* plan, double* ms, int32_t* kinds, int32_t cap, int32_t* count);
 
 /* Replace psi0 (default |0...0>) with re/im planes of length 2^n (host or device
  * pointers), async on `stream`. */
@@ -244,6 +264,29 @@ qsb_status qsb_plan_state_device(const qsb_plan* plan, const double** re, const 
 
 /* Copy psi rows into caller device buffers (e.g. a slice of an all-gather buffer), async. */
 qsb_status qsb_plan_copy_state(const qsb_plan* plan, double* dst_re, double* dst_im, void* stream);
+
+/* ---- NCCL: the all-gather of psi rows (north star "only the final state
+ * vector is all-gathered with NCCL over NVLink") ----
+ *
+ * One process per GPU: rank 0 calls qsb_nccl_unique_id, the caller broadcasts the
+ * QSB_NCCL_ID_BYTES bytes (MPI, torch.distributed, a file ...), every rank calls
+ * qsb_comm_create on its handle (ncclCommInitRank on the handle's device). The
+ * in-process multi-device handle (qsb_options.n_devices > 1) builds its own
+ * communicator with ncclCommInitAll and needs none of this. */
+#define QSB_NCCL_ID_BYTES 128
+typedef struct qsb_comm qsb_comm;
+
+qsb_status qsb_nccl_unique_id(void* id_out);
+qsb_status qsb_comm_create(qsb_handle* handle, const void* id, int32_t n_ranks, int32_t rank, qsb_comm** out);
+qsb_status qsb_comm_destroy(qsb_comm* comm);
+/* NCCL version (e.g. 22809) of the library in use; loads libnccl. */
+qsb_status qsb_nccl_version(int32_t* version);
+
+/* All-gather the psi rows of every rank's plan into full-length device planes
+ * (2^n doubles each) on every rank, async on `stream`. Rank r's plan must own
+ * rows [r * 2^n / n_ranks, (r + 1) * 2^n / n_ranks) (row blocks, not column blocks). */
+qsb_status qsb_plan_allgather_state(const qsb_plan* plan, qsb_comm* comm, double* psi_re, double* psi_im,
+                                    void* stream);
 
 /* Kernel timing of the last execute, from CUDA events on the launching stream:
  * total, the K2 GEMM chain, and the mean single-GEMM duration (ms). Synchronises. */
@@ -315,9 +358,14 @@ qsb_status qsb_sv_plan_execute(qsb_sv_plan* plan, void* stream);
 /* Device planes of the result, [2^n][col_count] row-major (valid until the next execute/destroy). */
 qsb_status qsb_sv_plan_result_device(const qsb_sv_plan* plan, const double** re, const double** im);
 
-/* Reference memory accounting (unitary_backend.cpp:156-179), BackendKind 0 = Unitary, 1 = Fsv. */
+/* Reference memory accounting (unitary_backend.cpp:156-179), BackendKind 0 = Unitary, 1 = Fsv:
+ * memory_estimate (8 bytes per complex) and engine_memory_estimate (the reference
+ * engine's 3 N^2 + N complex doubles); 0 outside the reference's qubit ranges. */
 uint64_t qsb_memory_estimate(int32_t n_qubits, int32_t kind);
 uint64_t qsb_engine_memory_estimate(int32_t n_qubits, int32_t kind);
+/* This library's device footprint for a one-device dense run: two 2^n x 2^n complex
+ * V buffers + psi0 + psi (the HBM-derived guard budgets it at 92 % of device memory). */
+uint64_t qsb_hbm_footprint(int32_t n_qubits);
 
 #ifdef __cplusplus
 }

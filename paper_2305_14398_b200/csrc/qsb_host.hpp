@@ -126,7 +126,10 @@ struct Buffers {
 struct DeviceCtx {
     int device = 0;
     cudaStream_t stream = nullptr;
-    qsbh::Buffers cache;  // reused by the host-API calls
+    bool owns_stream = true;  // virtual shards on one device share that device's first stream
+    qsbh::Buffers cache;
+    void* nccl_comm = nullptr;  // ncclComm_t of this device in the handle's communicator (distinct devices)
+    qsbh::DevBuf gathered;      // [2][N] psi all-gathered over NCCL  // reused by the host-API calls
     // Pinned host staging for uploads on `stream` (descriptor arrays): reused by
     // the next call only after that call's stream synchronisation.
     struct Pinned {
@@ -158,6 +161,7 @@ struct qsb_handle {
     int gemm_mode = QSB_GEMM_AUTO;
     int flags = 0;
     std::vector<std::unique_ptr<DeviceCtx>> devs;
+    int nccl_ranks = 0;  // devices in the current NCCL communicator (devs[0 .. nccl_ranks)), 0 = none
     std::mutex mu;
     DeviceCtx& dev0() { return *devs.front(); }
 };

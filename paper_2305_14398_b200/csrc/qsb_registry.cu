@@ -196,20 +196,24 @@ __global__ void __launch_bounds__(THREADS, 1) gram_kernel(const __grid_constant_
     if (lane == 0) atomic_max_nonneg(maxdev, dev);
 }
 
-// N < 64: the reference's triple loop (linalg.cpp:139-151), one thread per entry.
-__global__ void gram_small_kernel(const double* __restrict__ re, const double* __restrict__ im, int N,
+// Dimensions that are not a multiple of the 64-wide tile (N < 64 for the
+// power-of-two registry matrices): the reference's triple loop (linalg.cpp:138-151),
+// one thread per entry, 64-bit indices, every product and sum separately rounded
+// in the reference's order (x86-64 without FMA contraction), so a verdict at the
+// tolerance boundary is the reference's.
+__global__ void gram_small_kernel(const double* __restrict__ re, const double* __restrict__ im, int64_t N,
                                   unsigned long long* __restrict__ maxdev) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     double dev = 0.0;
     if (idx < N * N) {
-        const int i = idx / N, j = idx % N;
+        const int64_t i = idx / N, j = idx % N;
         double sr = 0.0, si = 0.0;
-        for (int k = 0; k < N; ++k) {
+        for (int64_t k = 0; k < N; ++k) {
             const double air = re[k * N + i], aii = im[k * N + i], ajr = re[k * N + j], aji = im[k * N + j];
-            sr += air * ajr + aii * aji;
-            si += air * aji - aii * ajr;
+            sr = __dadd_rn(sr, __dadd_rn(__dmul_rn(air, ajr), __dmul_rn(aii, aji)));
+            si = __dadd_rn(si, __dsub_rn(__dmul_rn(air, aji), __dmul_rn(aii, ajr)));
         }
-        if (i == j) sr -= 1.0;
+        if (i == j) sr = __dsub_rn(sr, 1.0);
         dev = fmax(fabs(sr), fabs(si));
     }
     dev = warp_max(dev);
@@ -240,8 +244,10 @@ int launch_gram(const void* tmapT, int N, unsigned long long* maxdev, void* stre
 }
 
 int launch_gram_small(const double* re, const double* im, int N, unsigned long long* maxdev, void* stream) {
-    const int blocks = (N * N + 255) / 256;
-    reg::gram_small_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(re, im, N, maxdev);
+    const int64_t blocks = (static_cast<int64_t>(N) * N + 255) / 256;
+    if (blocks > 0x7fffffff) return static_cast<int>(cudaErrorInvalidValue);
+    reg::gram_small_kernel<<<static_cast<unsigned>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        re, im, static_cast<int64_t>(N), maxdev);
     return static_cast<int>(cudaGetLastError());
 }
 

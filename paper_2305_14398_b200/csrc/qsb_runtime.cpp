@@ -32,6 +32,7 @@
 #include "../../include/qsb.h"
 #include "qsb_host.hpp"
 #include "qsb_internal.hpp"
+#include "qsb_nccl.hpp"
 #include "qsb_sv.hpp"
 
 namespace {
@@ -101,16 +102,21 @@ Interval interval_of(const qsb_op& op) {
     return {op.target, 1};
 }
 
-// Guard first, then reset placement (unitary_backend.cpp:197-206).
+// Guard first, then reset placement (unitary_backend.cpp:197-206). The message is
+// the reference's, word for word, with this backend's name: memory_estimate (8 bytes
+// per complex) and engine_memory_estimate (the reference engine's 3 N^2 x 16 B). The
+// reference computes engine_memory_estimate inside the message, so above 29 qubits
+// that call's ArgumentError is what a refused circuit raises (unitary_backend.cpp:170-172).
 void check_guard(const qsb_circuit* c, int guard) {
     if (c->n_qubits > guard) {
+        if (c->n_qubits > 29) raise(QSB_ERR_ARGUMENT, "engine_memory_estimate: qubit count must be in [1, 29]");
         const uint64_t est = qsb_memory_estimate(c->n_qubits, 0);
         char a[32], b[32];
         format_bytes(est, a, sizeof a);
-        format_bytes(c->n_qubits <= 29 ? engine_bytes(c->n_qubits) : ~uint64_t{0}, b, sizeof b);
+        format_bytes(qsb_engine_memory_estimate(c->n_qubits, 0), b, sizeof b);
         raise(QSB_ERR_RESOURCE,
               "unitary-b200 backend refuses %d qubits (guard %d): estimated memory %llu bytes (%s at 8 bytes per "
-              "complex; engine-accurate %s in HBM)",
+              "complex; engine-accurate %s)",
               c->n_qubits, guard, static_cast<unsigned long long>(est), a, b);
     }
     check_reset_placement(c);
@@ -315,7 +321,15 @@ struct qsb_plan {
     bool timing = false;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     bool timed_run = false;
+    bool per_gemm = false;              // timing mode 2: an event pair around every K2 launch
+    std::vector<cudaEvent_t> gev;       // [2 * gemms] (mode 2)
+    std::vector<int32_t> gemm_kind;     // per K2 launch: bit 0 real layer, bit 1 materialised, bit 2 4M
     qsb_plan_info info{};
+};
+
+struct qsb_comm {
+    void* comm = nullptr;  // ncclComm_t
+    int n_ranks = 1, rank = 0, device = 0;
 };
 
 namespace {
@@ -368,18 +382,25 @@ void upload_tables(qsb_plan* p, const qsb_circuit* c) {
     if (total == 0) return;
     p->b.tables.ensure(total * sizeof(double));
     double* base = p->b.tables.as<double>();
+    // On the plan's stream (non-blocking): a legacy-stream cudaMemcpy would not be
+    // ordered before the K1 / K2 launches on dc->stream that read the tables.
+    // Pageable sources are staged by the call itself, so the vectors may go out of scope.
+    cudaStream_t s = p->dc->stream;
     for (int f : p->cc.used_functions) {
         const qsb_function& fn = c->functions[f];
         const size_t d = static_cast<size_t>(fn.dim);
         if (mono[f]) {
-            cuda_check(cudaMemcpy(base + off[f], vre[f].data(), d * 8, cudaMemcpyHostToDevice), "upload function");
-            cuda_check(cudaMemcpy(base + off[f] + d, vim[f].data(), d * 8, cudaMemcpyHostToDevice), "upload function");
-            cuda_check(cudaMemcpy(base + off[f] + 2 * d, cols[f].data(), d * 4, cudaMemcpyHostToDevice),
+            cuda_check(cudaMemcpyAsync(base + off[f], vre[f].data(), d * 8, cudaMemcpyHostToDevice, s),
+                       "upload function");
+            cuda_check(cudaMemcpyAsync(base + off[f] + d, vim[f].data(), d * 8, cudaMemcpyHostToDevice, s),
+                       "upload function");
+            cuda_check(cudaMemcpyAsync(base + off[f] + 2 * d, cols[f].data(), d * 4, cudaMemcpyHostToDevice, s),
                        "upload function");
         } else {
             const size_t d2 = d * d;
-            cuda_check(cudaMemcpy(base + off[f], fn.re, d2 * 8, cudaMemcpyHostToDevice), "upload function");
-            cuda_check(cudaMemcpy(base + off[f] + d2, fn.im, d2 * 8, cudaMemcpyHostToDevice), "upload function");
+            cuda_check(cudaMemcpyAsync(base + off[f], fn.re, d2 * 8, cudaMemcpyHostToDevice, s), "upload function");
+            cuda_check(cudaMemcpyAsync(base + off[f] + d2, fn.im, d2 * 8, cudaMemcpyHostToDevice, s),
+                       "upload function");
         }
     }
     auto patch = [&](qsb::LayerDesc& d) {
@@ -739,8 +760,10 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
         const bool three = p->tile == qsb::kTileWs3M || p->tile == qsb::kTileWs3MS;
         in.n_real_gemms = 0;
         in.gemm_hw_flops = 0.0;
+        p->gemm_kind.assign(p->chain.size(), 0);
         for (size_t i = 1; i < p->chain.size() && !p->small; ++i) {
             const bool real = p->real_ok && p->chain[i].real != 0;
+            p->gemm_kind[i] = (real ? 1 : 0) | (p->mat[i] ? 2 : 0) | (!three ? 4 : 0);
             in.n_real_gemms += real ? 1 : 0;
             in.gemm_hw_flops += (real ? 4.0 : (three ? 6.0 : 8.0)) * mn2;
         }
@@ -755,6 +778,8 @@ void release_plan(std::unique_ptr<qsb_plan>& p) {
     DeviceScope ds(p->dc->device);
     if (p->graph) cudaGraphExecDestroy(p->graph);
     for (auto& e : p->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : p->gev)
         if (e) cudaEventDestroy(e);
     if (p->borrowed) p->dc->cache = std::move(p->b);
     p.reset();
@@ -809,7 +834,10 @@ void enqueue(qsb_plan* p, cudaStream_t s) {
         a.tmap_b_real = &p->tmap_b_real;
         a.splits = p->splits;
         a.sk = p->sk;  // flags start at zero and every owner re-arms its own (no memset between GEMMs)
+        const bool gt = ev && p->per_gemm;
+        if (gt) cuda_check(cudaEventRecord(p->gev[2 * (i - 1)], s), "event");
         cuda_check(qsb::launch_zgemm(a, p->tile, p->h->gemm_mode, s), "zgemm_gen_kernel");
+        if (gt) cuda_check(cudaEventRecord(p->gev[2 * (i - 1) + 1], s), "event");
         cur ^= 1;
     }
     if (ev) cuda_check(cudaEventRecord(p->ev[2], s), "event");
@@ -833,6 +861,10 @@ void execute(qsb_plan* p, cudaStream_t s, bool allow_graph) {
     if (p->timing) {
         for (auto& e : p->ev)
             if (!e) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+        if (p->per_gemm && p->gev.empty() && p->chain.size() > 1) {
+            p->gev.assign(2 * (p->chain.size() - 1), nullptr);
+            for (auto& e : p->gev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+        }
     }
     if (!use_graph) {
         enqueue(p, s);
@@ -910,7 +942,18 @@ qsb_status qsb_create(const qsb_options* options, qsb_handle** out) {
             min_mem = (min_mem == 0.0) ? mem : std::min(min_mem, mem);
             auto dc = std::make_unique<DeviceCtx>();
             dc->device = id;
-            cuda_check(cudaStreamCreateWithFlags(&dc->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            // One stream per physical device: shards repeated on one GPU ("virtual shards")
+            // run one after the other. Two stream-K GEMMs (persistent grids sized to the SM
+            // count, owners spinning on contributors) running concurrently on one device
+            // could each be partly resident and wait on each other forever.
+            for (const auto& prev : h->devs)
+                if (prev->device == id) {
+                    dc->stream = prev->stream;
+                    dc->owns_stream = false;
+                    break;
+                }
+            if (dc->owns_stream)
+                cuda_check(cudaStreamCreateWithFlags(&dc->stream, cudaStreamNonBlocking), "cudaStreamCreate");
             h->devs.push_back(std::move(dc));
         }
         // HBM-derived default guard: each device's row block of both V buffers
@@ -936,14 +979,17 @@ qsb_status qsb_create(const qsb_options* options, qsb_handle** out) {
     });
 }
 
+static void release_comms(qsb_handle* h);
+
 qsb_status qsb_destroy(qsb_handle* h) {
     return guarded([&] {
         if (!h) return;
         {
             std::lock_guard<std::mutex> lk(h->mu);
+            release_comms(h);
             for (auto& dc : h->devs) {
                 DeviceScope ds(dc->device);
-                if (dc->stream) cudaStreamDestroy(dc->stream);
+                if (dc->stream && dc->owns_stream) cudaStreamDestroy(dc->stream);
                 dc->cache = Buffers{};
             }
         }
@@ -956,6 +1002,60 @@ qsb_status qsb_qubit_guard(const qsb_handle* h, int32_t* guard) {
         if (!h || !guard) raise(QSB_ERR_ARGUMENT, "null argument");
         *guard = h->guard;
     });
+}
+
+// The handle's NCCL communicator over devs[0 .. G) (distinct devices), built
+// once with ncclCommInitAll and kept until a call needs a different G.
+static void release_comms(qsb_handle* h) {
+    if (h->nccl_ranks == 0) return;
+    for (auto& dc : h->devs)
+        if (dc->nccl_comm) {
+            DeviceScope ds(dc->device);
+            nccl().comm_destroy(static_cast<ncclComm_t>(dc->nccl_comm));
+            dc->nccl_comm = nullptr;
+        }
+    h->nccl_ranks = 0;
+}
+
+static void ensure_comms(qsb_handle* h, int G) {
+    if (h->nccl_ranks == G) return;
+    const NcclApi& nc = nccl_or_raise();
+    release_comms(h);
+    std::vector<int> ids(G);
+    for (int g = 0; g < G; ++g) ids[g] = h->devs[g]->device;
+    std::vector<ncclComm_t> comms(G, nullptr);
+    nccl_check(nc.comm_init_all(comms.data(), G, ids.data()), "ncclCommInitAll");
+    for (int g = 0; g < G; ++g) h->devs[g]->nccl_comm = comms[g];
+    h->nccl_ranks = G;
+}
+
+// ncclAllGather of the shards' psi rows (re and im planes) into devs[g]->gathered on
+// every device, one group call from this thread (single-thread multi-device NCCL).
+static void allgather_psi(qsb_handle* h, const std::vector<std::unique_ptr<qsb_plan>>& plans, int64_t N,
+                          int64_t rows) {
+    const int G = static_cast<int>(plans.size());
+    ensure_comms(h, G);
+    const NcclApi& nc = nccl_or_raise();
+    for (int g = 0; g < G; ++g) {
+        DeviceScope ds(h->devs[g]->device);
+        h->devs[g]->gathered.ensure(2 * static_cast<size_t>(N) * 8);
+    }
+    nccl_check(nc.group_start(), "ncclGroupStart");
+    ncclResult_t first = ncclSuccess;
+    for (int g = 0; g < G && first == ncclSuccess; ++g) {
+        const qsb_plan* p = plans[g].get();
+        DeviceCtx& dc = *h->devs[g];
+        DeviceScope ds(dc.device);
+        const double* src = p->b.psi.as<double>() + (p->row_begin - p->eff_begin);
+        double* dst = dc.gathered.as<double>();
+        auto comm = static_cast<ncclComm_t>(dc.nccl_comm);
+        first = nc.all_gather(src, dst, static_cast<size_t>(rows), ncclFloat64, comm, dc.stream);
+        if (first == ncclSuccess)
+            first = nc.all_gather(src + p->M, dst + N, static_cast<size_t>(rows), ncclFloat64, comm, dc.stream);
+    }
+    const ncclResult_t end = nc.group_end();
+    nccl_check(first, "ncclAllGather (psi rows)");
+    nccl_check(end, "ncclGroupEnd");
 }
 
 // Host-API execution: the row blocks of U over the handle's devices (one block
@@ -976,6 +1076,14 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
         G = p2;
     }
     const int64_t rows = N / G;
+    // psi is all-gathered over NCCL (north star) whenever the shards sit on distinct
+    // devices; repeated ids (virtual shards) cannot form a communicator.
+    bool distinct = true;
+    for (int a = 0; a < G; ++a)
+        for (int b = a + 1; b < G; ++b) distinct = distinct && h->devs[a]->device != h->devs[b]->device;
+    const bool use_nccl = psi_re && !(h->flags & QSB_FLAG_COLUMN_BLOCKS) && distinct &&
+                          (G > 1 || (h->flags & QSB_FLAG_NCCL_GATHER));
+    double* gathered_host = nullptr;
     std::vector<std::unique_ptr<qsb_plan>> plans(G);
     std::vector<double*> staged(G, nullptr);
     std::vector<std::vector<double>> vt(G);  // column blocks: V = U[:, cols]^T on the host
@@ -1003,6 +1111,8 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
             if (psi_re && p->columns) {
                 // column blocks: every shard returns a full-length share of psi, summed below
                 staged[g] = static_cast<double*>(p->dc->stage_out(2 * static_cast<size_t>(N) * 8));
+            } else if (use_nccl) {
+                // rows stay on the device for the all-gather below
             } else if (psi_re && p->small) {
                 // the one-CTA kernel writes psi straight into pinned staging (mapped): no copy call
                 staged[g] = static_cast<double*>(p->dc->stage_out(2 * static_cast<size_t>(p->M) * 8));
@@ -1018,6 +1128,7 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
                 if (psi_re)
                     cuda_check(cudaMemcpyAsync(staged[g], p->b.psi.p, 2 * static_cast<size_t>(N) * 8,
                                                cudaMemcpyDeviceToHost, s), "download psi");
+            } else if (use_nccl) {
             } else if (mapped_psi) {
                 // written by the kernel; read after the stream synchronisation below
             } else if (psi_re && p->M <= 65536) {
@@ -1048,6 +1159,15 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
                 cuda_check(cudaMemcpyAsync(u_im + p->row_begin * N, v + plane + off * N, rows * N * 8,
                                            cudaMemcpyDeviceToHost, s), "download U");
             }
+        }
+        if (use_nccl) {
+            allgather_psi(h, plans, N, rows);
+            // every device now holds all of psi; read device 0's copy
+            DeviceCtx& d0 = *h->devs[0];
+            DeviceScope ds(d0.device);
+            gathered_host = static_cast<double*>(d0.stage_out(2 * static_cast<size_t>(N) * 8));
+            cuda_check(cudaMemcpyAsync(gathered_host, d0.gathered.p, 2 * static_cast<size_t>(N) * 8,
+                                       cudaMemcpyDeviceToHost, d0.stream), "download psi");
         }
         const auto t2 = now();
         for (int g = 0; g < G; ++g) {
@@ -1080,6 +1200,10 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
                     }
                 std::vector<double>().swap(vt[g]);
             }
+        }
+        if (gathered_host) {
+            std::memcpy(psi_re, gathered_host, N * 8);
+            std::memcpy(psi_im, gathered_host + N, N * 8);
         }
         if (trace) {
             const auto t3 = now();
@@ -1279,6 +1403,9 @@ qsb_status qsb_plan_create(qsb_handle* h, const qsb_circuit* c, int64_t row_begi
     return guarded([&] {
         if (!h || !out) raise(QSB_ERR_ARGUMENT, "null argument");
         *out = nullptr;
+        // under the handle lock: make_plan writes the device's pinned staging, which a
+        // concurrent host call on this handle may be reading (small plans map it)
+        std::lock_guard<std::mutex> lk(h->mu);
         std::unique_ptr<qsb_plan> p = make_plan(h, &h->dev0(), c, row_begin, row_count, false);
         *out = p.release();
     });
@@ -1301,7 +1428,9 @@ qsb_status qsb_plan_get_info(const qsb_plan* plan, qsb_plan_info* info) {
 qsb_status qsb_plan_set_timing(qsb_plan* plan, int32_t enable) {
     return guarded([&] {
         if (!plan) raise(QSB_ERR_ARGUMENT, "null argument");
+        if (enable < 0 || enable > 2) raise(QSB_ERR_ARGUMENT, "timing mode %d not in {0, 1, 2}", enable);
         plan->timing = enable != 0;
+        plan->per_gemm = enable == 2;
     });
 }
 
@@ -1387,6 +1516,106 @@ qsb_status qsb_plan_last_timing(qsb_plan* plan, double* total_ms, double* gemm_m
     });
 }
 
+// ------------------------------------------------------------------ NCCL (one process per GPU)
+
+qsb_status qsb_nccl_unique_id(void* id_out) {
+    return guarded([&] {
+        if (!id_out) raise(QSB_ERR_ARGUMENT, "null argument");
+        static_assert(sizeof(ncclUniqueId) == QSB_NCCL_ID_BYTES, "ncclUniqueId size");
+        ncclUniqueId id;
+        nccl_check(nccl_or_raise().get_unique_id(&id), "ncclGetUniqueId");
+        std::memcpy(id_out, &id, sizeof id);
+    });
+}
+
+qsb_status qsb_nccl_version(int32_t* version) {
+    return guarded([&] {
+        if (!version) raise(QSB_ERR_ARGUMENT, "null argument");
+        *version = nccl_or_raise().version;
+    });
+}
+
+qsb_status qsb_comm_create(qsb_handle* h, const void* id, int32_t n_ranks, int32_t rank, qsb_comm** out) {
+    return guarded([&] {
+        if (!h || !id || !out) raise(QSB_ERR_ARGUMENT, "null argument");
+        *out = nullptr;
+        if (n_ranks < 1 || rank < 0 || rank >= n_ranks)
+            raise(QSB_ERR_ARGUMENT, "rank %d out of range for %d ranks", rank, n_ranks);
+        const NcclApi& nc = nccl_or_raise();
+        auto c = std::make_unique<qsb_comm>();
+        c->n_ranks = n_ranks;
+        c->rank = rank;
+        c->device = h->dev0().device;
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof uid);
+        DeviceScope ds(c->device);
+        ncclComm_t comm = nullptr;
+        nccl_check(nc.comm_init_rank(&comm, n_ranks, uid, rank), "ncclCommInitRank");
+        c->comm = comm;
+        *out = c.release();
+    });
+}
+
+qsb_status qsb_comm_destroy(qsb_comm* comm) {
+    return guarded([&] {
+        if (!comm) return;
+        std::unique_ptr<qsb_comm> c(comm);
+        if (c->comm) {
+            DeviceScope ds(c->device);
+            nccl_check(nccl_or_raise().comm_destroy(static_cast<ncclComm_t>(c->comm)), "ncclCommDestroy");
+        }
+    });
+}
+
+qsb_status qsb_plan_allgather_state(const qsb_plan* plan, qsb_comm* comm, double* psi_re, double* psi_im,
+                                    void* stream) {
+    return guarded([&] {
+        if (!plan || !comm || !psi_re || !psi_im) raise(QSB_ERR_ARGUMENT, "null argument");
+        if (plan->columns) raise(QSB_ERR_ARGUMENT, "all-gather needs row-block plans (column shares are summed)");
+        if (plan->dc->device != comm->device)
+            raise(QSB_ERR_ARGUMENT, "plan on device %d, communicator on device %d", plan->dc->device, comm->device);
+        const int64_t N = plan->N;
+        if (plan->row_count * comm->n_ranks != N || plan->row_begin != comm->rank * plan->row_count)
+            raise(QSB_ERR_ARGUMENT, "rank %d of %d must own rows [%lld, +%lld); the plan owns [%lld, +%lld)",
+                  comm->rank, comm->n_ranks, static_cast<long long>(comm->rank * (N / comm->n_ranks)),
+                  static_cast<long long>(N / comm->n_ranks), static_cast<long long>(plan->row_begin),
+                  static_cast<long long>(plan->row_count));
+        const NcclApi& nc = nccl_or_raise();
+        DeviceScope ds(plan->dc->device);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->dc->stream;
+        const double* src = psi_rows(plan);
+        auto c = static_cast<ncclComm_t>(comm->comm);
+        const size_t rows = static_cast<size_t>(plan->row_count);
+        nccl_check(nc.group_start(), "ncclGroupStart");
+        ncclResult_t r = nc.all_gather(src, psi_re, rows, ncclFloat64, c, s);
+        if (r == ncclSuccess) r = nc.all_gather(src + plan->M, psi_im, rows, ncclFloat64, c, s);
+        const ncclResult_t end = nc.group_end();
+        nccl_check(r, "ncclAllGather (psi rows)");
+        nccl_check(end, "ncclGroupEnd");
+    });
+}
+
+qsb_status qsb_plan_gemm_times(qsb_plan* plan, double* ms, int32_t* kinds, int32_t cap, int32_t* count) {
+    return guarded([&] {
+        if (!plan || !count) raise(QSB_ERR_ARGUMENT, "null argument");
+        if (!plan->per_gemm || !plan->timed_run || plan->small)
+            raise(QSB_ERR_ARGUMENT, "no per-GEMM timed execute on this plan (qsb_plan_set_timing mode 2, tiled path)");
+        const int G = static_cast<int>(plan->chain.size()) - 1;
+        *count = G;
+        if (G <= 0) return;
+        DeviceScope ds(plan->dc->device);
+        cuda_check(cudaEventSynchronize(plan->gev.back()), "cudaEventSynchronize");
+        for (int i = 0; i < G && i < cap; ++i) {
+            if (ms) {
+                float t = 0;
+                cuda_check(cudaEventElapsedTime(&t, plan->gev[2 * i], plan->gev[2 * i + 1]), "cudaEventElapsedTime");
+                ms[i] = t;
+            }
+            if (kinds) kinds[i] = plan->gemm_kind[i + 1];
+        }
+    });
+}
+
 uint64_t qsb_memory_estimate(int32_t n_qubits, int32_t kind) {
     // unitary_backend.cpp:156-166 (8 bytes per complex, the paper's accounting)
     if (n_qubits < 1 || n_qubits > 30) return 0;
@@ -1395,9 +1624,17 @@ uint64_t qsb_memory_estimate(int32_t n_qubits, int32_t kind) {
 }
 
 uint64_t qsb_engine_memory_estimate(int32_t n_qubits, int32_t kind) {
-    // this engine: two 2^n x 2^n complex buffers (V, V') + psi0 + psi, 16 bytes per complex
+    // engine_memory_estimate (unitary_backend.cpp:168-179): the reference engine's
+    // accounting, 3 N^2 complex doubles (identity, step operator, product) + N
     if (n_qubits < 1 || n_qubits > 29) return 0;
-    return kind == 0 ? engine_bytes(n_qubits) : (uint64_t{1} << n_qubits) * 16;
+    const uint64_t dim = uint64_t{1} << n_qubits;
+    return kind == 0 ? 3 * dim * dim * 16 + dim * 16 : dim * 16;
+}
+
+uint64_t qsb_hbm_footprint(int32_t n_qubits) {
+    // this library on one device: two V buffers of 2^n x 2^n complex doubles + psi0 + psi
+    if (n_qubits < 1 || n_qubits > 29) return 0;
+    return engine_bytes(n_qubits);
 }
 
 }  // extern "C"

@@ -633,7 +633,8 @@ std::unique_ptr<qsb_sv_plan> make_sv_plan(qsb_handle* h, DeviceCtx* dc, const qs
             size_t off = 0;
             auto put = [&](const void* src, size_t nbytes) {
                 char* dst = base + off;
-                if (nbytes) cuda_check(cudaMemcpy(dst, src, nbytes, cudaMemcpyHostToDevice), "upload function");
+                if (nbytes)  // on the plan stream: ordered before the passes that read the tables
+                    cuda_check(cudaMemcpyAsync(dst, src, nbytes, cudaMemcpyHostToDevice, dc->stream), "upload function");
                 off += (nbytes + 15) & ~size_t{15};
                 return dst;
             };
@@ -868,6 +869,7 @@ qsb_status qsb_sv_plan_create(qsb_handle* h, const qsb_circuit* c, int32_t mode,
     return guarded([&] {
         if (!h || !out) raise(QSB_ERR_ARGUMENT, "null argument");
         *out = nullptr;
+        std::lock_guard<std::mutex> lk(h->mu);  // make_sv_plan writes the device's pinned staging
         std::unique_ptr<qsb_sv_plan> p = make_sv_plan(h, &h->dev0(), c, mode, col_begin, col_count, false);
         *out = p.release();
     });

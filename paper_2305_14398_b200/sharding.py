@@ -4,7 +4,10 @@ Rank r owns rows [r*B, r*B + B) of U = L_last ... L_first. It computes
 V = L_last[rows, :] and then V <- V * L for every further layer, regenerating
 each operator tile locally from the replicated descriptor — no communication
 during the chain. The only exchange is the final all-gather of the psi row
-slices (16 * B bytes per rank) with NCCL (gloo on CPU for the host tests).
+slices (16 * B bytes per rank): ``dist.all_gather_into_tensor`` over NCCL on
+GPUs, and the very same call over gloo in the CPU tests. (The C ABI has its own
+NCCL all-gather for C++ hosts and the in-process multi-device handle:
+qsb_plan_allgather_state / qsb_simulate_full_state with n_devices > 1.)
 """
 from __future__ import annotations
 
@@ -32,32 +35,32 @@ def row_shard(N: int, world: int, rank: int) -> Tuple[int, int]:
 
 def gather_rows(local_re, local_im, N: int, world: int):
     """All-gather equal row blocks (padded to block_rows) into full psi planes.
-    Works for CUDA tensors over NCCL and CPU tensors over gloo."""
+    One code path for every backend: each rank contributes a flat [re | im]
+    buffer of 2 * block_rows doubles, gathered rank-major into one flat tensor
+    (CUDA tensors over NCCL, CPU tensors over gloo)."""
     import torch
     import torch.distributed as dist
 
     b = block_rows(N, world)
-    local = torch.zeros(2, b, dtype=local_re.dtype, device=local_re.device)
+    local = torch.zeros(2 * b, dtype=local_re.dtype, device=local_re.device)
     n = local_re.numel()
     if n:
-        local[0, :n].copy_(local_re)
-        local[1, :n].copy_(local_im)
-    if dist.get_backend() == "nccl":
-        out = torch.empty(world, 2, b, dtype=local.dtype, device=local.device)
-        dist.all_gather_into_tensor(out, local)
-    else:
-        parts = [torch.empty_like(local) for _ in range(world)]
-        dist.all_gather(parts, local)
-        out = torch.stack(parts)
-    full = out.permute(1, 0, 2).reshape(2, world * b)[:, :N]
+        local[:n].copy_(local_re)
+        local[b:b + n].copy_(local_im)
+    out = torch.empty(world * 2 * b, dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, local)
+    full = out.view(world, 2, b).permute(1, 0, 2).reshape(2, world * b)[:, :N]
     return full[0], full[1]
 
 
 def gather_state(plan, psi_re, psi_im, begin: int, count: int, world: int, stream: int = 0) -> None:
     """Fill psi_re/psi_im (length N, CUDA) with the full state: the local plan's
-    rows, all-gathered across ranks when world > 1."""
+    rows, all-gathered across ranks when world > 1. Row-block plans only: a
+    column-block plan's state is a full-length share that must be summed."""
     import torch
 
+    if plan is not None and getattr(plan, "columns", False):
+        raise ValueError("gather_state needs row-block plans; column-block shares are summed, not gathered")
     N = psi_re.numel()
     if world == 1:
         plan.copy_state(psi_re.data_ptr(), psi_im.data_ptr(), stream)

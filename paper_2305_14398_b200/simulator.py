@@ -15,7 +15,7 @@ import numpy as np
 
 from . import native
 from .circuit import Circuit, GateRegistry
-from .errors import LookupError_
+from .errors import LookupError_, ShapeError
 
 BACKEND_ID = "unitary-b200"
 FSV_BACKEND_ID = "fsv-b200"
@@ -81,13 +81,29 @@ class Plan:
     def __init__(self, sim: "B200UnitarySimulator", flat: native.FlatCircuit, row_begin: int, row_count: int):
         self._flat = flat
         self._sim = sim
+        self.columns = bool(sim.flags & native.FLAG_COLUMN_BLOCKS)
         self._p = ctypes.c_void_p()
         native.check(native.lib().qsb_plan_create(sim._h, flat.ptr, row_begin, row_count, ctypes.byref(self._p)))
         self.info = native.QsbPlanInfo()
         native.check(native.lib().qsb_plan_get_info(self._p, ctypes.byref(self.info)))
 
-    def set_timing(self, enable: bool) -> None:
-        native.check(native.lib().qsb_plan_set_timing(self._p, 1 if enable else 0))
+    def set_timing(self, enable) -> None:
+        """False/0 off, True/1 phase events, 2 also an event pair around every K2 launch."""
+        native.check(native.lib().qsb_plan_set_timing(self._p, int(enable)))
+
+    def gemm_times(self) -> Tuple[List[float], List[int]]:
+        """Per-K2-launch ms and kind bits (1 real, 2 materialised, 4 4M) of the last mode-2 execute."""
+        count = ctypes.c_int32()
+        native.check(native.lib().qsb_plan_gemm_times(self._p, None, None, 0, ctypes.byref(count)))
+        ms = np.zeros(max(count.value, 1))
+        kinds = np.zeros(max(count.value, 1), dtype=np.int32)
+        native.check(native.lib().qsb_plan_gemm_times(self._p, native.dptr(ms), native.dptr(kinds), count.value,
+                                                      ctypes.byref(count)))
+        return ms[:count.value].tolist(), kinds[:count.value].tolist()
+
+    def allgather_state(self, comm: "Comm", dst_re_ptr: int, dst_im_ptr: int, stream: int = 0) -> None:
+        """ncclAllGather of every rank's psi rows into full-length device planes (qsb_plan_allgather_state)."""
+        native.check(native.lib().qsb_plan_allgather_state(self._p, comm._c, dst_re_ptr, dst_im_ptr, stream or None))
 
     def set_initial_state(self, re_ptr: int, im_ptr: int, stream: int = 0) -> None:
         native.check(native.lib().qsb_plan_set_initial_state(self._p, re_ptr, im_ptr, stream or None))
@@ -125,6 +141,55 @@ class Plan:
             pass
 
 
+def _state_planes(re, im, dim: Optional[int] = None) -> Tuple[np.ndarray, np.ndarray]:
+    """Contiguous float64 re/im planes of equal length (= dim when given). The C ABI
+    carries no lengths, so a short plane would be a host out-of-bounds read: raise
+    ShapeError like the reference's matvec (linalg.cpp:89-94) instead."""
+    re = np.ascontiguousarray(re, dtype=np.float64).reshape(-1)
+    im = np.ascontiguousarray(im, dtype=np.float64).reshape(-1)
+    if len(re) != len(im):
+        raise ShapeError(f"state planes differ in length: {len(re)} real vs {len(im)} imaginary")
+    if dim is not None and len(re) != dim:
+        raise ShapeError(f"matvec: {dim}x{dim} times vector of length {len(re)}")
+    return re, im
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through libqsb (rank 0; broadcast the bytes to the other ranks)."""
+    buf = ctypes.create_string_buffer(native.NCCL_ID_BYTES)
+    native.check(native.lib().qsb_nccl_unique_id(buf))
+    return buf.raw
+
+
+def nccl_version() -> int:
+    v = ctypes.c_int32()
+    native.check(native.lib().qsb_nccl_version(ctypes.byref(v)))
+    return v.value
+
+
+class Comm:
+    """An NCCL communicator of one process per GPU (qsb_comm_create on the handle's device)."""
+
+    def __init__(self, sim: "B200UnitarySimulator", unique_id: bytes, n_ranks: int, rank: int) -> None:
+        if len(unique_id) != native.NCCL_ID_BYTES:
+            raise ValueError("an NCCL unique id has 128 bytes")
+        self._id = ctypes.create_string_buffer(unique_id, native.NCCL_ID_BYTES)
+        self._c = ctypes.c_void_p()
+        native.check(native.lib().qsb_comm_create(sim._h, self._id, n_ranks, rank, ctypes.byref(self._c)))
+        self.n_ranks, self.rank = n_ranks, rank
+
+    def close(self) -> None:
+        if self._c:
+            native.check(native.lib().qsb_comm_destroy(self._c))
+            self._c = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class B200UnitarySimulator(Simulator):
     """The drop-in backend: Algorithm 1 on B200 (unitary_backend.cpp:194-215)."""
 
@@ -143,6 +208,7 @@ class B200UnitarySimulator(Simulator):
         native.check(L.qsb_qubit_guard(self._h, ctypes.byref(g)))
         self._guard = g.value
         self.device = device
+        self.flags = flags
 
     def name(self) -> str:
         return BACKEND_ID
@@ -165,8 +231,7 @@ class B200UnitarySimulator(Simulator):
     def simulate_from_state(self, circuit, registry, psi0_re: np.ndarray, psi0_im: np.ndarray) -> StateVector:
         flat = self._flat(circuit, registry)
         N = 1 << flat.n_qubits
-        r0 = np.ascontiguousarray(psi0_re, dtype=np.float64)
-        i0 = np.ascontiguousarray(psi0_im, dtype=np.float64)
+        r0, i0 = _state_planes(psi0_re, psi0_im, N)
         re = np.empty(N)
         im = np.empty(N)
         native.check(native.lib().qsb_simulate_from_state(self._h, flat.ptr, native.dptr(r0), native.dptr(i0),
@@ -198,8 +263,7 @@ class B200UnitarySimulator(Simulator):
         return re, im
 
     def probabilities(self, re: np.ndarray, im: np.ndarray) -> Tuple[np.ndarray, float]:
-        re = np.ascontiguousarray(re, dtype=np.float64)
-        im = np.ascontiguousarray(im, dtype=np.float64)
+        re, im = _state_planes(re, im)
         p = np.empty(len(re))
         norm = ctypes.c_double()
         native.check(native.lib().qsb_probabilities(self._h, native.dptr(re), native.dptr(im), len(re),
@@ -320,8 +384,7 @@ class B200FsvSimulator(_HandleOwner):
     def simulate_from_state(self, circuit, registry, psi0_re: np.ndarray, psi0_im: np.ndarray) -> StateVector:
         flat = self._flat(circuit, registry)
         N = 1 << flat.n_qubits
-        r0 = np.ascontiguousarray(psi0_re, dtype=np.float64)
-        i0 = np.ascontiguousarray(psi0_im, dtype=np.float64)
+        r0, i0 = _state_planes(psi0_re, psi0_im, N)
         re = np.empty(N)
         im = np.empty(N)
         native.check(native.lib().qsb_fsv_simulate_from_state(self._h, flat.ptr, native.dptr(r0), native.dptr(i0),
@@ -380,8 +443,7 @@ class B200StructuredUnitarySimulator(_HandleOwner):
 def _collapse_on(sim: "_HandleOwner", re: np.ndarray, im: np.ndarray, seed: int) -> int:
     """collapse (state.cpp:81-98) through qsb_collapse: K4 probabilities on the
     GPU, sequential inverse-CDF walk in the native runtime."""
-    re = np.ascontiguousarray(re, dtype=np.float64)
-    im = np.ascontiguousarray(im, dtype=np.float64)
+    re, im = _state_planes(re, im)
     idx = ctypes.c_uint64()
     native.check(native.lib().qsb_collapse(sim._h, native.dptr(re), native.dptr(im), len(re), ctypes.c_uint64(seed),
                                            ctypes.byref(idx)))

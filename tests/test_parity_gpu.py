@@ -137,6 +137,9 @@ def test_errors_match_reference(sim):
     with pytest.raises(q.ResourceError) as e:
         small.simulate_full_state(q.Circuit(4))
     assert "estimated memory 2176 bytes" in str(e.value)  # memory_estimate(4) (unitary_backend.cpp:156-166)
+    # the reference's message word for word (unitary_backend.cpp:197-205), this backend's name
+    assert str(e.value).endswith("unitary-b200 backend refuses 4 qubits (guard 3): estimated memory 2176 bytes "
+                                 "(2.18 kB at 8 bytes per complex; engine-accurate 12.54 kB)"), str(e.value)
     assert small.simulate_full_state(q.Circuit(3)).dimension() == 8
     small.close()
 

@@ -67,3 +67,41 @@ def test_gloo_row_gather_reassembles_psi(tmp_path, golden, world, case):
     got = np.load(out)
     re, im = golden.psi(case)
     assert np.array_equal(got[0], re) and np.array_equal(got[1], im)
+
+
+def _last_json(out: str):
+    import json
+
+    for line in reversed(out.strip().splitlines()):
+        if line.startswith("{"):
+            return json.loads(line)
+    raise AssertionError(f"no JSON line in:\n{out}")
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bench_entry_point_runs_world_ranks_over_gloo(world):
+    """`python bench.py --gpus N` re-executes itself under torch.distributed.run with
+    N ranks; --dry-run then drives the same rank checks, row_shard and gather_rows
+    (all_gather_into_tensor, the call NCCL runs on GPUs) over gloo."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--dry-run", "--gpus", str(world),
+                        "--workload", "qft-12"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    line = _last_json(r.stdout)
+    assert line["n_gpus"] == world and line["gathered_ok"] and line["backend"] == "gloo"
+
+
+def test_bench_refuses_more_gpus_than_visible():
+    """--gpus N with fewer visible GPUs fails loudly instead of timing one GPU."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    have = torch.cuda.device_count()
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", str(max(2, have + 1)), "--steps", "1",
+                        "--warmup", "1"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 2, r.stdout + r.stderr
+    assert "visible GPUs" in _last_json(r.stdout)["error"]
