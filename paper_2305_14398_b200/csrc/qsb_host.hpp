@@ -162,6 +162,16 @@ struct qsb_handle {
     int flags = 0;
     std::vector<std::unique_ptr<DeviceCtx>> devs;
     int nccl_ranks = 0;  // devices in the current NCCL communicator (devs[0 .. nccl_ranks)), 0 = none
+    // Host-API plan cache (qsb_runtime.cpp run_full): the last call's plans, one per
+    // row block, keyed by the circuit's structure; registry matrix contents are kept
+    // and compared on reuse. Any path that needs the devices' memory drops it first.
+    std::vector<qsb_plan*> cached;
+    std::vector<char> cache_key;
+    std::vector<std::vector<double>> cached_fn;  // [2 * function + plane] contents, used functions only
+    void (*drop_cache)(qsb_handle*) = nullptr;
+    void drop_plan_cache() {
+        if (drop_cache) drop_cache(this);
+    }
     std::mutex mu;
     DeviceCtx& dev0() { return *devs.front(); }
 };

@@ -673,16 +673,9 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
             o.pad = 0;
             std::memcpy(o.blocks, d.blocks, sizeof(qsb::BlockDesc) * static_cast<size_t>(d.nblocks));
         }
-        // A one-shot call (run_full) lets the kernel read the pinned staging in place
-        // (mapped host memory): no copy call. Plans that outlive the call upload.
-        void* mapped = nullptr;
-        // (K2s only: K2m fetches one descriptor per layer on its critical path.)
-        if (borrow_cache && N <= 64 && cudaHostGetDevicePointer(&mapped, st, 0) == cudaSuccess) {
-            p->small_layers_dev = mapped;
-        } else {
-            cudaGetLastError();
-            cuda_check(cudaMemcpyAsync(p->b.layers.p, st, bytes, cudaMemcpyHostToDevice, dc->stream), "upload layers");
-        }
+        // uploaded once: host-API plans are cached across calls (run_full), so the kernel
+        // must not read the pinned staging in place — the next plan reuses it
+        cuda_check(cudaMemcpyAsync(p->b.layers.p, st, bytes, cudaMemcpyHostToDevice, dc->stream), "upload layers");
         if (trace) {
             const auto t4 = tnow();
             auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
@@ -986,6 +979,7 @@ qsb_status qsb_destroy(qsb_handle* h) {
         if (!h) return;
         {
             std::lock_guard<std::mutex> lk(h->mu);
+            h->drop_plan_cache();
             release_comms(h);
             for (auto& dc : h->devs) {
                 DeviceScope ds(dc->device);
@@ -1031,7 +1025,7 @@ static void ensure_comms(qsb_handle* h, int G) {
 
 // ncclAllGather of the shards' psi rows (re and im planes) into devs[g]->gathered on
 // every device, one group call from this thread (single-thread multi-device NCCL).
-static void allgather_psi(qsb_handle* h, const std::vector<std::unique_ptr<qsb_plan>>& plans, int64_t N,
+static void allgather_psi(qsb_handle* h, const std::vector<qsb_plan*>& plans, int64_t N,
                           int64_t rows) {
     const int G = static_cast<int>(plans.size());
     ensure_comms(h, G);
@@ -1043,7 +1037,7 @@ static void allgather_psi(qsb_handle* h, const std::vector<std::unique_ptr<qsb_p
     nccl_check(nc.group_start(), "ncclGroupStart");
     ncclResult_t first = ncclSuccess;
     for (int g = 0; g < G && first == ncclSuccess; ++g) {
-        const qsb_plan* p = plans[g].get();
+        const qsb_plan* p = plans[g];
         DeviceCtx& dc = *h->devs[g];
         DeviceScope ds(dc.device);
         const double* src = p->b.psi.as<double>() + (p->row_begin - p->eff_begin);
@@ -1058,12 +1052,94 @@ static void allgather_psi(qsb_handle* h, const std::vector<std::unique_ptr<qsb_p
     nccl_check(end, "ncclGroupEnd");
 }
 
+// ---- host-API plan cache ----
+
+// Structure key of a host call: everything a plan compiles from except the registry
+// matrices' contents (kept separately): qubits, step packing, every qsb_op (gate
+// values included), function dimensions, the row-block count and the handle flags.
+static std::vector<char> plan_key(const qsb_circuit* c, int G, int flags) {
+    std::vector<char> k;
+    auto put = [&](const void* p, size_t n) {
+        const char* b = static_cast<const char*>(p);
+        k.insert(k.end(), b, b + n);
+    };
+    const int32_t head[4] = {c->n_qubits, c->n_steps, G, flags};
+    put(head, sizeof head);
+    if (c->n_steps > 0) {
+        put(c->step_offsets, sizeof(int32_t) * (static_cast<size_t>(c->n_steps) + 1));
+        const int n_ops = c->step_offsets[c->n_steps] - c->step_offsets[0];
+        put(c->ops + c->step_offsets[0], sizeof(qsb_op) * static_cast<size_t>(std::max(n_ops, 0)));
+    }
+    put(&c->n_functions, sizeof c->n_functions);
+    for (int f = 0; f < c->n_functions; ++f) put(&c->functions[f].dim, sizeof(int64_t));
+    return k;
+}
+
+static std::vector<char> used_function_mask(const qsb_circuit* c) {
+    std::vector<char> used(static_cast<size_t>(std::max(c->n_functions, 0)), 0);
+    if (c->n_steps > 0)
+        for (int i = c->step_offsets[0]; i < c->step_offsets[c->n_steps]; ++i)
+            if (c->ops[i].kind == QSB_OP_FUNCTION) used[c->ops[i].function] = 1;
+    return used;
+}
+
+static void keep_functions(qsb_handle* h, const qsb_circuit* c) {
+    const std::vector<char> used = used_function_mask(c);
+    h->cached_fn.assign(2 * used.size(), {});
+    for (size_t f = 0; f < used.size(); ++f) {
+        if (!used[f]) continue;
+        const size_t d2 = static_cast<size_t>(c->functions[f].dim) * static_cast<size_t>(c->functions[f].dim);
+        h->cached_fn[2 * f].assign(c->functions[f].re, c->functions[f].re + d2);
+        h->cached_fn[2 * f + 1].assign(c->functions[f].im, c->functions[f].im + d2);
+    }
+}
+
+// Registry matrices equal to the kept copies? Large ones are compared on several
+// host threads (this runs while the reused plans execute on the GPU).
+static bool functions_unchanged(const qsb_handle* h, const qsb_circuit* c) {
+    const std::vector<char> used = used_function_mask(c);
+    if (h->cached_fn.size() != 2 * used.size()) return false;
+    for (size_t f = 0; f < used.size(); ++f) {
+        if (!used[f]) continue;
+        for (int plane = 0; plane < 2; ++plane) {
+            const std::vector<double>& kept = h->cached_fn[2 * f + plane];
+            const double* now = plane ? c->functions[f].im : c->functions[f].re;
+            const size_t n = kept.size();
+            const size_t workers =
+                n >= (size_t{1} << 18) ? std::min<size_t>(16, std::max(1u, std::thread::hardware_concurrency())) : 1;
+            if (workers <= 1) {
+                if (std::memcmp(kept.data(), now, n * 8) != 0) return false;
+                continue;
+            }
+            std::vector<char> ok(workers, 1);
+            std::vector<std::thread> pool;
+            for (size_t w = 0; w < workers; ++w)
+                pool.emplace_back([&, w] {
+                    const size_t b = n * w / workers, e = n * (w + 1) / workers;
+                    ok[w] = std::memcmp(kept.data() + b, now + b, (e - b) * 8) == 0;
+                });
+            for (auto& t : pool) t.join();
+            if (!std::all_of(ok.begin(), ok.end(), [](char v) { return v != 0; })) return false;
+        }
+    }
+    return true;
+}
+
+static void drop_plan_cache(qsb_handle* h) {
+    for (qsb_plan* raw : h->cached) {
+        std::unique_ptr<qsb_plan> p(raw);
+        release_plan(p);
+    }
+    h->cached.clear();
+    h->cache_key.clear();
+    h->cached_fn.clear();
+}
+
 // Host-API execution: the row blocks of U over the handle's devices (one block
 // when the handle has a single device), each computed with no communication;
 // psi rows and U rows land directly at their offsets in the host planes.
-static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re, const double* psi0_im,
-                     double* psi_re, double* psi_im, double* u_re, double* u_im) {
-    std::lock_guard<std::mutex> lk(h->mu);
+static bool run_full_locked(qsb_handle* h, const qsb_circuit* c, const double* psi0_re, const double* psi0_im,
+                            double* psi_re, double* psi_im, double* u_re, double* u_im, bool allow_hit) {
     validate_circuit_shape(c);
     check_guard(c, h->guard);
     const int64_t N = int64_t{1} << c->n_qubits;
@@ -1084,23 +1160,46 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
     const bool use_nccl = psi_re && !(h->flags & QSB_FLAG_COLUMN_BLOCKS) && distinct &&
                           (G > 1 || (h->flags & QSB_FLAG_NCCL_GATHER));
     double* gathered_host = nullptr;
-    std::vector<std::unique_ptr<qsb_plan>> plans(G);
     std::vector<double*> staged(G, nullptr);
     std::vector<std::vector<double>> vt(G);  // column blocks: V = U[:, cols]^T on the host
-    auto release_all = [&] {
-        for (auto& p : plans) release_plan(p);
-    };
     // QSB_TRACE=1: host-side phase timings of this call on stderr
     static const bool trace = std::getenv("QSB_TRACE") != nullptr;
     auto now = [] { return std::chrono::steady_clock::now(); };
     const auto t0 = now();
+    // Plans of the last call are kept (compiled descriptors, uploaded tables, V buffers,
+    // CUDA graph): a call with the same circuit structure reuses them and checks the
+    // registry matrices' contents against the kept copies while the GPU runs.
+    std::vector<char> key = plan_key(c, G, h->flags);
+    if (c->n_steps > 0)  // (a hit skips compile(), which checks every operation)
+        for (int i = c->step_offsets[0]; i < c->step_offsets[c->n_steps]; ++i) check_op(c, c->ops[i]);
+    const bool hit = allow_hit && !h->cached.empty() && h->cache_key == key;
+    if (!hit) {
+        drop_plan_cache(h);
+        try {
+            for (int g = 0; g < G; ++g)
+                h->cached.push_back(make_plan(h, h->devs[g].get(), c, g * rows, rows, true).release());
+        } catch (...) {
+            drop_plan_cache(h);
+            throw;
+        }
+        h->cache_key = std::move(key);
+        keep_functions(h, c);
+        h->drop_cache = drop_plan_cache;
+    }
+    std::vector<qsb_plan*>& plans = h->cached;
     try {
-        for (int g = 0; g < G; ++g) plans[g] = make_plan(h, h->devs[g].get(), c, g * rows, rows, true);
         const auto t1 = now();
         for (int g = 0; g < G; ++g) {
-            qsb_plan* p = plans[g].get();
+            qsb_plan* p = plans[g];
             DeviceScope ds(p->dc->device);
             cudaStream_t s = p->dc->stream;
+            p->psi_dev_out = nullptr;
+            if (!psi0_re && !p->x_is_e0) {  // a cached plan last ran from a caller's psi0
+                if (!p->small || p->columns)
+                    cuda_check(qsb::sv_launch_init_identity(p->b.x.as<double>(), p->b.x.as<double>() + N, N, 1, 0, s),
+                               "init psi0");
+                p->x_is_e0 = true;
+            }
             if (psi0_re) {
                 p->x_is_e0 = false;
                 cuda_check(cudaMemcpyAsync(p->b.x.p, psi0_re, N * 8, cudaMemcpyHostToDevice, s), "upload psi0");
@@ -1122,7 +1221,7 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
                 else
                     cudaGetLastError();
             }
-            execute(p, s, false);
+            execute(p, s, hit && !p->small && !p->columns);
             const int64_t off = p->row_begin - p->eff_begin;
             if (p->columns) {
                 if (psi_re)
@@ -1160,7 +1259,9 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
                                            cudaMemcpyDeviceToHost, s), "download U");
             }
         }
-        if (use_nccl) {
+        // the GPU is running: check the registry matrices of a reused plan meanwhile
+        const bool same = !hit || functions_unchanged(h, c);
+        if (use_nccl && same) {
             allgather_psi(h, plans, N, rows);
             // every device now holds all of psi; read device 0's copy
             DeviceCtx& d0 = *h->devs[0];
@@ -1170,6 +1271,14 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
                                        cudaMemcpyDeviceToHost, d0.stream), "download psi");
         }
         const auto t2 = now();
+        if (!same) {  // a registered matrix changed under an identical structure: redo from scratch
+            for (int g = 0; g < G; ++g) {
+                DeviceScope ds(plans[g]->dc->device);
+                cuda_check(cudaStreamSynchronize(plans[g]->dc->stream), "cudaStreamSynchronize");
+            }
+            drop_plan_cache(h);
+            return false;
+        }
         for (int g = 0; g < G; ++g) {
             DeviceScope ds(plans[g]->dc->device);
             cuda_check(cudaStreamSynchronize(plans[g]->dc->stream), "cudaStreamSynchronize");
@@ -1178,7 +1287,7 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
                              "expected %d over-count %d\n", d[0], d[1], d[2], d[3], d[4], d[5]);
                 std::memset(d, 0, 8 * sizeof(int));
             }
-            const qsb_plan* p = plans[g].get();
+            const qsb_plan* p = plans[g];
             if (staged[g] && p->columns) {
                 // shares summed in shard order (deterministic); shard 0 initialises
                 for (int64_t k = 0; k < N; ++k) {
@@ -1208,14 +1317,21 @@ static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re,
         if (trace) {
             const auto t3 = now();
             auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
-            std::fprintf(stderr, "qsb trace: n=%d plans %.0f us, enqueue %.0f us, wait+copy %.0f us\n",
-                         c->n_qubits, us(t0, t1), us(t1, t2), us(t2, t3));
+            std::fprintf(stderr, "qsb trace: n=%d %s plans %.0f us, enqueue %.0f us, wait+copy %.0f us\n",
+                         c->n_qubits, hit ? "cached" : "new", us(t0, t1), us(t1, t2), us(t2, t3));
         }
     } catch (...) {
-        release_all();
+        drop_plan_cache(h);
         throw;
     }
-    release_all();
+    return true;
+}
+
+static void run_full(qsb_handle* h, const qsb_circuit* c, const double* psi0_re, const double* psi0_im,
+                     double* psi_re, double* psi_im, double* u_re, double* u_im) {
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!run_full_locked(h, c, psi0_re, psi0_im, psi_re, psi_im, u_re, u_im, true))
+        run_full_locked(h, c, psi0_re, psi0_im, psi_re, psi_im, u_re, u_im, false);
 }
 
 qsb_status qsb_simulate_full_state(qsb_handle* h, const qsb_circuit* c, double* psi_re, double* psi_im) {
@@ -1298,6 +1414,7 @@ qsb_status qsb_layer_operator(qsb_handle* h, const qsb_circuit* c, int32_t step,
     return guarded([&] {
         if (!h || !re || !im) raise(QSB_ERR_ARGUMENT, "null argument");
         std::lock_guard<std::mutex> lk(h->mu);
+        h->drop_plan_cache();  // its V buffers would sit next to this call's operator
         validate_circuit_shape(c);
         if (c->n_qubits > h->guard) check_guard(c, h->guard);
         if (step < 0 || step >= c->n_steps) raise(QSB_ERR_ARGUMENT, "step %d out of range", step);
@@ -1365,6 +1482,7 @@ qsb_status qsb_is_unitary(qsb_handle* h, const double* re, const double* im, int
             raise(QSB_ERR_RESOURCE, "is_unitary: dimension %lld exceeds the supported 65536",
                   static_cast<long long>(dim));
         std::lock_guard<std::mutex> lk(h->mu);
+        h->drop_plan_cache();
         DeviceCtx& dc = h->dev0();
         DeviceScope ds(dc.device);
         Buffers& b = dc.cache;
@@ -1406,6 +1524,7 @@ qsb_status qsb_plan_create(qsb_handle* h, const qsb_circuit* c, int64_t row_begi
         // under the handle lock: make_plan writes the device's pinned staging, which a
         // concurrent host call on this handle may be reading (small plans map it)
         std::lock_guard<std::mutex> lk(h->mu);
+        h->drop_plan_cache();  // a device-resident plan allocates its own buffers
         std::unique_ptr<qsb_plan> p = make_plan(h, &h->dev0(), c, row_begin, row_count, false);
         *out = p.release();
     });

@@ -739,6 +739,7 @@ size_t sv_elems(const qsb_sv_plan* p) { return (size_t{1} << p->n) * static_cast
 void run_structured(qsb_handle* h, const qsb_circuit* c, double* u_re, double* u_im, double* psi_re,
                     double* psi_im) {
     std::lock_guard<std::mutex> lk(h->mu);
+    h->drop_plan_cache();  // the dense path's kept V buffers would sit next to U
     validate_circuit_shape(c);
     const int64_t N = int64_t{1} << c->n_qubits;
     int G = static_cast<int>(h->devs.size());
@@ -786,6 +787,7 @@ void run_structured(qsb_handle* h, const qsb_circuit* c, double* u_re, double* u
 void run_fsv(qsb_handle* h, const qsb_circuit* c, const double* psi0_re, const double* psi0_im, double* psi_re,
              double* psi_im) {
     std::lock_guard<std::mutex> lk(h->mu);
+    h->drop_plan_cache();
     DeviceCtx& dc = h->dev0();
     std::unique_ptr<qsb_sv_plan> p = make_sv_plan(h, &dc, c, QSB_SV_STATE, 0, 1, true);
     try {
@@ -870,6 +872,7 @@ qsb_status qsb_sv_plan_create(qsb_handle* h, const qsb_circuit* c, int32_t mode,
         if (!h || !out) raise(QSB_ERR_ARGUMENT, "null argument");
         *out = nullptr;
         std::lock_guard<std::mutex> lk(h->mu);  // make_sv_plan writes the device's pinned staging
+        h->drop_plan_cache();
         std::unique_ptr<qsb_sv_plan> p = make_sv_plan(h, &h->dev0(), c, mode, col_begin, col_count, false);
         *out = p.release();
     });
