@@ -164,7 +164,9 @@ typedef struct qsb_plan_info {
 
 /* K2 variants reported in qsb_plan_info.gemm_tile. */
 enum { QSB_TILE_128x64 = 0, QSB_TILE_64x64 = 1, QSB_TILE_32x32 = 2, QSB_TILE_WS4M = 3, QSB_TILE_WS3M = 4,
-       QSB_TILE_WS3M_SUMPLANE = 5 };
+       QSB_TILE_WS3M_SUMPLANE = 5,
+       QSB_TILE_WS_CHAIN = 6 /* K2c: every GEMM of the chain in one persistent launch (3M sum-plane
+                                tiles, real layers as two real products), gemm_splits = its k-splits */ };
 
 int qsb_abi_version(void);
 

@@ -177,7 +177,17 @@ int main(int argc, char** argv) {
             what = e.what();
             ok = what.find(std::to_string(memory_estimate(4, BackendKind::Unitary))) != std::string::npos;
         }
-        report("guard -> ResourceError with memory estimate", ok, what);
+        // the reference backend's own refusal, word for word but for the backend name
+        std::string ref_what;
+        try {
+            make_simulator("unitary", o)->simulate_full_state(Circuit(4), {});
+        } catch (const ResourceError& e) {
+            ref_what = e.what();
+        }
+        const std::string from = "unitary backend", to = "unitary-b200 backend";
+        if (ref_what.rfind(from, 0) == 0) ref_what.replace(0, from.size(), to);
+        ok = ok && !ref_what.empty() && what == ref_what;
+        report("guard -> ResourceError with the reference's message", ok, what + " | reference: " + ref_what);
         bool reset_ok = false;
         try {
             Circuit bad(2);

@@ -105,6 +105,22 @@ struct GemmArgs {
                              // distributed shared memory in rank order (deterministic)
 };
 
+// K2c: every GEMM of a chain in one persistent launch (qsb_kernels.cu).
+struct ChainArgs {
+    const void* tmap3[2];      // 3-plane (re, im, re + im) tensor maps of V buffers 0 / 1
+    const void* tmap2[2];      // 2-plane (re, im) views for real layers
+    const LayerDesc* layers;   // device array: the operator of GEMM l (l = 0 .. n_gemms - 1)
+    int n_gemms;
+    double* v[2];              // [3][M][N] each; GEMM l reads v[l & 1], writes v[(l + 1) & 1]
+    int M, N;
+    int splits;                // k-splits per tile (1, 2, 4, 8)
+    double* ws;                // chain_ws_bytes(M, N, splits)
+    int* tile_flags;           // [tiles], zeroed by launch_chain
+    int* row_done;             // [M / 64], zeroed by launch_chain
+};
+size_t chain_ws_bytes(int M, int N, int splits);
+int launch_chain(const ChainArgs& a, void* stream);
+
 int launch_expand(const LayerDesc& layer, uint32_t row_begin, int M, int N, double* out, int planes,
                   void* stream);
 int gemm_tile_planes(int tile);  // planes of the V buffers a tile variant reads/writes (2, or 3 with Vr+Vi)

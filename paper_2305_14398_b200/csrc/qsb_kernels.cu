@@ -635,6 +635,200 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+// Producer side of the warp-specialised K2: operator tile B (rows ktg*BK.., columns
+// n0..n0+BN) of `layer` generated into the stage at bBase by the 128 producer
+// threads (ptid), in the consumers' swizzled layout. Zero tiles are cleared;
+// monomial layers write zeros plus the hits; others fold block entries per element.
+template <bool THREE_M, bool SUMPLANE, bool REAL>
+__device__ __forceinline__ void ws_produce_b(const LayerDesc& layer, uint32_t bBase, int ptid, int ktg, int n0) {
+    using C = WsCfg<THREE_M, SUMPLANE, REAL>;
+    constexpr int BN = C::BN;
+    const TilePrefix tp = tile_prefix<C::LOWBITS>(layer, static_cast<uint32_t>(ktg * C::BK),
+                                                  static_cast<uint32_t>(n0));
+    if (tp.zero) {
+        // whole operator tile is zero: clear the B planes of this stage
+        for (int o = ptid * 16; o < C::B_BYTES; o += 16 * 32 * C::PRODUCER_WARPS) sts128(bBase + o, 0.0, 0.0);
+    } else if (layer.monomial) {
+        // one nonzero per operator row: thread = (line n, half of the 8 k-chunks);
+        // an entry is nonzero only where the row's column is this line's
+        static_assert(32 * C::PRODUCER_WARPS == 2 * BN, "two producer threads per tile line");
+        const int n = ptid & (BN - 1);
+        const int half = ptid / BN;
+        const uint32_t col = static_cast<uint32_t>(n0 + n);
+        // FP64 arithmetic only for the (at most BK) hits: the FP64 pipe is the DMMA pipe.
+        // Columns of this thread's 8 rows first (single-block layers — CNOT, CR, X,
+        // DJ oracle — with independent loads), then the entries of the hits.
+        int64_t cols[8];
+        const uint32_t rbase = static_cast<uint32_t>(ktg * C::BK + 8 * half);
+        if (layer.nblocks == 1) {
+            const BlockDesc& B = layer.blocks[0];
+            const uint32_t keep = ~(B.mask << B.shift);
+            int32_t cb[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t rb = ((rbase + q) >> B.shift) & B.mask;
+                cb[q] = static_cast<int32_t>(rb);
+                if (B.mono == 2) {
+                    cb[q] = __ldg(B.t_col + rb);
+                } else if (B.mono == 1) {
+                    if (B.kind == kBlockGate)
+                        cb[q] = static_cast<int32_t>(rb ^ 1u);
+                    else if (rb & B.cmask)
+                        cb[q] = static_cast<int32_t>(rb ^ B.tmask);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                cols[q] = cb[q] < 0 ? -1
+                                    : static_cast<int64_t>(((rbase + q) & keep) |
+                                                           (static_cast<uint32_t>(cb[q]) << B.shift));
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) cols[q] = mono_col(layer, rbase + q);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int pch = half * 4 + q;  // k = 2 pch, 2 pch + 1
+            const uint32_t r0 = rbase + 2 * q;
+            double v0r = 0.0, v0i = 0.0, v1r = 0.0, v1i = 0.0, s0 = 0.0, s1 = 0.0;
+            if (cols[2 * q] == static_cast<int64_t>(col)) {
+                layer_entry(layer, r0, col, v0r, v0i);
+                if (THREE_M && !REAL) s0 = __dadd_rn(v0r, v0i);
+            }
+            if (cols[2 * q + 1] == static_cast<int64_t>(col)) {
+                layer_entry(layer, r0 + 1, col, v1r, v1i);
+                if (THREE_M && !REAL) s1 = __dadd_rn(v1r, v1i);
+            }
+            const uint32_t off = n * 128 + ((pch ^ (n & 7)) << 4);
+            sts128(bBase + off, v0r, v1r);
+            if (!REAL) sts128(bBase + BN * 128 + off, v0i, v1i);
+            if (THREE_M && !REAL) sts128(bBase + 2 * BN * 128 + off, s0, s1);
+        }
+    } else {
+        constexpr int EB = 4;  // elements per batch = 2 (k, k+1) pairs
+#pragma unroll
+        for (int q0 = 0; q0 < C::PAIRS; q0 += EB / 2) {
+            uint32_t rr[EB], cc[EB];
+            int nn[EB / 2], pp[EB / 2];
+#pragma unroll
+            for (int h = 0; h < EB / 2; ++h) {
+                const int idx = ptid + (q0 + h) * 32 * C::PRODUCER_WARPS;
+                nn[h] = idx % BN;
+                pp[h] = idx / BN;
+                rr[2 * h] = static_cast<uint32_t>(ktg * C::BK + 2 * pp[h]);
+                rr[2 * h + 1] = rr[2 * h] + 1;
+                cc[2 * h] = cc[2 * h + 1] = static_cast<uint32_t>(n0 + nn[h]);
+            }
+            double vr[EB], vi[EB];
+            gen_batch<EB, C::LOWBITS>(layer, tp, rr, cc, vr, vi);
+#pragma unroll
+            for (int h = 0; h < EB / 2; ++h) {
+                const uint32_t off = nn[h] * 128 + ((pp[h] ^ (nn[h] & 7)) << 4);
+                sts128(bBase + off, vr[2 * h], vr[2 * h + 1]);
+                if (REAL) continue;
+                sts128(bBase + BN * 128 + off, vi[2 * h], vi[2 * h + 1]);
+                if (THREE_M) {
+                    // real layers: Br + Bi = Br (adding an exact zero; no FP64 op)
+                    if (layer.real)
+                        sts128(bBase + 2 * BN * 128 + off, vr[2 * h], vr[2 * h + 1]);
+                    else
+                        sts128(bBase + 2 * BN * 128 + off, __dadd_rn(vr[2 * h], vi[2 * h]),
+                               __dadd_rn(vr[2 * h + 1], vi[2 * h + 1]));
+                }
+            }
+        }
+    }
+}
+
+// Consumer side of the warp-specialised K2: the DMMAs of one stage (BK = 16, two
+// k-halves of the lane's 128-bit fragments) into this warp's accumulators. The
+// plane addresses are passed in, so stage layouts of different sizes share it.
+template <bool THREE_M, bool SUMPLANE, bool REAL, int NACC, int NT>
+__device__ __forceinline__ void ws_consume_stage(uint32_t aRe, uint32_t aIm, uint32_t aSm, uint32_t bRe, uint32_t bIm,
+                                                 uint32_t bSm, int wm, int wn, int g, int t,
+                                                 double (&acc)[NACC][4][NT][2]) {
+    using C = WsCfg<THREE_M, SUMPLANE, REAL>;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint32_t choff = static_cast<uint32_t>(((2 * t + h) ^ g) << 4);
+        double2 ar[4], ai[4], as2[4], br[NT], bi[NT], bs[NT];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t line = static_cast<uint32_t>(wm * 32 + i * 8 + g) * 128 + choff;
+            ar[i] = lds128(aRe + line);
+            ai[i] = lds128(aIm + line);
+            if (SUMPLANE && !REAL) as2[i] = lds128(aSm + line);
+        }
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            const uint32_t line = static_cast<uint32_t>(wn * C::WT_N + j * 8 + g) * 128 + choff;
+            br[j] = lds128(bRe + line);
+            if (!REAL) bi[j] = lds128(bIm + line);
+            if (THREE_M && !REAL) bs[j] = lds128(bSm + line);
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            double xr[4], xi[4], yr[NT], yi[NT];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                xr[i] = e ? ar[i].y : ar[i].x;
+                xi[i] = e ? ai[i].y : ai[i].x;
+            }
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                yr[j] = e ? br[j].y : br[j].x;
+                if (!REAL) yi[j] = e ? bi[j].y : bi[j].x;
+            }
+            if (REAL) {
+                // Cr += Ar Br, Ci += Ai Br (Bi = 0 exactly)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) dmma(acc[0][i][j], xr[i], yr[j]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) dmma(acc[1][i][j], xi[i], yr[j]);
+            } else if (THREE_M) {
+                double xs[4], ys[NT];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) xs[i] = SUMPLANE ? (e ? as2[i].y : as2[i].x) : __dadd_rn(xr[i], xi[i]);
+#pragma unroll
+                for (int j = 0; j < NT; ++j) ys[j] = e ? bs[j].y : bs[j].x;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) dmma(acc[0][i][j], xr[i], yr[j]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) dmma(acc[1][i][j], xi[i], yi[j]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) dmma(acc[2][i][j], xs[i], ys[j]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) dmma(acc[0][i][j], xr[i], yr[j]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) dmma(acc[1][i][j], xr[i], yi[j]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) dmma(acc[0][i][j], xi[i], neg(yi[j]));
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) dmma(acc[1][i][j], xi[i], yr[j]);
+            }
+        }
+    }
+}
+
 // MAT_B: the operator was materialised (transposed, [planes][N][N], by
 // expand_t_kernel) and B tiles arrive by TMA like A — no FP64 generation work
 // in the producer, whose FP64 instructions would otherwise queue behind DMMA on
@@ -744,101 +938,7 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
                 mbar_expect_tx(tma_bar, C::A_TMA_BYTES);
                 tma_load_3d(stage, &tmA, tma_bar, ktg * C::BK, m0, 0);
             }
-            const TilePrefix tp = tile_prefix<C::LOWBITS>(layer, static_cast<uint32_t>(ktg * C::BK),
-                                                          static_cast<uint32_t>(n0));
-            if (tp.zero) {
-                // whole operator tile is zero: clear the B planes of this stage
-                for (int o = ptid * 16; o < C::B_BYTES; o += 16 * 32 * C::PRODUCER_WARPS) sts128(bBase + o, 0.0, 0.0);
-            } else if (layer.monomial) {
-                // one nonzero per operator row: thread = (line n, half of the 8 k-chunks);
-                // an entry is nonzero only where the row's column is this line's
-                static_assert(32 * C::PRODUCER_WARPS == 2 * BN, "two producer threads per tile line");
-                const int n = ptid & (BN - 1);
-                const int half = ptid / BN;
-                const uint32_t col = static_cast<uint32_t>(n0 + n);
-                // FP64 arithmetic only for the (at most BK) hits: the FP64 pipe is the DMMA pipe.
-                // Columns of this thread's 8 rows first (single-block layers — CNOT, CR, X,
-                // DJ oracle — with independent loads), then the entries of the hits.
-                int64_t cols[8];
-                const uint32_t rbase = static_cast<uint32_t>(ktg * C::BK + 8 * half);
-                if (layer.nblocks == 1) {
-                    const BlockDesc& B = layer.blocks[0];
-                    const uint32_t keep = ~(B.mask << B.shift);
-                    int32_t cb[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const uint32_t rb = ((rbase + q) >> B.shift) & B.mask;
-                        cb[q] = static_cast<int32_t>(rb);
-                        if (B.mono == 2) {
-                            cb[q] = __ldg(B.t_col + rb);
-                        } else if (B.mono == 1) {
-                            if (B.kind == kBlockGate)
-                                cb[q] = static_cast<int32_t>(rb ^ 1u);
-                            else if (rb & B.cmask)
-                                cb[q] = static_cast<int32_t>(rb ^ B.tmask);
-                        }
-                    }
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        cols[q] = cb[q] < 0 ? -1
-                                            : static_cast<int64_t>(((rbase + q) & keep) |
-                                                                   (static_cast<uint32_t>(cb[q]) << B.shift));
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) cols[q] = mono_col(layer, rbase + q);
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int pch = half * 4 + q;  // k = 2 pch, 2 pch + 1
-                    const uint32_t r0 = rbase + 2 * q;
-                    double v0r = 0.0, v0i = 0.0, v1r = 0.0, v1i = 0.0, s0 = 0.0, s1 = 0.0;
-                    if (cols[2 * q] == static_cast<int64_t>(col)) {
-                        layer_entry(layer, r0, col, v0r, v0i);
-                        if (THREE_M && !REAL) s0 = __dadd_rn(v0r, v0i);
-                    }
-                    if (cols[2 * q + 1] == static_cast<int64_t>(col)) {
-                        layer_entry(layer, r0 + 1, col, v1r, v1i);
-                        if (THREE_M && !REAL) s1 = __dadd_rn(v1r, v1i);
-                    }
-                    const uint32_t off = n * 128 + ((pch ^ (n & 7)) << 4);
-                    sts128(bBase + off, v0r, v1r);
-                    if (!REAL) sts128(bBase + BN * 128 + off, v0i, v1i);
-                    if (THREE_M && !REAL) sts128(bBase + 2 * BN * 128 + off, s0, s1);
-                }
-            } else {
-                constexpr int EB = 4;  // elements per batch = 2 (k, k+1) pairs
-#pragma unroll
-                for (int q0 = 0; q0 < C::PAIRS; q0 += EB / 2) {
-                    uint32_t rr[EB], cc[EB];
-                    int nn[EB / 2], pp[EB / 2];
-#pragma unroll
-                    for (int h = 0; h < EB / 2; ++h) {
-                        const int idx = ptid + (q0 + h) * 32 * C::PRODUCER_WARPS;
-                        nn[h] = idx % BN;
-                        pp[h] = idx / BN;
-                        rr[2 * h] = static_cast<uint32_t>(ktg * C::BK + 2 * pp[h]);
-                        rr[2 * h + 1] = rr[2 * h] + 1;
-                        cc[2 * h] = cc[2 * h + 1] = static_cast<uint32_t>(n0 + nn[h]);
-                    }
-                    double vr[EB], vi[EB];
-                    gen_batch<EB, C::LOWBITS>(layer, tp, rr, cc, vr, vi);
-#pragma unroll
-                    for (int h = 0; h < EB / 2; ++h) {
-                        const uint32_t off = nn[h] * 128 + ((pp[h] ^ (nn[h] & 7)) << 4);
-                        sts128(bBase + off, vr[2 * h], vr[2 * h + 1]);
-                        if (REAL) continue;
-                        sts128(bBase + BN * 128 + off, vi[2 * h], vi[2 * h + 1]);
-                        if (THREE_M) {
-                            // real layers: Br + Bi = Br (adding an exact zero; no FP64 op)
-                            if (layer.real)
-                                sts128(bBase + 2 * BN * 128 + off, vr[2 * h], vr[2 * h + 1]);
-                            else
-                                sts128(bBase + 2 * BN * 128 + off, __dadd_rn(vr[2 * h], vi[2 * h]),
-                                       __dadd_rn(vr[2 * h + 1], vi[2 * h + 1]));
-                        }
-                    }
-                }
-            }
+            ws_produce_b<THREE_M, SUMPLANE, REAL>(layer, bBase, ptid, ktg, n0);
             __syncwarp();
             if (lane == 0) mbar_arrive(sFull + 8 * s);
         }
@@ -893,85 +993,7 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
         const uint32_t bRe = aRe + C::A_BYTES;
         const uint32_t bIm = bRe + BN * 128;
         const uint32_t bSm = bIm + BN * 128;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const uint32_t choff = static_cast<uint32_t>(((2 * t + h) ^ g) << 4);
-            double2 ar[4], ai[4], as2[4], br[NT], bi[NT], bs[NT];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const uint32_t line = static_cast<uint32_t>(wm * 32 + i * 8 + g) * 128 + choff;
-                ar[i] = lds128(aRe + line);
-                ai[i] = lds128(aIm + line);
-                if (SUMPLANE && !REAL) as2[i] = lds128(aSm + line);
-            }
-#pragma unroll
-            for (int j = 0; j < NT; ++j) {
-                const uint32_t line = static_cast<uint32_t>(wn * C::WT_N + j * 8 + g) * 128 + choff;
-                br[j] = lds128(bRe + line);
-                if (!REAL) bi[j] = lds128(bIm + line);
-                if (THREE_M && !REAL) bs[j] = lds128(bSm + line);
-            }
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                double xr[4], xi[4], yr[NT], yi[NT];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    xr[i] = e ? ar[i].y : ar[i].x;
-                    xi[i] = e ? ai[i].y : ai[i].x;
-                }
-#pragma unroll
-                for (int j = 0; j < NT; ++j) {
-                    yr[j] = e ? br[j].y : br[j].x;
-                    if (!REAL) yi[j] = e ? bi[j].y : bi[j].x;
-                }
-                if (REAL) {
-                    // Cr += Ar Br, Ci += Ai Br (Bi = 0 exactly)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-#pragma unroll
-                        for (int j = 0; j < NT; ++j) dmma(acc[0][i][j], xr[i], yr[j]);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-#pragma unroll
-                        for (int j = 0; j < NT; ++j) dmma(acc[1][i][j], xi[i], yr[j]);
-                } else if (THREE_M) {
-                    double xs[4], ys[NT];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) xs[i] = SUMPLANE ? (e ? as2[i].y : as2[i].x) : __dadd_rn(xr[i], xi[i]);
-#pragma unroll
-                    for (int j = 0; j < NT; ++j) ys[j] = e ? bs[j].y : bs[j].x;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-#pragma unroll
-                        for (int j = 0; j < NT; ++j) dmma(acc[0][i][j], xr[i], yr[j]);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-#pragma unroll
-                        for (int j = 0; j < NT; ++j) dmma(acc[1][i][j], xi[i], yi[j]);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-#pragma unroll
-                        for (int j = 0; j < NT; ++j) dmma(acc[2][i][j], xs[i], ys[j]);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-#pragma unroll
-                        for (int j = 0; j < NT; ++j) dmma(acc[0][i][j], xr[i], yr[j]);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-#pragma unroll
-                        for (int j = 0; j < NT; ++j) dmma(acc[1][i][j], xr[i], yi[j]);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-#pragma unroll
-                        for (int j = 0; j < NT; ++j) dmma(acc[0][i][j], xi[i], neg(yi[j]));
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-#pragma unroll
-                        for (int j = 0; j < NT; ++j) dmma(acc[1][i][j], xi[i], yr[j]);
-                }
-            }
-        }
+        ws_consume_stage<THREE_M, SUMPLANE, REAL>(aRe, aIm, aSm, bRe, bIm, bSm, wm, wn, g, t, acc);
     }
     if (pending >= 0) {  // the segment's last stage, before the epilogue
         __syncwarp();
@@ -1335,6 +1357,261 @@ int launch_zgemm(const GemmArgs& a, int tile, int /*gemm_mode*/, void* stream) {
     case kTile64x64: return launch_zgemm_t<64, 64>(a, stream);
     default: return launch_zgemm_t<32, 32>(a, stream);
     }
+}
+
+// ----------------------------------------------------------------------------
+// K2c: the whole GEMM chain of a plan in ONE persistent launch, dataflow across layers
+// ----------------------------------------------------------------------------
+//
+// P persistent CTAs (one per SM, all co-resident) take units u = c, c + P, c + 2P, ...
+// of the chain's unit list, GEMM-major: unit = (GEMM l, output tile t = (tm, tn), k-split
+// s of S, KT / S k-tiles each). Rows tm of V_{l+1} = V_l L_l depend only on rows tm of
+// V_l (the row-block independence of SURVEY 8(e), at tile granularity), so a unit of
+// GEMM l loads its A rows as soon as row_done[tm] >= l * tiles_n — every tile of row
+// block tm of GEMM l-1 stored — while GEMM l-1 is still running on other row blocks:
+// no grid-wide barrier, no per-GEMM launch, pipeline fill or tail wave. The same
+// counter orders the overwrite of V_{l-1} (read only by units of row tm of GEMM l-1).
+// Split-K: the unit holding the LAST k-split finishes the tile — it waits for the other
+// splits' partials (tile_flags, monotonic over the chain) and adds them to its own in
+// split order (a fixed order: the same bits every run). Every wait targets a lower unit index and every CTA runs its
+// units in increasing order, so the lowest unfinished unit can always proceed: no
+// deadlock while all P CTAs are resident (one stream per device).
+// Each GEMM runs as 3M (complex layer) or as two real products (real layer) by a
+// run-time, CTA-uniform branch on layers[l].real; stages use the 3M sum-plane layout
+// for both (a real layer fills two A planes and one B plane of it). Operator tiles are
+// always generated in shared memory (chains with a layer that needs materialising
+// keep the per-GEMM launches).
+struct ChainCfg {
+    using C3 = WsCfg<true, true, false>;
+    using CR = WsCfg<true, true, true>;
+    static constexpr int THREADS = C3::THREADS;
+    static constexpr int STAGE = C3::STAGE;
+    static constexpr int STAGES = C3::STAGES;
+    static constexpr int SMEM = C3::SMEM;
+    static constexpr int NT = C3::NT;
+    static constexpr int NV = 3 * 4 * NT * 2;  // accumulator values per consumer thread
+    static constexpr int CT = 32 * C3::CONSUMER_WARPS;
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(ChainCfg::THREADS, 1)
+    zgemm_chain_kernel(const __grid_constant__ CUtensorMap tm3_0, const __grid_constant__ CUtensorMap tm3_1,
+                       const __grid_constant__ CUtensorMap tm2_0, const __grid_constant__ CUtensorMap tm2_1,
+                       const LayerDesc* __restrict__ layers, int n_gemms, double* __restrict__ v0,
+                       double* __restrict__ v1, int M, int N, int S, double* __restrict__ ws,
+                       int* __restrict__ tile_flags, int* __restrict__ row_done) {
+    using C = ChainCfg::C3;
+    constexpr int BM = C::BM, BN = C::BN, NT = ChainCfg::NT, NV = ChainCfg::NV, CT = ChainCfg::CT;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sBase = smem_u32(smem);
+    const uint32_t sFull = sBase + C::STAGES * C::STAGE;
+    const uint32_t sEmpty = sFull + 8 * C::STAGES;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    const int tiles_n = N / BN;
+    const int T = (M / BM) * tiles_n;
+    const long long U1 = static_cast<long long>(T) * S;
+    const long long U = U1 * n_gemms;
+    const int KS = (N / C::BK) / S;
+    if (tid == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(sFull + 8 * s, 1 + C::PRODUCER_WARPS);
+            mbar_init(sEmpty + 8 * s, C::CONSUMER_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm3_0)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm3_1)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm2_0)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm2_1)) : "memory");
+    }
+    __syncthreads();
+
+    if (warp >= C::CONSUMER_WARPS) {
+        // ------------------------------ producer warpgroup
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::PRODUCER_REGS));
+        const int ptid = tid - 32 * C::CONSUMER_WARPS;
+        int kc = 0;
+        for (long long u = blockIdx.x; u < U; u += gridDim.x) {
+            const int l = static_cast<int>(u / U1);
+            const int rem = static_cast<int>(u % U1);
+            const int tile = rem / S, sp = rem % S;
+            const int tm = tile / tiles_n;
+            const int m0 = tm * BM, n0 = (tile % tiles_n) * BN;
+            const LayerDesc& L = layers[l];
+            const bool real = L.real != 0;
+            if (l > 0 && ptid == 0) {
+                // rows tm of V_l are complete (every tile of row block tm of GEMM l-1 stored)
+                const int need = l * tiles_n;
+                while (ld_acquire(row_done + tm) < need) __nanosleep(64);
+                // generic-proxy stores of other CTAs, acquired above, before our async-proxy (TMA) reads
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+            const CUtensorMap* ta = real ? ((l & 1) ? &tm2_1 : &tm2_0) : ((l & 1) ? &tm3_1 : &tm3_0);
+            const uint32_t a_bytes = real ? ChainCfg::CR::A_TMA_BYTES : C::A_TMA_BYTES;
+            for (int ktg = sp * KS; ktg < (sp + 1) * KS; ++ktg, ++kc) {
+                const int s = kc % C::STAGES;
+                if (kc >= C::STAGES) mbar_wait(sEmpty + 8 * s, ((kc / C::STAGES) & 1) ^ 1);
+                const uint32_t stage = sBase + s * C::STAGE;
+                const uint32_t tma_bar = sFull + 8 * s;
+                if (ptid == 0) {
+                    mbar_expect_tx(tma_bar, a_bytes);
+                    tma_load_3d(stage, ta, tma_bar, ktg * C::BK, m0, 0);
+                }
+                if (real)
+                    ws_produce_b<true, true, true>(L, stage + C::A_BYTES, ptid, ktg, n0);
+                else
+                    ws_produce_b<true, true, false>(L, stage + C::A_BYTES, ptid, ktg, n0);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(sFull + 8 * s);
+            }
+        }
+        return;
+    }
+
+    // ------------------------------ consumer warpgroups
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::CONSUMER_REGS));
+    const int g = lane >> 2;
+    const int t = lane & 3;
+    const int wm = warp / C::CWN;
+    const int wn = warp % C::CWN;
+    const size_t plane = static_cast<size_t>(M) * N;
+    int kc = 0;
+    int pending = -1;  // stage released after the next block boundary (see zgemm_ws_kernel)
+    auto vidx = [](int a, int i, int j, int e) { return ((a * 4 + i) * NT + j) * 2 + e; };
+    for (long long u = blockIdx.x; u < U; u += gridDim.x) {
+        const int l = static_cast<int>(u / U1);
+        const int rem = static_cast<int>(u % U1);
+        const int tile = rem / S, sp = rem % S;
+        const int tm = tile / tiles_n;
+        const int m0 = tm * BM, n0 = (tile % tiles_n) * BN;
+        const bool real = layers[l].real != 0;
+        double acc[3][4][NT][2];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) acc[a][i][j][0] = acc[a][i][j][1] = 0.0;
+        for (int k = 0; k < KS; ++k, ++kc) {
+            if (pending >= 0) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(sEmpty + 8 * pending);
+            }
+            const int s = kc % C::STAGES;
+            mbar_wait(sFull + 8 * s, (kc / C::STAGES) & 1);
+            pending = s;
+            const uint32_t aRe = sBase + s * C::STAGE;
+            const uint32_t aIm = aRe + BM * 128;
+            const uint32_t aSm = aIm + BM * 128;
+            const uint32_t bRe = aRe + C::A_BYTES;
+            const uint32_t bIm = bRe + BN * 128;
+            const uint32_t bSm = bIm + BN * 128;
+            if (real)
+                ws_consume_stage<true, true, true>(aRe, aIm, aSm, bRe, bIm, bSm, wm, wn, g, t, acc);
+            else
+                ws_consume_stage<true, true, false>(aRe, aIm, aSm, bRe, bIm, bSm, wm, wn, g, t, acc);
+        }
+        if (pending >= 0) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(sEmpty + 8 * pending);
+            pending = -1;
+        }
+        if (S > 1) {
+            double* slot = ws + static_cast<size_t>(tile) * (S - 1) * NV * CT + tid;
+            if (sp < S - 1) {
+                // contributor: publish the partial, then count it in (release)
+                double* dst = slot + static_cast<size_t>(sp) * NV * CT;
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < NT; ++j)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) __stcg(dst + vidx(a, i, j, e) * CT, acc[a][i][j][e]);
+                __threadfence();
+                asm volatile("bar.sync 1, %0;" ::"n"(CT) : "memory");
+                if (tid == 0) {
+                    __threadfence();
+                    atomicAdd(tile_flags + tile, 1);
+                }
+                continue;
+            }
+            // finisher: its own k range plus the other splits' partials
+            const int need = (l + 1) * (S - 1);
+            while (ld_acquire(tile_flags + tile) < need) __nanosleep(32);
+            for (int q = 0; q < S - 1; ++q) {  // fixed order: own + p_0 + p_1 + ... (deterministic)
+                const double* src = slot + static_cast<size_t>(q) * NV * CT;
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < NT; ++j)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) acc[a][i][j][e] += __ldcg(src + vidx(a, i, j, e) * CT);
+            }
+        }
+        // store the tile: re, im and the sum plane (the next GEMM may be 3M)
+        double* out = (l & 1) ? v0 : v1;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                const int row = m0 + wm * 32 + i * 8 + g;
+                const int col = n0 + wn * C::WT_N + j * 8 + 2 * t;
+                const size_t o = static_cast<size_t>(row) * N + col;
+                double r0, r1, i0, i1;
+                if (real) {
+                    r0 = acc[0][i][j][0];
+                    r1 = acc[0][i][j][1];
+                    i0 = acc[1][i][j][0];
+                    i1 = acc[1][i][j][1];
+                } else {
+                    r0 = acc[0][i][j][0] - acc[1][i][j][0];
+                    r1 = acc[0][i][j][1] - acc[1][i][j][1];
+                    i0 = acc[2][i][j][0] - acc[0][i][j][0] - acc[1][i][j][0];
+                    i1 = acc[2][i][j][1] - acc[0][i][j][1] - acc[1][i][j][1];
+                }
+                *reinterpret_cast<double2*>(out + o) = make_double2(r0, r1);
+                *reinterpret_cast<double2*>(out + plane + o) = make_double2(i0, i1);
+                *reinterpret_cast<double2*>(out + 2 * plane + o) = make_double2(__dadd_rn(r0, i0), __dadd_rn(r1, i1));
+            }
+        // publish: the tile counts towards row block tm of V_{l+1} (release)
+        __threadfence();
+        asm volatile("bar.sync 1, %0;" ::"n"(CT) : "memory");
+        if (tid == 0) {
+            __threadfence();
+            atomicAdd(row_done + tm, 1);
+        }
+    }
+}
+
+size_t chain_ws_bytes(int M, int N, int S) {
+    const size_t T = static_cast<size_t>(M / ChainCfg::C3::BM) * (N / ChainCfg::C3::BN);
+    return S > 1 ? T * (S - 1) * ChainCfg::NV * ChainCfg::CT * sizeof(double) : 0;
+}
+
+int launch_chain(const ChainArgs& a, void* stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int T = (a.M / ChainCfg::C3::BM) * (a.N / ChainCfg::C3::BN);
+    int e;
+    if ((e = static_cast<int>(cudaMemsetAsync(a.row_done, 0, sizeof(int) * (a.M / ChainCfg::C3::BM), s)))) return e;
+    if (a.splits > 1 && (e = static_cast<int>(cudaMemsetAsync(a.tile_flags, 0, sizeof(int) * T, s)))) return e;
+    const unsigned P = static_cast<unsigned>(ws_max_active_clusters(1));
+    zgemm_chain_kernel<<<P, ChainCfg::THREADS, ChainCfg::SMEM, s>>>(
+        *static_cast<const CUtensorMap*>(a.tmap3[0]), *static_cast<const CUtensorMap*>(a.tmap3[1]),
+        *static_cast<const CUtensorMap*>(a.tmap2[0]), *static_cast<const CUtensorMap*>(a.tmap2[1]), a.layers,
+        a.n_gemms, a.v[0], a.v[1], a.M, a.N, a.splits, a.ws, a.tile_flags, a.row_done);
+    return static_cast<int>(cudaGetLastError());
 }
 
 // ----------------------------------------------------------------------------
@@ -2108,6 +2385,9 @@ int configure_kernels() {
     if ((e = configure_ws_t<false, false>())) return e;
     if ((e = configure_ws_t<true, false>())) return e;
     if ((e = configure_ws_t<true, true>())) return e;
+    if ((e = static_cast<int>(cudaFuncSetAttribute(zgemm_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   ChainCfg::SMEM))))
+        return e;
     query_ws_clusters();
     if ((e = configure_small_t<8>()) || (e = configure_small_t<16>()) || (e = configure_small_t<32>()) ||
         (e = configure_small_t<64>()))

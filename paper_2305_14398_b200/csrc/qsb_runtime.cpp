@@ -301,6 +301,8 @@ struct qsb_plan {
     int tile = qsb::kTile32x32;
     int splits = 1;  // K2 split-K cluster size (warp-specialised tiles)
     bool streamk = false;  // K2 stream-K schedule (warp-specialised tiles)
+    bool chain_k = false;  // K2c: every GEMM in one persistent dataflow launch
+    int chain_splits = 1;
     qsb::SkArgs sk;
     std::vector<char> mat;  // chain[i] (i >= 1) is materialised by K1t and streamed to K2 by TMA
     CUtensorMap tmap_b;     // the materialised operator ([planes][N][N], transposed)
@@ -422,6 +424,9 @@ void upload_tables(qsb_plan* p, const qsb_circuit* c) {
     };
     for (auto& d : p->cc.app) patch(d);
 }
+
+// K2c by default (QSB_CHAIN=1 / 0 force it on / off)
+constexpr bool kChainDefault = false;
 
 // Split-K factor for a warp-specialised tile grid of T output tiles (one CTA
 // per SM): the cluster size s in {1, 2, 4} whose T*s CTAs fill the last wave of
@@ -602,7 +607,43 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     // per element on the producer warps (they queue behind DMMA on the shared FP64
     // pipe) are materialised once by K1t and streamed to K2 by TMA instead.
     p->mat.assign(p->chain.size(), 0);
-    if (!p->small && p->tile >= qsb::kTileWs4M) {
+    // K2c (one persistent launch for the whole chain, dataflow between GEMMs by row
+    // block) where the per-GEMM launch, fill and tail are a visible share of a GEMM:
+    // mid sizes, 3M sum-plane tiles, every operator generated in shared memory (a chain
+    // with a dense non-monomial layer, e.g. DJ's H on every qubit, keeps per-GEMM launches
+    // with that layer materialised). Forced schedules (tests, A/B) keep the GEMM path.
+    {
+        const char* env = std::getenv("QSB_CHAIN");  // 0 off, 1 on wherever possible
+        const int force = env && *env ? std::atoi(env) : -1;
+        const int max_n = std::getenv("QSB_CHAIN_MAXN") ? std::atoi(std::getenv("QSB_CHAIN_MAXN")) : 2048;
+        bool ok = !p->small && !p->columns && p->tile == qsb::kTileWs3MS && p->chain.size() > 2 && p->M % 64 == 0 &&
+                  N >= 512 && force != 0 && !std::getenv("QSB_TILE") && !std::getenv("QSB_SPLITK") &&
+                  !std::getenv("QSB_STREAMK") && !std::getenv("QSB_MATERIALIZE") &&
+                  !std::getenv("QSB_NO_REAL") && !(h->flags & QSB_FLAG_MATERIALIZE);
+        if (ok && force != 1 && (N > max_n || !kChainDefault)) ok = false;
+        for (size_t i = 1; ok && i < p->chain.size(); ++i) {
+            const qsb::LayerDesc& d = p->chain[i];
+            int low = 0;
+            for (int b = 0; b < d.nblocks; ++b)
+                if (d.blocks[b].shift < 6) low += d.blocks[b].kind == qsb::kBlockGate ? 1 : 4;
+            const double frac = std::ldexp(1.0, -__builtin_popcount(d.zmask >> 6));
+            if (!d.monomial && frac * low >= 1.0) ok = false;  // dense non-monomial: keep it materialised
+        }
+        if (ok) {
+            const int T = (p->M / 64) * (static_cast<int>(N) / 64);
+            const int P = qsb::ws_max_active_clusters(1);
+            int S = 1;
+            if (const char* e = std::getenv("QSB_CHAIN_SPLITS")) S = std::max(1, std::atoi(e));
+            else
+                while (T * S < P && S < 8) S *= 2;
+            while (S > 1 && static_cast<int>(N) / 16 / S < 4) S /= 2;
+            p->chain_k = true;
+            p->chain_splits = S;
+            p->streamk = false;
+            p->splits = 1;
+        }
+    }
+    if (!p->small && p->tile >= qsb::kTileWs4M && !p->chain_k) {
         const char* env = std::getenv("QSB_MATERIALIZE");  // "0" never, "1" every layer (tests)
         const int force = env && *env ? std::atoi(env) : -1;
         bool any = false;
@@ -732,6 +773,19 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
             if (p->b.v[1].p) p->tmap_real[1] = make_tmap(p->b.v[1].p, p->M, p->N, rows, 2);
         }
     }
+    if (p->chain_k) {
+        // K2c: the GEMMs' operators as a device array, the split-K workspace and counters
+        const size_t G = p->chain.size() - 1;
+        const size_t bytes = sizeof(qsb::LayerDesc) * G;
+        p->b.layers.ensure(bytes);
+        void* st = dc->stage(bytes);
+        std::memcpy(st, p->chain.data() + 1, bytes);
+        cuda_check(cudaMemcpyAsync(p->b.layers.p, st, bytes, cudaMemcpyHostToDevice, dc->stream), "upload layers");
+        const int T = (p->M / 64) * (p->N / 64);
+        const size_t wsb = qsb::chain_ws_bytes(p->M, p->N, p->chain_splits);
+        if (wsb) p->b.skws.ensure(wsb);
+        p->b.skflags.ensure(sizeof(int) * (static_cast<size_t>(T) + p->M / 64));
+    }
     // Plans executed on a caller's stream (qsb_plan_execute) must see the uploads.
     if (!borrow_cache) cuda_check(cudaStreamSynchronize(dc->stream), "cudaStreamSynchronize");
     const int gemms = p->small ? static_cast<int>(p->chain.size()) - 1 : static_cast<int>(p->chain.size()) - 1;
@@ -741,13 +795,14 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     in.n_layers = static_cast<int>(p->cc.app.size());
     in.n_gemms = gemms;
     in.n_identity_layers = p->n_identity;
-    in.n_launches = p->small ? 1 : 1 + gemms + 1 + static_cast<int>(std::count(p->mat.begin(), p->mat.end(), 1));
+    in.n_launches = p->small ? 1
+                    : (p->chain_k ? 3 : 1 + gemms + 1 + static_cast<int>(std::count(p->mat.begin(), p->mat.end(), 1)));
     in.row_begin = row_begin;
     in.row_count = row_count;
     in.gemm_flops = 8.0 * static_cast<double>(p->M) * static_cast<double>(N) * static_cast<double>(N) * gemms;
     in.expand_bytes = p->small ? 0.0 : 8.0 * p->planes * static_cast<double>(p->M) * static_cast<double>(N);
-    in.gemm_tile = p->small ? -1 : p->tile;
-    in.gemm_splits = p->small ? 1 : (p->streamk ? -1 : p->splits);  // -1: stream-K schedule
+    in.gemm_tile = p->small ? -1 : (p->chain_k ? QSB_TILE_WS_CHAIN : p->tile);
+    in.gemm_splits = p->small ? 1 : (p->chain_k ? p->chain_splits : (p->streamk ? -1 : p->splits));  // -1: stream-K
     {
         const double mn2 = static_cast<double>(p->M) * static_cast<double>(N) * static_cast<double>(N);
         const bool three = p->tile == qsb::kTileWs3M || p->tile == qsb::kTileWs3MS;
@@ -810,7 +865,26 @@ void enqueue(qsb_plan* p, cudaStream_t s) {
                    "expand_kernel");
     if (ev) cuda_check(cudaEventRecord(p->ev[1], s), "event");
     int cur = 0;
-    for (size_t i = 1; i < p->chain.size(); ++i) {
+    if (p->chain_k) {
+        qsb::ChainArgs a;
+        a.tmap3[0] = &p->tmap[0];
+        a.tmap3[1] = &p->tmap[1];
+        a.tmap2[0] = &p->tmap_real[0];
+        a.tmap2[1] = &p->tmap_real[1];
+        a.layers = p->b.layers.as<qsb::LayerDesc>();
+        a.n_gemms = static_cast<int>(p->chain.size()) - 1;
+        a.v[0] = p->b.v[0].as<double>();
+        a.v[1] = p->b.v[1].as<double>();
+        a.M = p->M;
+        a.N = p->N;
+        a.splits = p->chain_splits;
+        a.ws = p->b.skws.as<double>();
+        a.tile_flags = p->b.skflags.as<int>();
+        a.row_done = a.tile_flags + (p->M / 64) * (p->N / 64);
+        cuda_check(qsb::launch_chain(a, s), "zgemm_chain_kernel");
+        cur = a.n_gemms & 1;
+    }
+    for (size_t i = 1; i < p->chain.size() && !p->chain_k; ++i) {
         const bool mat = p->mat[i] != 0;
         if (mat && p->columns)  // operand L^T: its transposed planes are the rows of L
             cuda_check(qsb::launch_expand(p->chain[i], 0, p->N, p->N, p->b.lmat.as<double>(),
@@ -1717,8 +1791,9 @@ qsb_status qsb_plan_allgather_state(const qsb_plan* plan, qsb_comm* comm, double
 qsb_status qsb_plan_gemm_times(qsb_plan* plan, double* ms, int32_t* kinds, int32_t cap, int32_t* count) {
     return guarded([&] {
         if (!plan || !count) raise(QSB_ERR_ARGUMENT, "null argument");
-        if (!plan->per_gemm || !plan->timed_run || plan->small)
-            raise(QSB_ERR_ARGUMENT, "no per-GEMM timed execute on this plan (qsb_plan_set_timing mode 2, tiled path)");
+        if (!plan->per_gemm || !plan->timed_run || plan->small || plan->chain_k)
+            raise(QSB_ERR_ARGUMENT, "no per-GEMM timed execute on this plan (qsb_plan_set_timing mode 2, per-GEMM "
+                                    "launches only: not the one-launch K2s / K2m / K2c chains)");
         const int G = static_cast<int>(plan->chain.size()) - 1;
         *count = G;
         if (G <= 0) return;

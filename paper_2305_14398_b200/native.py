@@ -32,7 +32,8 @@ GEMM_AUTO, GEMM_4M, GEMM_3M = 0, 1, 2
 FLAG_NO_GRAPH, FLAG_MATERIALIZE, FLAG_COLUMN_BLOCKS, FLAG_NCCL_GATHER = 1, 2, 4, 8
 NCCL_ID_BYTES = 128
 TILE_NAMES = {0: "zgemm_gen_kernel<128,64> (4M)", 1: "zgemm_gen_kernel<64,64> (4M)", 2: "zgemm_gen_kernel<32,32> (4M)",
-              3: "zgemm_ws_kernel<4M>", 4: "zgemm_ws_kernel<3M>", 5: "zgemm_ws_kernel<3M, sum plane>"}
+              3: "zgemm_ws_kernel<4M>", 4: "zgemm_ws_kernel<3M>", 5: "zgemm_ws_kernel<3M, sum plane>",
+              6: "zgemm_chain_kernel (K2c: the whole chain in one persistent launch)"}
 
 
 class QsbFunction(ctypes.Structure):

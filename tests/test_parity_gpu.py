@@ -799,3 +799,57 @@ def test_small_k2m_matches_row_resident(monkeypatch, sim, orc, n):
             kr, ki = sim.build_unitary(flat)
             monkeypatch.delenv(env)
             assert rel_frob(ur, ui, kr, ki) <= TOL, env
+
+
+@pytest.mark.parametrize("splits", ["", "1", "2", "4", "8"])
+@pytest.mark.parametrize("name,n", [("qft", 9), ("entangle", 10), ("qft", 10), ("entangle", 9)])
+def test_chain_kernel(monkeypatch, sim, orc, splits, name, n):
+    """K2c (QSB_CHAIN=1): every GEMM of the chain in one persistent launch, dataflow
+    between GEMMs by row block, real and complex layers mixed, k-split partials summed
+    in a fixed order. psi and U against the oracle (1e-10), U against the per-GEMM
+    path (1e-12), and bit-identical across repeated runs (deterministic)."""
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+    from paper_2305_14398_b200.simulator import B200UnitarySimulator
+
+    c, reg = q.make_named_circuit(name, n)
+    flat = native.flatten(c, reg)
+    per_gemm = sim.build_unitary(flat)
+    monkeypatch.setenv("QSB_CHAIN", "1")
+    if splits:
+        monkeypatch.setenv("QSB_CHAIN_SPLITS", splits)
+    s = B200UnitarySimulator(device=0)
+    plan = s.plan(flat)
+    assert plan.info.gemm_tile == 6 and plan.info.n_launches == 3, plan.info.gemm_tile
+    if splits:
+        assert plan.info.gemm_splits == int(splits)
+    plan.close()
+    a = s.build_unitary(flat)
+    b = s.build_unitary(flat)
+    out = s.simulate_full_state(flat)
+    s.close()
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert rel_frob(a[0], a[1], per_gemm[0], per_gemm[1]) <= 1e-12
+    re, im = orc.fsv(flat)
+    assert rel_frob(out.re, out.im, re, im) <= TOL
+    for col in (0, 5, (1 << n) - 1):
+        cr, ci = orc.unitary_column(flat, col)
+        assert rel_frob(a[0][:, col], a[1][:, col], cr, ci) <= TOL
+
+
+def test_chain_kernel_row_shards(monkeypatch, orc):
+    """K2c on row shards (M < N): each shard's rows equal the full unitary's."""
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+    from paper_2305_14398_b200.simulator import B200UnitarySimulator
+
+    monkeypatch.setenv("QSB_CHAIN", "1")
+    c, reg = q.make_named_circuit("qft", 10)
+    flat = native.flatten(c, reg)
+    s = B200UnitarySimulator(devices=[0, 0, 0, 0])
+    ur, ui = s.build_unitary(flat)
+    psi = s.simulate_full_state(flat)
+    s.close()
+    re, im = orc.fsv(flat)
+    assert rel_frob(psi.re, psi.im, re, im) <= TOL
+    assert rel_frob(ur[:, 0], ui[:, 0], re, im) <= TOL
