@@ -88,26 +88,54 @@ def oracle_available() -> bool:
     return oracle.reference_available()
 
 
-def cpu_sample(workload: str, repeats: int = 1):
+def cpu_sample(workload: str, repeats: int = 2):
     """Reference CPU time of a named BASELINE workload (cpu_sample_circuit)."""
     name, n = WORKLOADS[workload]
     return cpu_sample_circuit(name, n, repeats)
 
 
-def cpu_sample_circuit(name: str, n: int, repeats: int = 1):
-    """Time the reference CPU path on a bounded sample and extrapolate to one
-    circuit. Components:
-      T = sum_steps [fold(step) + GEMM_par(N)] + extra_layers * GEMM_ser(N)
-    where GEMM_* come from the reference's own matmul on a row slab of the
-    accumulate GEMM (linalg.cpp:72-87 accepts rectangular shapes), fold from
-    step_unitary of a single-layer step (unitary_backend.cpp:141-154)."""
+FULL_RUN_LIMIT_S = 30.0  # model-predicted reference time under which the whole circuit is run instead
+# reference worker threads (QSIM_THREADS semantics): 0 = every host core
+REF_THREADS = int(os.environ.get("QSB_REF_THREADS", "0") or 0)
+
+
+def ref_cores() -> int:
+    return REF_THREADS if REF_THREADS > 0 else (os.cpu_count() or 1)
+
+
+def cpu_full_run(name: str, n: int) -> float:
+    """ms of one whole reference UnitarySimulator::simulate_full_state ("unitary-parallel")."""
+    import oracle
+
+    ref = oracle.Reference()
+    prog = ref.named(name, n)
+    ref.L.refsh_set_worker_count(REF_THREADS)
+    return ref.L.refsh_time_simulate(prog.h, b"unitary-parallel", n) * 1e3
+
+
+def cpu_sample_circuit(name: str, n: int, repeats: int = 2, allow_full: bool = True):
+    """Time the reference CPU path (oracle/_ref: the unmodified reference library)
+    on this host's cores for one circuit. When the component model below predicts
+    at most FULL_RUN_LIMIT_S, the whole UnitarySimulator::simulate_full_state
+    ("unitary-parallel", all cores) is run and timed — a measurement. Otherwise a
+    bounded sample of the reference's own components is timed and extrapolated
+    (SURVEY.md 8(d)):
+      T = (steps + extra) * fold + steps * GEMM_par(N) + extra * GEMM_ser(N)
+    per step: step_unitary folds every layer (unitary_backend.cpp:141-154) and
+    multiplies a multi-layer step's layers serially (:151), then one parallel
+    accumulate matmul (:211). GEMM_* come from the reference's own matmul on row
+    slabs of N/4 (parallel) and N/16 (serial) rows (linalg.cpp:72-87 accepts
+    rectangular shapes; smaller slabs mis-predict by up to 2x: thread start-up
+    and cache effects), fold from step_unitary of a single-layer step; each
+    component is the minimum of `repeats` timings. The model's error against full
+    runs on the GPU box's host is committed in profiles/cpu_pin.json."""
     import oracle
     import paper_2305_14398_b200 as q
     from paper_2305_14398_b200 import native
 
     workload = f"{name}-{n}"
     N = 1 << n
-    cores = os.cpu_count() or 1
+    cores = ref_cores()
     c, reg = q.make_named_circuit(name, n)
     flat = native.flatten(c, reg)
     orc = oracle.Oracle()
@@ -123,54 +151,60 @@ def cpu_sample_circuit(name: str, n: int, repeats: int = 1):
             # small sizes: time the whole reference simulate_full_state directly
             t_full = []
             for _ in range(max(1, repeats)):
-                ref.L.refsh_set_worker_count(0)
+                ref.L.refsh_set_worker_count(REF_THREADS)
                 t_full.append(ref.L.refsh_time_simulate(prog.h, b"unitary-parallel", n))
             t_par = min(t_full)
             ref.L.refsh_set_worker_count(1)
             t_ser = min(ref.L.refsh_time_simulate(prog.h, b"unitary", n) for _ in range(max(1, repeats)))
-            ref.L.refsh_set_worker_count(0)
+            ref.L.refsh_set_worker_count(REF_THREADS)
             best = min(t_par, t_ser)
             return {"value": best * 1e3, "unit": "ms", "cores": cores, "kind": kind,
                     "sample": f"full reference UnitarySimulator::simulate_full_state of {workload} "
                               f"(best of unitary / unitary-parallel, {repeats} run(s))"}
-        rows_par = max(cores * 4, 64)
-        rows_ser = 8
-        t_fold, t_par, t_ser = [], [], []
-        for _ in range(max(1, repeats)):
-            ref.L.refsh_set_worker_count(0)  # QSIM_THREADS unset: all host cores
-            t_fold.append(ref.L.refsh_time_step_unitary(prog.h, single))
-            t_par.append(ref.L.refsh_time_matmul(rows_par, N, 1))
-            t_ser.append(ref.L.refsh_time_matmul(rows_ser, N, 0))
-        fold = min(t_fold)
-        gemm_par = min(t_par) * N / rows_par
-        gemm_ser = min(t_ser) * N / rows_ser
+        rows_par = max(N // 4, 64)
+        rows_ser = max(N // 16, 8)
+        ref.L.refsh_set_worker_count(REF_THREADS)  # 0 = QSIM_THREADS unset: all host cores
+        fold = min(ref.L.refsh_time_step_unitary(prog.h, single) for _ in range(max(1, repeats)))
+        gemm_par = min(ref.L.refsh_time_matmul(rows_par, N, 1) for _ in range(max(1, repeats))) * N / rows_par
+        gemm_ser = (min(ref.L.refsh_time_matmul(rows_ser, N, 0) for _ in range(max(1, repeats))) * N / rows_ser
+                    if extra else 0.0)
+        total = (n_steps + extra) * fold + n_steps * gemm_par + extra * gemm_ser
+        comps = {"fold": fold, "gemm_parallel": gemm_par, "gemm_serial": gemm_ser, "steps": n_steps,
+                 "extra_layers": extra, "model_s": total}
+        if allow_full and total <= FULL_RUN_LIMIT_S:
+            return {"value": cpu_full_run(name, n), "unit": "ms", "cores": cores, "kind": kind,
+                    "sample": f"full reference UnitarySimulator::simulate_full_state of {workload} "
+                              f"(unitary-parallel, {cores} threads, one run)",
+                    "components_s": comps, "full_run": True}
         sample = (f"reference step_unitary(single-layer step) + matmul({rows_par}x{N} . {N}x{N}, Parallel, "
-                  f"{cores} threads) + matmul({rows_ser}x{N} . {N}x{N}, Serial); extrapolated to {n_steps} steps "
-                  f"+ {extra} serial extra-layer GEMMs")
-    else:
-        kind = "port"
-        orc.set_threads(cores)
-        import numpy as np
+                  f"{cores} threads) + matmul({rows_ser}x{N} . {N}x{N}, Serial), min of {repeats}; "
+                  f"extrapolated to {n_steps} steps + {extra} serial extra-layer GEMMs")
+        return {"value": total * 1e3, "unit": "ms", "cores": cores, "kind": kind, "sample": sample,
+                "components_s": comps, "full_run": False}
+    kind = "port"
+    orc.set_threads(cores)
+    import numpy as np
 
-        rows_par = max(cores * 4, 64)
-        rows_ser = 8
-        a = np.random.default_rng(0).uniform(-1, 1, (rows_par, N)) * (1 + 0.5j)
-        b = np.eye(N, dtype=complex)
-        t0 = time.perf_counter()
-        orc.layer_operator(flat, single, 0)
-        fold = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        orc.matmul(a, b)
-        gemm_par = (time.perf_counter() - t0) * N / rows_par
-        orc.set_threads(1)
-        t0 = time.perf_counter()
-        orc.matmul(a[:rows_ser], b)
-        gemm_ser = (time.perf_counter() - t0) * N / rows_ser
-        sample = "C oracle port (oracle/_ref absent): same components, extrapolated"
-    total = n_steps * (fold + gemm_par) + extra * (fold + gemm_ser)
-    return {"value": total * 1e3, "unit": "ms", "cores": cores, "kind": kind, "sample": sample,
+    rows_par = max(N // 4, 64)
+    rows_ser = max(N // 16, 8)
+    a = np.random.default_rng(0).uniform(-1, 1, (rows_par, N)) * (1 + 0.5j)
+    b = np.eye(N, dtype=complex)
+    t0 = time.perf_counter()
+    orc.layer_operator(flat, single, 0)
+    fold = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    orc.matmul(a, b)
+    gemm_par = (time.perf_counter() - t0) * N / rows_par
+    orc.set_threads(1)
+    t0 = time.perf_counter()
+    orc.matmul(a[:rows_ser], b)
+    gemm_ser = (time.perf_counter() - t0) * N / rows_ser
+    total = (n_steps + extra) * fold + n_steps * gemm_par + extra * gemm_ser
+    return {"value": total * 1e3, "unit": "ms", "cores": cores, "kind": kind,
+            "sample": "C oracle port (oracle/_ref absent): same components, extrapolated",
             "components_s": {"fold": fold, "gemm_parallel": gemm_par, "gemm_serial": gemm_ser,
-                             "steps": n_steps, "extra_layers": extra}}
+                             "steps": n_steps, "extra_layers": extra, "model_s": total},
+            "full_run": False}
 
 
 def model_validation(workload: str):
@@ -205,15 +239,19 @@ def run_reference(args):
         return 0
     name, n = WORKLOADS[args.workload]
     t0 = time.perf_counter()
-    if n <= 8:
-        for _ in range(args.warmup):
-            cpu_sample(args.workload)
-        runs = [cpu_sample(args.workload) for _ in range(args.steps)]
-        value = statistics.mean(r["value"] for r in runs)
-        last = runs[-1]
+    first = cpu_sample(args.workload)
+    if n <= 8 or first.get("full_run"):
+        # the whole circuit is affordable: time it --steps times (bounded to ~2 minutes)
+        per = first["value"] / 1e3
+        reps = max(1, min(args.steps, int(120.0 / max(per, 1e-6))))
+        vals = [first["value"]] + [cpu_full_run(name, n) if first.get("full_run") else cpu_sample(args.workload)["value"]
+                                   for _ in range(reps - 1)]
+        value = statistics.mean(vals)
+        runs = vals
+        last = first
         extrapolated, timed = False, len(runs)
     else:
-        last = cpu_sample(args.workload)
+        last = first  # one timed sample of the components, extrapolated once
         value = last["value"]
         extrapolated, timed = True, 1
     wall = time.perf_counter() - t0
@@ -489,7 +527,7 @@ def run_ours(args):
                           f"NCCL all-gather of psi ({16 * N // vr} bytes per rank)"}
         if world == 1 and vr == 1 and not args.no_cpu_baseline:
             cb = cpu_sample(args.workload)
-            cb["extrapolated"] = "components_s" in cb
+            cb["extrapolated"] = not cb.get("full_run", True) if "components_s" in cb else False
             if cb["extrapolated"]:
                 cb["model_validation"] = model_validation(args.workload)
             line["cpu_baseline"] = cb

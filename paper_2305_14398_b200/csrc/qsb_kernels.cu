@@ -906,6 +906,7 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
     // (out), so wait for its completion. Then let the next GEMM start launching.
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    __syncwarp();  // converged at the aligned CTA barrier (synccheck flagged lanes leaving griddepcontrol.wait apart)
     __syncthreads();
 
     if (warp >= C::CONSUMER_WARPS) {
@@ -1585,7 +1586,9 @@ __global__ void __launch_bounds__(ChainCfg::THREADS, 1)
                 *reinterpret_cast<double2*>(out + plane + o) = make_double2(i0, i1);
                 *reinterpret_cast<double2*>(out + 2 * plane + o) = make_double2(__dadd_rn(r0, i0), __dadd_rn(r1, i1));
             }
-        // publish: the tile counts towards row block tm of V_{l+1} (release)
+        // publish: the tile counts towards row block tm of V_{l+1} (release); the proxy fence
+        // orders these generic stores before the async-proxy (TMA) reads that consume them
+        asm volatile("fence.proxy.async.global;" ::: "memory");
         __threadfence();
         asm volatile("bar.sync 1, %0;" ::"n"(CT) : "memory");
         if (tid == 0) {

@@ -5,7 +5,7 @@
 #   gpurun --timeout 3000 -- 'bash tools/gpu_pin_sanitize.sh [pin|san|all]'
 set -u
 cd "$(dirname "$0")/.."
-OUT=gpurun_out/r2_sanitize
+OUT=${OUTDIR:-gpurun_out/r2_sanitize}
 mkdir -p "$OUT"
 WHAT=${1:-all}
 nproc > "$OUT/nproc.txt"; lscpu | head -20 >> "$OUT/nproc.txt"
@@ -16,7 +16,7 @@ if [ "$WHAT" = pin ] || [ "$WHAT" = all ]; then
 fi
 if [ "$WHAT" = san ] || [ "$WHAT" = all ]; then
   CS=/usr/local/cuda/bin/compute-sanitizer
-  CASES=$(python tools/sanitize_cases.py list)
+  CASES=$(python tools/sanitize_cases.py ${SAN_CASES:-list})
   for tool in ${SAN_TOOLS:-memcheck synccheck racecheck initcheck}; do
     for c in $CASES; do
       extra=""

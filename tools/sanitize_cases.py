@@ -50,6 +50,10 @@ CASES = {
     "k2_gen_128x64": (k2_circuit, 9, {"QSB_TILE": "0"}, native.GEMM_AUTO),
     "k2_gen_64x64": (k2_circuit, 9, {"QSB_TILE": "1"}, native.GEMM_AUTO),
     "k2_gen_32x32": (k2_circuit, 8, {"QSB_TILE": "2"}, native.GEMM_AUTO),
+    # K2c: the whole chain in one persistent dataflow launch (k-splits 1 / 2 / 4)
+    "k2c_qft9": ("qft", 9, {"QSB_CHAIN": "1"}, native.GEMM_AUTO),
+    "k2c_entangle10": ("entangle", 10, {"QSB_CHAIN": "1"}, native.GEMM_AUTO),
+    "k2c_qft10_s4": ("qft", 10, {"QSB_CHAIN": "1", "QSB_CHAIN_SPLITS": "4"}, native.GEMM_AUTO),
     # K2m cluster chains (N = 64 / 128 / 256), with and without double-buffered operators
     "k2m_qft6": ("qft", 6, {}, native.GEMM_AUTO),
     "k2m_qft7": ("qft", 7, {}, native.GEMM_AUTO),
@@ -126,6 +130,10 @@ if __name__ == "__main__":
     which = sys.argv[1]
     if which == "list":
         print(" ".join(list(CASES) + ["registry", "sv"]))
+        sys.exit(0)
+    if which.startswith("list:"):  # cases whose name starts with one of the comma-separated prefixes
+        pre = which[5:].split(",")
+        print(" ".join(c for c in list(CASES) + ["registry", "sv"] if any(c.startswith(p) for p in pre)))
         sys.exit(0)
     if which == "registry":
         sys.exit(run_registry())
