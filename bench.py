@@ -463,10 +463,10 @@ def run_ours(args):
         plan = None
     e2e_clocks = None
     if vr > 1:
-        e2e_ms, h2d, d2h = None, 0, 0  # the projection times one shard, not a full circuit
+        e2e_ms, h2d, d2h, e2e_calls = None, 0, 0, 0  # the projection times one shard, not a full circuit
     else:
         with ClockSampler(local, "e2e") as eclk:
-            e2e_ms, h2d, d2h = e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr)
+            e2e_ms, h2d, d2h, e2e_calls = e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr)
         e2e_clocks = eclk.summary()
 
     if rank == 0:
@@ -508,6 +508,7 @@ def run_ours(args):
                                         "mma.sync.m8n8k4.f64 loop, tools/microbench/fp64_peak.cu, "
                                         "profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no FP64 entry"},
             "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "calls_timed": e2e_calls,
                     "api": "qsb_simulate_full_state (C ABI)" if world == 1 else
                            "qsb_plan_create/execute + NCCL all-gather + D2H",
                     "clocks": e2e_clocks},
@@ -576,13 +577,17 @@ def e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr):
         re = np.empty(N)
         im = np.empty(N)
         L = native.lib()
+        t0 = time.perf_counter()
         native.check(L.qsb_simulate_full_state(sim._h, flat.ptr, native.dptr(re), native.dptr(im)))
+        first = time.perf_counter() - t0
+        # as many calls as --steps within ~20 s (at least 3): run_bench's repeated calls
+        steps = max(3, min(args.steps, int(20.0 / max(first, 1e-6))))
         times = []
         for _ in range(steps):
             t0 = time.perf_counter()
             native.check(L.qsb_simulate_full_state(sim._h, flat.ptr, native.dptr(re), native.dptr(im)))
             times.append((time.perf_counter() - t0) * 1e3)
-        return sum(times) / len(times), h2d, d2h
+        return sum(times) / len(times), h2d, d2h, len(times)
     psi_re = torch.empty(N, dtype=torch.float64, device="cuda")
     psi_im = torch.empty(N, dtype=torch.float64, device="cuda")
     host = torch.empty(2, N, dtype=torch.float64, pin_memory=True)
@@ -604,7 +609,7 @@ def e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr):
         t = torch.tensor([dt], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         times.append(float(t.item()))
-    return sum(times) / len(times), h2d, d2h
+    return sum(times) / len(times), h2d, d2h, len(times)
 
 
 # --------------------------------------------------------------- state-vector engine arms
