@@ -303,6 +303,14 @@ struct qsb_plan {
     bool streamk = false;  // K2 stream-K schedule (warp-specialised tiles)
     bool chain_k = false;  // K2c: every GEMM in one persistent dataflow launch
     int chain_splits = 1;
+    // Row-block parts on one device: the plan's rows split into independent sub-plans
+    // whose GEMM chains run concurrently on two streams (fork / join), so one chain's
+    // per-GEMM ramp and tail overlap the other's work (mid sizes)
+    std::vector<std::unique_ptr<qsb_plan>> parts;
+    std::vector<cudaStream_t> sides;   // parts 1 .. k-1 (part 0 runs on the caller's stream)
+    std::vector<cudaEvent_t> joins;
+    cudaEvent_t fork_ev = nullptr;
+    bool no_streamk = false;  // a part: its grids run next to another part's, so no persistent stream-K grid
     qsb::SkArgs sk;
     std::vector<char> mat;  // chain[i] (i >= 1) is materialised by K1t and streamed to K2 by TMA
     CUtensorMap tmap_b;     // the materialised operator ([planes][N][N], transposed)
@@ -427,6 +435,8 @@ void upload_tables(qsb_plan* p, const qsb_circuit* c) {
 
 // K2c by default (QSB_CHAIN=1 / 0 force it on / off)
 constexpr bool kChainDefault = false;
+// Row-block parts per plan by default (QSB_PARTS forces a count)
+int kPartsDefault(int64_t N) { return N <= 0 ? 1 : 1; }
 
 // Split-K factor for a warp-specialised tile grid of T output tiles (one CTA
 // per SM): the cluster size s in {1, 2, 4} whose T*s CTAs fill the last wave of
@@ -506,8 +516,72 @@ int pick_tile(int M, int N, int gemm_mode, int* splits) {
 
 // Build a plan; the caller holds the handle mutex when borrow_cache is set.
 std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circuit* c, int64_t row_begin,
-                                    int64_t row_count, bool borrow_cache) {
+                                    int64_t row_count, bool borrow_cache, bool as_part = false);
+
+// Row-block parts for a plan of `rows` rows of a 2^n unitary: QSB_PARTS forces the
+// count (1 = off); by default the sizes where the per-GEMM ramp / tail is a visible share.
+int pick_parts(int n, int64_t rows, int flags) {
+    if (flags & QSB_FLAG_COLUMN_BLOCKS) return 1;
+    const int64_t N = int64_t{1} << n;
+    if (N < 512 || std::getenv("QSB_TILE") || std::getenv("QSB_SPLITK") || std::getenv("QSB_STREAMK") ||
+        std::getenv("QSB_CHAIN"))
+        return 1;
+    int parts = 1;
+    if (const char* e = std::getenv("QSB_PARTS"))
+        parts = std::max(1, std::atoi(e));
+    else
+        parts = kPartsDefault(N);
+    while (parts > 1 && (rows % parts != 0 || rows / parts < 128 || ((rows / parts) & (rows / parts - 1)) != 0))
+        parts /= 2;
+    return parts;
+}
+
+std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circuit* c, int64_t row_begin,
+                                    int64_t row_count, bool borrow_cache, bool as_part) {
     static const bool trace = std::getenv("QSB_TRACE") != nullptr;
+    if (!as_part) {
+        validate_circuit_shape(c);
+        const int nparts = (row_count > 0 && c->n_qubits <= 30) ? pick_parts(c->n_qubits, row_count, h->flags) : 1;
+        if (nparts > 1) {
+            check_guard(c, h->guard);
+            auto p = std::make_unique<qsb_plan>();
+            p->h = h;
+            p->dc = dc;
+            p->N = 1 << c->n_qubits;
+            p->row_begin = row_begin;
+            p->row_count = row_count;
+            p->eff_begin = row_begin;
+            p->M = static_cast<int>(row_count);
+            const int64_t rows = row_count / nparts;
+            for (int i = 0; i < nparts; ++i)
+                p->parts.push_back(make_plan(h, dc, c, row_begin + i * rows, rows, false, true));
+            DeviceScope ds(dc->device);
+            cuda_check(cudaEventCreateWithFlags(&p->fork_ev, cudaEventDisableTiming), "cudaEventCreate");
+            p->sides.assign(nparts - 1, nullptr);
+            p->joins.assign(nparts - 1, nullptr);
+            for (int i = 0; i + 1 < nparts; ++i) {
+                cuda_check(cudaStreamCreateWithFlags(&p->sides[i], cudaStreamNonBlocking), "cudaStreamCreate");
+                cuda_check(cudaEventCreateWithFlags(&p->joins[i], cudaEventDisableTiming), "cudaEventCreate");
+            }
+            p->b.psi.ensure(2 * static_cast<size_t>(row_count) * 8);  // the parts' psi rows, gathered
+            const qsb_plan_info& f = p->parts[0]->info;
+            qsb_plan_info& in = p->info;
+            in = f;
+            in.row_begin = row_begin;
+            in.row_count = row_count;
+            in.gemm_flops = in.gemm_hw_flops = in.expand_bytes = 0.0;
+            in.n_launches = 0;
+            for (const auto& q : p->parts) {
+                in.gemm_flops += q->info.gemm_flops;
+                in.gemm_hw_flops += q->info.gemm_hw_flops;
+                in.expand_bytes += q->info.expand_bytes;
+                in.n_launches += q->info.n_launches;
+            }
+            p->gemm_kind = p->parts[0]->gemm_kind;
+            p->chain = p->parts[0]->chain;  // (layer count for the accessors; the parts own the work)
+            return p;
+        }
+    }
     auto tnow = [] { return std::chrono::steady_clock::now(); };
     const auto t0 = tnow();
     validate_circuit_shape(c);
@@ -574,7 +648,7 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     p->tile = p->small ? qsb::kTile32x32 : pick_tile(p->M, p->N, h->gemm_mode, &p->splits);
     if (!p->small && p->tile >= qsb::kTileWs4M) {
         const int64_t T = static_cast<int64_t>(p->M / qsb::gemm_tile_rows(p->tile)) * (p->N / qsb::gemm_tile_cols(p->tile));
-        p->streamk = pick_streamk(T, p->N / 16, p->splits);
+        p->streamk = !as_part && pick_streamk(T, p->N / 16, p->splits);
         if (p->streamk) p->splits = 1;
     }
     if (p->tile == qsb::kTileWs3MS) {
@@ -616,7 +690,7 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
         const char* env = std::getenv("QSB_CHAIN");  // 0 off, 1 on wherever possible
         const int force = env && *env ? std::atoi(env) : -1;
         const int max_n = std::getenv("QSB_CHAIN_MAXN") ? std::atoi(std::getenv("QSB_CHAIN_MAXN")) : 2048;
-        bool ok = !p->small && !p->columns && p->tile == qsb::kTileWs3MS && p->chain.size() > 2 && p->M % 64 == 0 &&
+        bool ok = !as_part && !p->small && !p->columns && p->tile == qsb::kTileWs3MS && p->chain.size() > 2 && p->M % 64 == 0 &&
                   N >= 512 && force != 0 && !std::getenv("QSB_TILE") && !std::getenv("QSB_SPLITK") &&
                   !std::getenv("QSB_STREAMK") && !std::getenv("QSB_MATERIALIZE") &&
                   !std::getenv("QSB_NO_REAL") && !(h->flags & QSB_FLAG_MATERIALIZE);
@@ -824,6 +898,10 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
 void release_plan(std::unique_ptr<qsb_plan>& p) {
     if (!p) return;
     DeviceScope ds(p->dc->device);
+    for (auto& q : p->parts) release_plan(q);
+    for (auto& st : p->sides) cudaStreamDestroy(st);
+    for (auto& e : p->joins) cudaEventDestroy(e);
+    if (p->fork_ev) cudaEventDestroy(p->fork_ev);
     if (p->graph) cudaGraphExecDestroy(p->graph);
     for (auto& e : p->ev)
         if (e) cudaEventDestroy(e);
@@ -834,6 +912,34 @@ void release_plan(std::unique_ptr<qsb_plan>& p) {
 }
 
 void enqueue(qsb_plan* p, cudaStream_t s) {
+    if (!p->parts.empty()) {
+        // fork: part 0 on s, the others on the side stream; join back into s, then gather
+        // the parts' psi rows into this plan's psi (so its accessors see one shard)
+        const bool ev = p->timing && p->timed_run;
+        if (ev) {
+            cuda_check(cudaEventRecord(p->ev[0], s), "event");
+            cuda_check(cudaEventRecord(p->ev[1], s), "event");
+        }
+        cuda_check(cudaEventRecord(p->fork_ev, s), "event");
+        for (cudaStream_t st : p->sides) cuda_check(cudaStreamWaitEvent(st, p->fork_ev, 0), "cudaStreamWaitEvent");
+        for (size_t i = 0; i < p->parts.size(); ++i) enqueue(p->parts[i].get(), i == 0 ? s : p->sides[i - 1]);
+        for (size_t i = 0; i < p->sides.size(); ++i) {
+            cuda_check(cudaEventRecord(p->joins[i], p->sides[i]), "event");
+            cuda_check(cudaStreamWaitEvent(s, p->joins[i], 0), "cudaStreamWaitEvent");
+        }
+        if (ev) cuda_check(cudaEventRecord(p->ev[2], s), "event");
+        int64_t off = 0;
+        for (const auto& q : p->parts) {
+            const size_t bytes = static_cast<size_t>(q->row_count) * 8;
+            const double* src = q->b.psi.as<double>() + (q->row_begin - q->eff_begin);
+            cuda_check(cudaMemcpyAsync(p->b.psi.as<double>() + off, src, bytes, cudaMemcpyDeviceToDevice, s), "psi");
+            cuda_check(cudaMemcpyAsync(p->b.psi.as<double>() + p->M + off, src + q->M, bytes,
+                                       cudaMemcpyDeviceToDevice, s), "psi");
+            off += q->row_count;
+        }
+        if (ev) cuda_check(cudaEventRecord(p->ev[3], s), "event");
+        return;
+    }
     const uint32_t rb = static_cast<uint32_t>(p->eff_begin);
     if (p->small) {
         const auto* layers = p->small_layers_dev ? static_cast<const qsb::SmallLayerDesc*>(p->small_layers_dev)
@@ -1268,17 +1374,24 @@ static bool run_full_locked(qsb_handle* h, const qsb_circuit* c, const double* p
             DeviceScope ds(p->dc->device);
             cudaStream_t s = p->dc->stream;
             p->psi_dev_out = nullptr;
-            if (!psi0_re && !p->x_is_e0) {  // a cached plan last ran from a caller's psi0
-                if (!p->small || p->columns)
-                    cuda_check(qsb::sv_launch_init_identity(p->b.x.as<double>(), p->b.x.as<double>() + N, N, 1, 0, s),
-                               "init psi0");
-                p->x_is_e0 = true;
-            }
-            if (psi0_re) {
-                p->x_is_e0 = false;
-                cuda_check(cudaMemcpyAsync(p->b.x.p, psi0_re, N * 8, cudaMemcpyHostToDevice, s), "upload psi0");
-                cuda_check(cudaMemcpyAsync(p->b.x.as<double>() + N, psi0_im, N * 8, cudaMemcpyHostToDevice, s),
-                           "upload psi0");
+            // psi0 lives in each computing plan (the row-block parts, or the plan itself)
+            std::vector<qsb_plan*> targets;
+            for (auto& q : p->parts) targets.push_back(q.get());
+            if (targets.empty()) targets.push_back(p);
+            for (qsb_plan* t : targets) {
+                if (!psi0_re && !t->x_is_e0) {  // a cached plan last ran from a caller's psi0
+                    if (!t->small || t->columns)
+                        cuda_check(qsb::sv_launch_init_identity(t->b.x.as<double>(), t->b.x.as<double>() + N, N, 1, 0,
+                                                                s),
+                                   "init psi0");
+                    t->x_is_e0 = true;
+                }
+                if (psi0_re) {
+                    t->x_is_e0 = false;
+                    cuda_check(cudaMemcpyAsync(t->b.x.p, psi0_re, N * 8, cudaMemcpyHostToDevice, s), "upload psi0");
+                    cuda_check(cudaMemcpyAsync(t->b.x.as<double>() + N, psi0_im, N * 8, cudaMemcpyHostToDevice, s),
+                               "upload psi0");
+                }
             }
             double* mapped_psi = nullptr;
             if (psi_re && p->columns) {
@@ -1325,12 +1438,18 @@ static bool run_full_locked(qsb_handle* h, const qsb_circuit* c, const double* p
                 cuda_check(cudaMemcpyAsync(vt[g].data() + static_cast<size_t>(rows) * N, v + plane + off * N,
                                            rows * N * 8, cudaMemcpyDeviceToHost, s), "download U");
             } else if (u_re) {
-                const double* v = p->b.v[p->final_buf].as<double>();
-                const size_t plane = static_cast<size_t>(p->M) * N;
-                cuda_check(cudaMemcpyAsync(u_re + p->row_begin * N, v + off * N, rows * N * 8,
-                                           cudaMemcpyDeviceToHost, s), "download U");
-                cuda_check(cudaMemcpyAsync(u_im + p->row_begin * N, v + plane + off * N, rows * N * 8,
-                                           cudaMemcpyDeviceToHost, s), "download U");
+                std::vector<const qsb_plan*> src;
+                for (auto& q : p->parts) src.push_back(q.get());
+                if (src.empty()) src.push_back(p);
+                for (const qsb_plan* q : src) {
+                    const double* v = q->b.v[q->final_buf].as<double>();
+                    const size_t plane = static_cast<size_t>(q->M) * N;
+                    const int64_t qoff = q->row_begin - q->eff_begin;
+                    cuda_check(cudaMemcpyAsync(u_re + q->row_begin * N, v + qoff * N, q->row_count * N * 8,
+                                               cudaMemcpyDeviceToHost, s), "download U");
+                    cuda_check(cudaMemcpyAsync(u_im + q->row_begin * N, v + plane + qoff * N, q->row_count * N * 8,
+                                               cudaMemcpyDeviceToHost, s), "download U");
+                }
             }
         }
         // the GPU is running: check the registry matrices of a reused plan meanwhile
@@ -1646,14 +1765,45 @@ qsb_status qsb_plan_set_initial_state(qsb_plan* plan, const double* re, const do
             cudaGraphExecDestroy(plan->graph);
             plan->graph = nullptr;
         }
-        cuda_check(cudaMemcpyAsync(plan->b.x.p, re, N * 8, cudaMemcpyDefault, s), "copy psi0");
-        cuda_check(cudaMemcpyAsync(plan->b.x.as<double>() + N, im, N * 8, cudaMemcpyDefault, s), "copy psi0");
+        std::vector<qsb_plan*> targets;
+        for (auto& q : plan->parts) targets.push_back(q.get());
+        if (targets.empty()) targets.push_back(plan);
+        for (qsb_plan* t : targets) {
+            t->x_is_e0 = false;
+            cuda_check(cudaMemcpyAsync(t->b.x.p, re, N * 8, cudaMemcpyDefault, s), "copy psi0");
+            cuda_check(cudaMemcpyAsync(t->b.x.as<double>() + N, im, N * 8, cudaMemcpyDefault, s), "copy psi0");
+        }
     });
 }
 
-qsb_status qsb_plan_unitary_device(const qsb_plan* plan, const double** re, const double** im) {
+qsb_status qsb_plan_unitary_device(const qsb_plan* cplan, const double** re, const double** im) {
     return guarded([&] {
-        if (!plan || !re || !im) raise(QSB_ERR_ARGUMENT, "null argument");
+        if (!cplan || !re || !im) raise(QSB_ERR_ARGUMENT, "null argument");
+        const qsb_plan* plan = cplan;
+        if (!plan->parts.empty()) {
+            // row-block parts keep their rows in their own buffers: assemble them (after the
+            // last execute; this synchronises the device) into one [2][rows][N] block
+            qsb_plan* p = const_cast<qsb_plan*>(cplan);
+            DeviceScope ds(p->dc->device);
+            cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+            const size_t N = static_cast<size_t>(p->N), rows = static_cast<size_t>(p->row_count);
+            p->b.v[0].ensure(2 * rows * N * 8);
+            double* dst = p->b.v[0].as<double>();
+            size_t off = 0;
+            for (const auto& q : p->parts) {
+                const double* v = q->b.v[q->final_buf].as<double>();
+                const size_t qoff = static_cast<size_t>(q->row_begin - q->eff_begin) * N;
+                const size_t qplane = static_cast<size_t>(q->M) * N;
+                const size_t bytes = static_cast<size_t>(q->row_count) * N * 8;
+                cuda_check(cudaMemcpy(dst + off * N, v + qoff, bytes, cudaMemcpyDeviceToDevice), "assemble U");
+                cuda_check(cudaMemcpy(dst + rows * N + off * N, v + qplane + qoff, bytes, cudaMemcpyDeviceToDevice),
+                           "assemble U");
+                off += static_cast<size_t>(q->row_count);
+            }
+            *re = dst;
+            *im = dst + rows * N;
+            return;
+        }
         const double* v = plan->b.v[plan->final_buf].as<double>();
         const size_t plane = static_cast<size_t>(plan->M) * plan->N;
         const size_t off = static_cast<size_t>(plan->row_begin - plan->eff_begin) * plan->N;
@@ -1791,7 +1941,7 @@ qsb_status qsb_plan_allgather_state(const qsb_plan* plan, qsb_comm* comm, double
 qsb_status qsb_plan_gemm_times(qsb_plan* plan, double* ms, int32_t* kinds, int32_t cap, int32_t* count) {
     return guarded([&] {
         if (!plan || !count) raise(QSB_ERR_ARGUMENT, "null argument");
-        if (!plan->per_gemm || !plan->timed_run || plan->small || plan->chain_k)
+        if (!plan->per_gemm || !plan->timed_run || plan->small || plan->chain_k || !plan->parts.empty())
             raise(QSB_ERR_ARGUMENT, "no per-GEMM timed execute on this plan (qsb_plan_set_timing mode 2, per-GEMM "
                                     "launches only: not the one-launch K2s / K2m / K2c chains)");
         const int G = static_cast<int>(plan->chain.size()) - 1;

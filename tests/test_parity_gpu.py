@@ -853,3 +853,57 @@ def test_chain_kernel_row_shards(monkeypatch, orc):
     re, im = orc.fsv(flat)
     assert rel_frob(psi.re, psi.im, re, im) <= TOL
     assert rel_frob(ur[:, 0], ui[:, 0], re, im) <= TOL
+
+
+@pytest.mark.parametrize("parts", ["2", "4"])
+@pytest.mark.parametrize("name,n", [("qft", 9), ("entangle", 10), ("deutsch-jozsa", 10), ("qft", 11)])
+def test_row_block_parts(monkeypatch, sim, orc, parts, name, n):
+    """QSB_PARTS: a plan's rows split into independent sub-plans whose chains run
+    concurrently on one device (fork / join streams, captured in the plan's CUDA
+    graph on reuse). psi, U (host API and the assembled device U) against the single
+    plan (1e-12) and the oracle (1e-10); psi0 != |0...0>; timing API."""
+    import torch
+
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+    from paper_2305_14398_b200.simulator import B200UnitarySimulator, torch_view
+
+    c, reg = q.make_named_circuit(name, n)
+    flat = native.flatten(c, reg)
+    N = 1 << n
+    whole = sim.build_unitary(flat)
+    monkeypatch.setenv("QSB_PARTS", parts)
+    s = B200UnitarySimulator(device=0)
+    u1 = s.build_unitary(flat)
+    u2 = s.build_unitary(flat)  # the cached plan (graph of the fork / join)
+    psi = s.simulate_full_state(flat)
+    assert np.array_equal(u1[0], u2[0]) and np.array_equal(u1[1], u2[1])
+    assert rel_frob(u1[0], u1[1], whole[0], whole[1]) <= 1e-12
+    re, im = orc.fsv(flat)
+    assert rel_frob(psi.re, psi.im, re, im) <= TOL
+    rng = np.random.default_rng(n)
+    v = rng.standard_normal(N) + 1j * rng.standard_normal(N)
+    v /= np.linalg.norm(v)
+    gen = s.simulate_from_state(flat, None, v.real, v.imag)
+    ore, oim = orc.fsv(flat, np.ascontiguousarray(v.real), np.ascontiguousarray(v.imag))
+    assert rel_frob(gen.re, gen.im, ore, oim) <= TOL
+    # device plan: assembled U rows, psi rows, timing
+    plan = s.plan(flat)
+    plan.set_timing(True)
+    plan.execute()
+    total, chain, mean = plan.last_timing()
+    assert total > 0 and chain > 0
+    plan.set_timing(False)
+    plan.execute()
+    torch.cuda.synchronize()
+    pr, pi = plan.unitary_device()
+    ur = torch_view(pr, (N, N)).cpu().numpy()
+    ui = torch_view(pi, (N, N)).cpu().numpy()
+    assert rel_frob(ur, ui, whole[0], whole[1]) <= 1e-12
+    dre = torch.empty(N, dtype=torch.float64, device="cuda")
+    dim = torch.empty(N, dtype=torch.float64, device="cuda")
+    plan.copy_state(dre.data_ptr(), dim.data_ptr())
+    torch.cuda.synchronize()
+    assert rel_frob(dre.cpu().numpy(), dim.cpu().numpy(), re, im) <= TOL
+    plan.close()
+    s.close()

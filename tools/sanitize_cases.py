@@ -42,6 +42,7 @@ CASES = {
     "k2_splitk2": (k2_circuit, 10, {"QSB_STREAMK": "0", "QSB_SPLITK": "2"}, native.GEMM_AUTO),
     "k2_splitk4": (k2_circuit, 10, {"QSB_STREAMK": "0", "QSB_SPLITK": "4"}, native.GEMM_AUTO),
     "k2_splitk8": (k2_circuit, 10, {"QSB_STREAMK": "0", "QSB_SPLITK": "8"}, native.GEMM_AUTO),
+    "k2_splitk4_nopdl": (k2_circuit, 10, {"QSB_STREAMK": "0", "QSB_SPLITK": "4", "QSB_NO_PDL": "1"}, native.GEMM_AUTO),
     "k2_n9_default": (k2_circuit, 9, {}, native.GEMM_AUTO),
     # every layer materialised / every layer generated
     "k2_mat_all": (k2_circuit, 9, {"QSB_MATERIALIZE": "1"}, native.GEMM_AUTO),
