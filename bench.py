@@ -221,7 +221,9 @@ def model_validation(workload: str):
     out = {"source": "profiles/cpu_pin.json (tools/cpu_pin.py: full reference unitary-parallel "
                      "simulate_full_state vs the model, same host cores)",
            "workloads": {r["workload"]: round(r["model_error"], 4) for r in rows},
-           "max_abs_error": max(errs) if errs else None}
+           "max_abs_error": max(errs) if errs else None,
+           "model_used_when": f"the model predicts more than {FULL_RUN_LIMIT_S:.0f} s (QFT-11 and up); below "
+                              "that the whole reference circuit is run and timed"}
     if workload in out["workloads"]:
         out["this_workload_error"] = out["workloads"][workload]
     return out

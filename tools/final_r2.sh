@@ -1,0 +1,27 @@
+#!/bin/bash
+# Round-2 evidence on one B200: GPU tests, smoke, the default bench line with its
+# CPU baseline, the reference arm, the BASELINE configs, the 8-way QFT-14 shard,
+# the default command's ncu launch list, the stream-K order A/B with DRAM bytes,
+# and the qubit sweep.
+TAG=${1:-R2e}
+O=gpurun_out/$TAG
+mkdir -p $O
+export PYTHONUNBUFFERED=1
+timeout 2400 python -m pytest tests -m gpu -q -s -p no:cacheprovider --timeout 900 > $O/pytest.log 2>&1; echo "exit $?" >> $O/pytest.log
+tail -2 $O/pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
+timeout 900 python bench.py --steps 20 --warmup 5 > $O/bench.json 2> $O/bench.err; echo "bench exit $?"
+timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > $O/bench_reference.json 2> $O/bench_reference.err; echo "ref exit $?"
+for w in entangle-10 dj-11 qft-4; do timeout 600 python bench.py --workload $w --steps 20 --warmup 5; done > $O/bench_configs.jsonl 2> $O/bench_configs.err
+for w in entangle-10 dj-11; do timeout 600 python bench.py --impl reference --workload $w --steps 5 --warmup 1; done > $O/bench_configs_reference.jsonl 2>&1
+timeout 900 python bench.py --workload qft-14 --virtual-ranks 8 --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_qft14_v8.json 2> $O/bench_qft14_v8.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_bench.log 2>&1; echo "ncu exit $?"
+timeout 900 python tools/env_ab.py qft:12,qft:11 "base:" "dp:QSB_SK_DP=1" > $O/sk_dp_ab.txt 2>&1
+for v in base dp; do
+  if [ $v = dp ]; then export QSB_SK_DP=1; else unset QSB_SK_DP; fi
+  timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+     -k regex:zgemm_ws_kernel -s 100 -c 6 --csv --log-file $O/dram_$v.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
+done
+unset QSB_SK_DP
+timeout 2400 python tools/sweep.py --out $O/sweep.md > $O/sweep.log 2>&1; echo "sweep exit $?"

@@ -44,20 +44,27 @@ def write_table(path, rows):
     with open(path, "w") as f:
         f.write("# Time per circuit vs qubits on one B200 (tools/sweep.py)\n\n")
         f.write("Device time per circuit (CUDA events, one plan execution; inputs resident). "
-                "dense = Algorithm 1 (unitary-b200, FP64 tensor cores; TFLOP/s credited 8N^3 per GEMM); "
-                "struct = unitary-structured-b200; fsv = fsv-b200; cpu = the reference library on the "
-                f"host's {os.cpu_count()} cores (measured n <= 8, extrapolated above from bounded samples).\n\n")
-        f.write("| circuit | n | GEMMs | dense ms | dense TFLOP/s | struct ms | fsv ms | cpu ms | dense speed-up vs cpu |\n")
-        f.write("|---|---|---|---|---|---|---|---|---|\n")
+                "dense = Algorithm 1 (unitary-b200, FP64 tensor cores): hw frac = the FLOPs the DMMAs execute "
+                "(6N^3 3M / 4N^3 real layer per GEMM) over the measured 37.1 TF/s DMMA peak; TFLOP/s credited "
+                "8N^3 per GEMM (ZGEMM convention); struct = unitary-structured-b200; fsv = fsv-b200; cpu = the "
+                f"reference library on the host's {os.cpu_count()} cores: the whole circuit run and timed where "
+                "the component model predicts <= 30 s (m), else the model extrapolated from bounded samples (x; "
+                "its error against full runs: profiles/cpu_pin.json).\n\n")
+        f.write("| circuit | n | GEMMs | dense ms | dense hw frac | dense TFLOP/s (credited) | struct ms | fsv ms | "
+                "cpu ms | dense speed-up vs cpu |\n")
+        f.write("|---|---|---|---|---|---|---|---|---|---|\n")
 
         def fmt(v, p=3):
             return "" if v is None else (f"{v:.{p}g}" if isinstance(v, float) else str(v))
 
         for r in rows:
             sp = (r["cpu_ms"] / r["dense_ms"]) if r.get("cpu_ms") and r.get("dense_ms") else None
+            cpu = fmt(r.get('cpu_ms'), 4)
+            if cpu:
+                cpu += " (m)" if r.get("cpu_full") else " (x)"
             f.write(f"| {r['circuit']} | {r['n']} | {fmt(r.get('gemms'))} | {fmt(r.get('dense_ms'), 4)} | "
-                    f"{fmt(r.get('dense_tflops'))} | {fmt(r.get('struct_ms'), 4)} | {fmt(r.get('fsv_ms'), 4)} | "
-                    f"{fmt(r.get('cpu_ms'), 4)} | {fmt(sp)} |\n")
+                    f"{fmt(r.get('dense_hw_frac'))} | {fmt(r.get('dense_tflops'))} | {fmt(r.get('struct_ms'), 4)} | "
+                    f"{fmt(r.get('fsv_ms'), 4)} | {cpu} | {fmt(sp)} |\n")
 
 
 def main():
@@ -88,6 +95,8 @@ def main():
                 ms = time_plan(p, stream, 1 if n >= 13 else 3)
                 row["dense_ms"] = ms
                 row["dense_tflops"] = p.info.gemm_flops / (ms * 1e-3) / 1e12 if p.info.n_gemms else None
+                row["dense_hw_frac"] = (p.info.gemm_hw_flops / (ms * 1e-3) / 1e12 / bench.FP64_DMMA_PEAK_TFLOPS
+                                        if p.info.n_gemms else None)
                 row["gemms"] = p.info.n_gemms
                 p.close()
             if n <= args.max_sv:
@@ -100,7 +109,9 @@ def main():
             # the reference registers a DJ oracle with its O(8^n) host is_unitary: bounded at n = 10
             if n <= (min(args.cpu_max, 10) if key == "dj" else args.cpu_max) and bench.oracle_available():
                 t0 = time.time()
-                row["cpu_ms"] = bench.cpu_sample_circuit(name, n)["value"]
+                cb = bench.cpu_sample_circuit(name, n)
+                row["cpu_ms"] = cb["value"]
+                row["cpu_full"] = cb.get("full_run", n <= 8)
                 row["cpu_wall_s"] = time.time() - t0
             rows.append(row)
             print(row, flush=True)
