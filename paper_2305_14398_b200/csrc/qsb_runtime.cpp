@@ -35,6 +35,8 @@
 #include "qsb_nccl.hpp"
 #include "qsb_sv.hpp"
 
+extern char** environ;
+
 namespace {
 
 using namespace qsbh;
@@ -1252,6 +1254,10 @@ static std::vector<char> plan_key(const qsb_circuit* c, int G, int flags) {
     }
     put(&c->n_functions, sizeof c->n_functions);
     for (int f = 0; f < c->n_functions; ++f) put(&c->functions[f].dim, sizeof(int64_t));
+    // the plan-time switches (QSB_* environment: tile, split-K, stream-K, materialisation ...)
+    // select kernels at plan time, so a changed switch must not reuse a plan built under another
+    for (char** e = environ; e && *e; ++e)
+        if (std::strncmp(*e, "QSB_", 4) == 0) put(*e, std::strlen(*e) + 1);
     return k;
 }
 

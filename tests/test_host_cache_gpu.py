@@ -98,3 +98,29 @@ def test_other_paths_drop_the_cache(orc):
     b = s.simulate_full_state(flat)
     assert np.array_equal(a.re, b.re) and np.array_equal(a.im, b.im)
     s.close()
+
+
+def test_plan_switch_change_is_a_new_plan():
+    """A QSB_* plan-time switch changed between calls must not reuse a plan built
+    under the old setting (the cache key carries the QSB_* environment)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import os, sys; sys.path.insert(0, %r)\n"
+        "import paper_2305_14398_b200 as q\n"
+        "from paper_2305_14398_b200 import native\n"
+        "from paper_2305_14398_b200.simulator import B200UnitarySimulator\n"
+        "c, reg = q.make_named_circuit('qft', 9); f = native.flatten(c, reg)\n"
+        "s = B200UnitarySimulator(device=0)\n"
+        "s.simulate_full_state(f); s.simulate_full_state(f)\n"
+        "os.environ['QSB_SPLITK'] = '4'\n"
+        "s.simulate_full_state(f); s.simulate_full_state(f)\n"
+        "s.close()\n" % root)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                       env=dict(os.environ, QSB_TRACE="1"))
+    assert r.returncode == 0, r.stderr
+    kinds = [ln.split()[3] for ln in r.stderr.splitlines() if ln.startswith("qsb trace:")]
+    assert kinds == ["new", "cached", "new", "cached"], r.stderr
