@@ -166,18 +166,21 @@ def cpu_sample_circuit(name: str, n: int, repeats: int = 2, allow_full: bool = T
         ref.L.refsh_set_worker_count(REF_THREADS)  # 0 = QSIM_THREADS unset: all host cores
         fold = min(ref.L.refsh_time_step_unitary(prog.h, single) for _ in range(max(1, repeats)))
         gemm_par = min(ref.L.refsh_time_matmul(rows_par, N, 1) for _ in range(max(1, repeats))) * N / rows_par
-        gemm_ser = (min(ref.L.refsh_time_matmul(rows_ser, N, 0) for _ in range(max(1, repeats))) * N / rows_ser
-                    if extra else 0.0)
+        # the serial layer product streams a 16 N^2-byte operand once per row on one thread:
+        # memory-bound and the noisiest component on a shared (KVM) host, so one more sample
+        ser_samples = ([ref.L.refsh_time_matmul(rows_ser, N, 0) * N / rows_ser for _ in range(max(1, repeats) + 1)]
+                       if extra else [])
+        gemm_ser = min(ser_samples) if ser_samples else 0.0
         total = (n_steps + extra) * fold + n_steps * gemm_par + extra * gemm_ser
         comps = {"fold": fold, "gemm_parallel": gemm_par, "gemm_serial": gemm_ser, "steps": n_steps,
-                 "extra_layers": extra, "model_s": total}
+                 "extra_layers": extra, "model_s": total, "gemm_serial_samples": ser_samples}
         if allow_full and total <= FULL_RUN_LIMIT_S:
             return {"value": cpu_full_run(name, n), "unit": "ms", "cores": cores, "kind": kind,
                     "sample": f"full reference UnitarySimulator::simulate_full_state of {workload} "
                               f"(unitary-parallel, {cores} threads, one run)",
                     "components_s": comps, "full_run": True}
         sample = (f"reference step_unitary(single-layer step) + matmul({rows_par}x{N} . {N}x{N}, Parallel, "
-                  f"{cores} threads) + matmul({rows_ser}x{N} . {N}x{N}, Serial), min of {repeats}; "
+                  f"{cores} threads) + matmul({rows_ser}x{N} . {N}x{N}, Serial), min of {repeats} ({repeats + 1} serial); "
                   f"extrapolated to {n_steps} steps + {extra} serial extra-layer GEMMs")
         return {"value": total * 1e3, "unit": "ms", "cores": cores, "kind": kind, "sample": sample,
                 "components_s": comps, "full_run": False}

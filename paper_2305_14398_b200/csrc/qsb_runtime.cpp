@@ -808,15 +808,17 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
             const int T = (p->M / rows_t) * (p->N / cols_t);
             const int KT = p->N / 16;
             const int P = qsb::ws_max_active_clusters(1);
-            // QSB_SK_DP=1: data-parallel waves first, the last one to two waves' worth of
-            // tiles stream-K. The CTAs of a wave share A row blocks in L2, so DRAM traffic
-            // drops to the algorithmic 0.78 GB per QFT-12 launch (from 25.8 GB: each CTA's
-            // contiguous tile range re-reads its row block) — yet the circuit runs 2 %
-            // slower (1025 vs 1004 ms, r73): the K2 stays FP64-tensor bound either way, so
-            // all-stream-K is the default.
-            int W = 0;
+            // Data-parallel waves first (CTA c takes whole tile w P + c in wave w), the last
+            // one to two waves' worth of tiles stream-K. The CTAs of a wave work on
+            // consecutive tiles at the same k, so they share A row blocks and B k-slices in
+            // L2: DRAM traffic of a QFT-12 real-layer launch 17.1 GB -> 0.27 GB read at the
+            // same time (7.69 vs 7.70 ms; QFT-12 997.7 vs 997.0 ms, QFT-11 106.2 vs 106.3 ms:
+            // profiles/R2e_sk_dp_ab.txt). All-stream-K order (each CTA a contiguous tile range,
+            // re-reading its row block per tile) stays selectable: QSB_SK_DP=0. (Round 1
+            // measured this hybrid 2 % slower, before the deferred stage release.)
+            int W = T % P == 0 ? T / P : std::max(0, T / P - 1);
             if (const char* e = std::getenv("QSB_SK_DP"))
-                if (*e && std::atoi(e) == 1) W = T % P == 0 ? T / P : std::max(0, T / P - 1);
+                if (*e && std::atoi(e) == 0) W = 0;
             const long long I = static_cast<long long>(T - W * P) * KT;
             const int per = static_cast<int>(std::max<long long>(1, I / P));
             p->sk.dp_waves = W;

@@ -193,3 +193,34 @@ def test_abi_rejects_bad_circuits():
     assert L.qsb_step_layer_count(flat.ptr, 5, ctypes.byref(n)) == 4  # ARGUMENT
     flat.c.n_qubits = 0
     assert L.qsb_step_layer_count(flat.ptr, 0, ctypes.byref(n)) == 4
+
+
+def test_state_planes_reject_mismatched_lengths():
+    """The C ABI carries no lengths: short or mismatched psi planes raise ShapeError
+    in the binding (the reference's matvec ShapeError, linalg.cpp:89-94) instead of
+    becoming a host out-of-bounds read."""
+    import numpy as np
+    import pytest
+
+    from paper_2305_14398_b200.errors import ShapeError
+    from paper_2305_14398_b200.simulator import _state_planes
+
+    re, im = _state_planes(np.ones(8), np.zeros(8), 8)
+    assert re.dtype == np.float64 and len(im) == 8
+    with pytest.raises(ShapeError, match="matvec: 8x8 times vector of length 4"):
+        _state_planes(np.ones(4), np.zeros(4), 8)
+    with pytest.raises(ShapeError):
+        _state_planes(np.ones(8), np.zeros(7))
+
+
+def test_gather_state_rejects_column_block_plans():
+    """Column-block shares are summed, not gathered."""
+    import pytest
+
+    from paper_2305_14398_b200.sharding import gather_state
+
+    class ColumnPlan:
+        columns = True
+
+    with pytest.raises(ValueError, match="row-block"):
+        gather_state(ColumnPlan(), None, None, 0, 4, 2)
