@@ -73,6 +73,12 @@ def parse():
     return ap.parse_args()
 
 
+def mode_of(args) -> int:
+    from paper_2305_14398_b200 import native
+
+    return {"auto": native.GEMM_AUTO, "4m": native.GEMM_4M, "3m": native.GEMM_3M}[args.gemm_mode]
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -371,7 +377,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     name, n = WORKLOADS[args.workload]
     N = 1 << n
-    mode = {"auto": native.GEMM_AUTO, "4m": native.GEMM_4M, "3m": native.GEMM_3M}[args.gemm_mode]
+    mode = mode_of(args)
     sim = B200UnitarySimulator(device=local, gemm_mode=mode)
     c, reg = q.make_named_circuit(name, n)
     flat = native.flatten(c, reg)
@@ -468,10 +474,11 @@ def run_ours(args):
         plan = None
     e2e_clocks = None
     if vr > 1:
-        e2e_ms, h2d, d2h, e2e_calls = None, 0, 0, 0  # the projection times one shard, not a full circuit
+        e2e_ms, h2d, d2h, e2e_calls, e2e_cached = None, 0, 0, 0, None  # the projection times one shard
     else:
         with ClockSampler(local, "e2e") as eclk:
-            e2e_ms, h2d, d2h, e2e_calls = e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr)
+            e2e_ms, h2d, d2h, e2e_calls, e2e_cached = e2e_measure(sim, flat, args, world, rank, N, begin, count,
+                                                                   s_ptr)
         e2e_clocks = eclk.summary()
 
     if rank == 0:
@@ -514,6 +521,9 @@ def run_ours(args):
                                         "profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no FP64 entry"},
             "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "calls_timed": e2e_calls,
+                    "cold_call": "every call compiles the circuit and uploads its descriptors (QSB_FLAG_NO_PLAN_CACHE)"
+                                 if world == 1 else "every step creates the rank's plan, executes, all-gathers, D2H",
+                    "value_plan_cached": e2e_cached,
                     "api": "qsb_simulate_full_state (C ABI)" if world == 1 else
                            "qsb_plan_create/execute + NCCL all-gather + D2H",
                     "clocks": e2e_clocks},
@@ -579,20 +589,33 @@ def e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr):
     d2h = 16 * N
     steps = max(1, min(args.steps, 3))
     if world == 1:
+        from paper_2305_14398_b200.simulator import B200UnitarySimulator
+
         re = np.empty(N)
         im = np.empty(N)
         L = native.lib()
-        t0 = time.perf_counter()
-        native.check(L.qsb_simulate_full_state(sim._h, flat.ptr, native.dptr(re), native.dptr(im)))
-        first = time.perf_counter() - t0
-        # as many calls as --steps within ~20 s (at least 3): run_bench's repeated calls
-        steps = max(3, min(args.steps, int(20.0 / max(first, 1e-6))))
-        times = []
-        for _ in range(steps):
+
+        def timed_calls(handle):
             t0 = time.perf_counter()
-            native.check(L.qsb_simulate_full_state(sim._h, flat.ptr, native.dptr(re), native.dptr(im)))
-            times.append((time.perf_counter() - t0) * 1e3)
-        return sum(times) / len(times), h2d, d2h, len(times)
+            native.check(L.qsb_simulate_full_state(handle, flat.ptr, native.dptr(re), native.dptr(im)))
+            first = time.perf_counter() - t0
+            # as many calls as --steps within ~20 s (at least 3): run_bench's repeated calls
+            reps = max(3, min(args.steps, int(20.0 / max(first, 1e-6))))
+            times = []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                native.check(L.qsb_simulate_full_state(handle, flat.ptr, native.dptr(re), native.dptr(im)))
+                times.append((time.perf_counter() - t0) * 1e3)
+            return sum(times) / len(times), len(times)
+
+        # headline: every call compiles the circuit and uploads its descriptors / registry
+        # tables (QSB_FLAG_NO_PLAN_CACHE); beside it the repeated-call cost with the handle's
+        # plan cache (compiled plan reused, registry contents re-checked on the host)
+        cold = B200UnitarySimulator(device=sim.device, gemm_mode=mode_of(args), flags=native.FLAG_NO_PLAN_CACHE)
+        cold_ms, calls = timed_calls(cold._h)
+        cold.close()
+        cached_ms, _ = timed_calls(sim._h)
+        return cold_ms, h2d, d2h, calls, cached_ms
     psi_re = torch.empty(N, dtype=torch.float64, device="cuda")
     psi_im = torch.empty(N, dtype=torch.float64, device="cuda")
     host = torch.empty(2, N, dtype=torch.float64, pin_memory=True)
@@ -614,7 +637,7 @@ def e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr):
         t = torch.tensor([dt], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         times.append(float(t.item()))
-    return sum(times) / len(times), h2d, d2h, len(times)
+    return sum(times) / len(times), h2d, d2h, len(times), None
 
 
 # --------------------------------------------------------------- state-vector engine arms

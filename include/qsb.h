@@ -130,6 +130,8 @@ enum {
                                      [row_begin, row_begin + row_count) of U, its unitary buffer
                                      holds U[:, cols]^T and its state buffer the full-length share
                                      U[:, cols] psi0[cols] (2^n entries per plane) */
+    QSB_FLAG_NO_PLAN_CACHE = 16,  /* host-API calls compile and upload every call (no reuse of the last
+                                     call's plans): the cold-call cost */
     QSB_FLAG_NCCL_GATHER = 8      /* host-API calls all-gather the shards' psi rows over NCCL into a
                                      device-resident psi on every device even when the handle has a
                                      single device (a one-rank communicator; tests). With several
@@ -289,6 +291,11 @@ qsb_status qsb_nccl_version(int32_t* version);
  * rows [r * 2^n / n_ranks, (r + 1) * 2^n / n_ranks) (row blocks, not column blocks). */
 qsb_status qsb_plan_allgather_state(const qsb_plan* plan, qsb_comm* comm, double* psi_re, double* psi_im,
                                     void* stream);
+
+/* The optional second exchange of SURVEY 8(e): all-gather every rank's rows of U into
+ * full 2^n x 2^n device planes on every rank (16 N^2 / G bytes sent per rank), async. */
+qsb_status qsb_plan_allgather_unitary(const qsb_plan* plan, qsb_comm* comm, double* u_re, double* u_im,
+                                      void* stream);
 
 /* Kernel timing of the last execute, from CUDA events on the launching stream:
  * total, the K2 GEMM chain, and the mean single-GEMM duration (ms). Synchronises. */

@@ -829,6 +829,27 @@ __device__ __forceinline__ void ws_consume_stage(uint32_t aRe, uint32_t aIm, uin
     }
 }
 
+// Output tile of linear tile index t. group_m = 0: row-major. group_m = G > 0: tiles
+// are numbered group by group, a group being G row blocks x all column blocks walked
+// column by column (G row blocks per column), so the tiles of one data-parallel wave
+// (P consecutive indices) cover G row blocks x ~P/G column blocks instead of ~2 row
+// blocks x every column block: each wave re-reads ~P/G B column blocks instead of all
+// of them, and the group's G A row blocks stay in L2 across its waves.
+__device__ __forceinline__ void sk_tile_coords(int t, int tiles_n, int group_m, int tiles_m, int& tm, int& tn) {
+    if (group_m <= 1) {
+        tm = t / tiles_n;
+        tn = t % tiles_n;
+        return;
+    }
+    const int per_group = group_m * tiles_n;
+    const int g = t / per_group;
+    const int first = g * group_m;
+    const int rows = min(group_m, tiles_m - first);  // the last group may be shorter
+    const int r = t - g * per_group;
+    tm = first + r % rows;
+    tn = r / rows;
+}
+
 // MAT_B: the operator was materialised (transposed, [planes][N][N], by
 // expand_t_kernel) and B tiles arrive by TMA like A — no FP64 generation work
 // in the producer, whose FP64 instructions would otherwise queue behind DMMA on
@@ -917,8 +938,10 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
         int seg = 0, tile, seg_k0, seg_k1;
         long long it = it_begin;
         while (next_segment(seg, it, tile, seg_k0, seg_k1)) {
-        const int m0 = (tile / tiles_n) * BM;
-        const int n0 = (tile % tiles_n) * BN;
+        int tm, tn;
+        sk_tile_coords(tile, tiles_n, sk.enabled ? sk.group_m : 0, M / BM, tm, tn);
+        const int m0 = tm * BM;
+        const int n0 = tn * BN;
         for (int ktg = seg_k0; ktg < seg_k1; ++ktg, ++kc) {
             const int s = kc % C::STAGES;
             if (kc >= C::STAGES) mbar_wait(sEmpty + 8 * s, ((kc / C::STAGES) & 1) ^ 1);
@@ -970,8 +993,10 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
     int seg = 0, tile, seg_k0, seg_k1;
     long long it = it_begin;
     while (next_segment(seg, it, tile, seg_k0, seg_k1)) {
-    const int m0 = (tile / tiles_n) * BM;
-    const int n0 = (tile % tiles_n) * BN;
+    int tm, tn;
+    sk_tile_coords(tile, tiles_n, sk.enabled ? sk.group_m : 0, M / BM, tm, tn);
+    const int m0 = tm * BM;
+    const int n0 = tn * BN;
     double acc[NACC][4][NT][2];
 #pragma unroll
     for (int a = 0; a < NACC; ++a)

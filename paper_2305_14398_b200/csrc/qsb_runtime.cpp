@@ -437,6 +437,8 @@ void upload_tables(qsb_plan* p, const qsb_circuit* c) {
 
 // K2c by default (QSB_CHAIN=1 / 0 force it on / off)
 constexpr bool kChainDefault = false;
+// Row blocks per group of the stream-K / data-parallel tile numbering (QSB_SK_GROUP; 0 = row-major)
+constexpr int kSkGroup = 0;
 // Row-block parts per plan by default (QSB_PARTS forces a count)
 int kPartsDefault(int64_t N) { return N <= 0 ? 1 : 1; }
 
@@ -823,6 +825,13 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
             const int per = static_cast<int>(std::max<long long>(1, I / P));
             p->sk.dp_waves = W;
             p->sk.enabled = 1;
+            // grouped tile numbering (sk_tile_coords): a wave spans kSkGroup row blocks, so
+            // materialised B column blocks are re-read per wave ~P / kSkGroup times, not ~tiles_n
+            {
+                int gm = kSkGroup;
+                if (const char* e = std::getenv("QSB_SK_GROUP")) gm = std::max(0, std::atoi(e));
+                p->sk.group_m = gm;
+            }
             p->sk.tiles_n = p->N / cols_t;
             p->sk.tiles = T;
             p->sk.maxc = I > 0 ? (KT + per - 1) / per + 1 : 1;
@@ -1360,7 +1369,8 @@ static bool run_full_locked(qsb_handle* h, const qsb_circuit* c, const double* p
     std::vector<char> key = plan_key(c, G, h->flags);
     if (c->n_steps > 0)  // (a hit skips compile(), which checks every operation)
         for (int i = c->step_offsets[0]; i < c->step_offsets[c->n_steps]; ++i) check_op(c, c->ops[i]);
-    const bool hit = allow_hit && !h->cached.empty() && h->cache_key == key;
+    const bool no_cache = (h->flags & QSB_FLAG_NO_PLAN_CACHE) != 0;
+    const bool hit = allow_hit && !no_cache && !h->cached.empty() && h->cache_key == key;
     if (!hit) {
         drop_plan_cache(h);
         try {
@@ -1371,7 +1381,7 @@ static bool run_full_locked(qsb_handle* h, const qsb_circuit* c, const double* p
             throw;
         }
         h->cache_key = std::move(key);
-        keep_functions(h, c);
+        if (!no_cache) keep_functions(h, c);
         h->drop_cache = drop_plan_cache;
     }
     std::vector<qsb_plan*>& plans = h->cached;
@@ -1525,6 +1535,7 @@ static bool run_full_locked(qsb_handle* h, const qsb_circuit* c, const double* p
         drop_plan_cache(h);
         throw;
     }
+    if (no_cache) drop_plan_cache(h);
     return true;
 }
 
@@ -1965,6 +1976,36 @@ qsb_status qsb_plan_gemm_times(qsb_plan* plan, double* ms, int32_t* kinds, int32
             }
             if (kinds) kinds[i] = plan->gemm_kind[i + 1];
         }
+    });
+}
+
+qsb_status qsb_plan_allgather_unitary(const qsb_plan* plan, qsb_comm* comm, double* u_re, double* u_im,
+                                      void* stream) {
+    return guarded([&] {
+        if (!plan || !comm || !u_re || !u_im) raise(QSB_ERR_ARGUMENT, "null argument");
+        if (plan->columns) raise(QSB_ERR_ARGUMENT, "all-gather needs row-block plans");
+        if (!plan->parts.empty()) raise(QSB_ERR_ARGUMENT, "all-gather of U needs a plan without row-block parts");
+        if (plan->dc->device != comm->device)
+            raise(QSB_ERR_ARGUMENT, "plan on device %d, communicator on device %d", plan->dc->device, comm->device);
+        const int64_t N = plan->N;
+        if (plan->row_count * comm->n_ranks != N || plan->row_begin != comm->rank * plan->row_count)
+            raise(QSB_ERR_ARGUMENT, "rank %d of %d must own rows [%lld, +%lld)", comm->rank, comm->n_ranks,
+                  static_cast<long long>(comm->rank * (N / comm->n_ranks)), static_cast<long long>(N / comm->n_ranks));
+        if (plan->small) raise(QSB_ERR_ARGUMENT, "the one-launch chains (N <= 256) keep no U rows");
+        const NcclApi& nc = nccl_or_raise();
+        DeviceScope ds(plan->dc->device);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->dc->stream;
+        const double* v = plan->b.v[plan->final_buf].as<double>();
+        const size_t plane = static_cast<size_t>(plan->M) * N;
+        const size_t off = static_cast<size_t>(plan->row_begin - plan->eff_begin) * N;
+        const size_t count = static_cast<size_t>(plan->row_count) * N;
+        auto c = static_cast<ncclComm_t>(comm->comm);
+        nccl_check(nc.group_start(), "ncclGroupStart");
+        ncclResult_t r = nc.all_gather(v + off, u_re, count, ncclFloat64, c, s);
+        if (r == ncclSuccess) r = nc.all_gather(v + plane + off, u_im, count, ncclFloat64, c, s);
+        const ncclResult_t end = nc.group_end();
+        nccl_check(r, "ncclAllGather (U rows)");
+        nccl_check(end, "ncclGroupEnd");
     });
 }
 

@@ -29,7 +29,7 @@ assert OP_DTYPE.itemsize == 104
 
 OP_GATE, OP_CONTROL, OP_FUNCTION, OP_INSTRUCTION = 0, 1, 2, 3
 GEMM_AUTO, GEMM_4M, GEMM_3M = 0, 1, 2
-FLAG_NO_GRAPH, FLAG_MATERIALIZE, FLAG_COLUMN_BLOCKS, FLAG_NCCL_GATHER = 1, 2, 4, 8
+FLAG_NO_GRAPH, FLAG_MATERIALIZE, FLAG_COLUMN_BLOCKS, FLAG_NCCL_GATHER, FLAG_NO_PLAN_CACHE = 1, 2, 4, 8, 16
 NCCL_ID_BYTES = 128
 TILE_NAMES = {0: "zgemm_gen_kernel<128,64> (4M)", 1: "zgemm_gen_kernel<64,64> (4M)", 2: "zgemm_gen_kernel<32,32> (4M)",
               3: "zgemm_ws_kernel<4M>", 4: "zgemm_ws_kernel<3M>", 5: "zgemm_ws_kernel<3M, sum plane>",
@@ -207,6 +207,7 @@ def lib() -> ctypes.CDLL:
         "qsb_comm_create": (ctypes.c_int, [P, P, I32, I32, P]),
         "qsb_comm_destroy": (ctypes.c_int, [P]),
         "qsb_plan_allgather_state": (ctypes.c_int, [P, P, P, P, P]),
+        "qsb_plan_allgather_unitary": (ctypes.c_int, [P, P, P, P, P]),
         "qsb_collapse": (ctypes.c_int, [P, P, P, I64, U64, P]),
         "qsb_is_unitary": (ctypes.c_int, [P, P, P, I64, D, P, P]),
         "qsb_fsv_qubit_guard": (ctypes.c_int, [P, P]),

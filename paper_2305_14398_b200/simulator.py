@@ -101,6 +101,11 @@ class Plan:
                                                       ctypes.byref(count)))
         return ms[:count.value].tolist(), kinds[:count.value].tolist()
 
+    def allgather_unitary(self, comm: "Comm", dst_re_ptr: int, dst_im_ptr: int, stream: int = 0) -> None:
+        """ncclAllGather of every rank's rows of U into full N x N device planes (qsb_plan_allgather_unitary)."""
+        native.check(native.lib().qsb_plan_allgather_unitary(self._p, comm._c, dst_re_ptr, dst_im_ptr,
+                                                             stream or None))
+
     def allgather_state(self, comm: "Comm", dst_re_ptr: int, dst_im_ptr: int, stream: int = 0) -> None:
         """ncclAllGather of every rank's psi rows into full-length device planes (qsb_plan_allgather_state)."""
         native.check(native.lib().qsb_plan_allgather_state(self._p, comm._c, dst_re_ptr, dst_im_ptr, stream or None))

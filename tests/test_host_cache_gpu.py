@@ -102,7 +102,8 @@ def test_other_paths_drop_the_cache(orc):
 
 def test_plan_switch_change_is_a_new_plan():
     """A QSB_* plan-time switch changed between calls must not reuse a plan built
-    under the old setting (the cache key carries the QSB_* environment)."""
+    under the old setting (the cache key carries the QSB_* environment), and a
+    QSB_FLAG_NO_PLAN_CACHE handle compiles every call (the bench's cold e2e)."""
     import os
     import subprocess
     import sys
@@ -118,9 +119,12 @@ def test_plan_switch_change_is_a_new_plan():
         "s.simulate_full_state(f); s.simulate_full_state(f)\n"
         "os.environ['QSB_SPLITK'] = '4'\n"
         "s.simulate_full_state(f); s.simulate_full_state(f)\n"
-        "s.close()\n" % root)
+        "s.close()\n"
+        "cold = B200UnitarySimulator(device=0, flags=native.FLAG_NO_PLAN_CACHE)\n"
+        "cold.simulate_full_state(f); cold.simulate_full_state(f)\n"
+        "cold.close()\n" % root)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
                        env=dict(os.environ, QSB_TRACE="1"))
     assert r.returncode == 0, r.stderr
     kinds = [ln.split()[3] for ln in r.stderr.splitlines() if ln.startswith("qsb trace:")]
-    assert kinds == ["new", "cached", "new", "cached"], r.stderr
+    assert kinds == ["new", "cached", "new", "cached", "new", "new"], r.stderr

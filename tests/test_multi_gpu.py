@@ -67,6 +67,14 @@ def test_comm_allgather_one_rank(orc):
     assert torch.equal(re, re2) and torch.equal(im, im2)
     o_re, o_im = orc.fsv(flat)
     assert rel(re.cpu().numpy(), im.cpu().numpy(), o_re, o_im) <= 1e-10
+    # the optional U all-gather: the one rank's rows are the whole U
+    ur = torch.empty(N * N, dtype=torch.float64, device="cuda")
+    ui = torch.empty_like(ur)
+    plan.allgather_unitary(comm, ur.data_ptr(), ui.data_ptr())
+    torch.cuda.synchronize()
+    want = sim.build_unitary(flat)
+    assert np.array_equal(ur.cpu().numpy().reshape(N, N), want[0])
+    assert np.array_equal(ui.cpu().numpy().reshape(N, N), want[1])
     # a plan that does not own rank 0's block of a 2-rank split is refused
     with pytest.raises(Exception, match="must own rows"):
         half = sim.plan(flat, None, N // 2, N // 2)

@@ -907,3 +907,27 @@ def test_row_block_parts(monkeypatch, sim, orc, parts, name, n):
     assert rel_frob(dre.cpu().numpy(), dim.cpu().numpy(), re, im) <= TOL
     plan.close()
     s.close()
+
+
+@pytest.mark.parametrize("group", ["5", "16"])
+@pytest.mark.parametrize("name,n", [("qft", 11), ("deutsch-jozsa", 11), ("entangle", 11)])
+def test_grouped_tile_numbering(monkeypatch, sim, orc, group, name, n):
+    """QSB_SK_GROUP: the data-parallel / stream-K tiles numbered group by group of row
+    blocks (a short last group with 5) — U within 1e-12 of the row-major numbering,
+    psi against the oracle."""
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+    from paper_2305_14398_b200.simulator import B200UnitarySimulator
+
+    c, reg = q.make_named_circuit(name, n)
+    flat = native.flatten(c, reg)
+    monkeypatch.setenv("QSB_SK_GROUP", "0")
+    base = sim.build_unitary(flat)
+    monkeypatch.setenv("QSB_SK_GROUP", group)
+    s = B200UnitarySimulator(device=0)
+    u = s.build_unitary(flat)
+    psi = s.simulate_full_state(flat)
+    s.close()
+    assert rel_frob(u[0], u[1], base[0], base[1]) <= 1e-12
+    re, im = orc.fsv(flat)
+    assert rel_frob(psi.re, psi.im, re, im) <= TOL
