@@ -216,6 +216,24 @@ def cpu_sample_circuit(name: str, n: int, repeats: int = 2, allow_full: bool = T
             "full_run": False}
 
 
+def cpu_sample_subprocess(workload: str):
+    """cpu_sample in a fresh process that never imports torch or touches the GPU: the
+    reference's memory-bound serial products run up to 1.3-2x slower inside a process
+    that has loaded torch and run GPU work (measured on this image), which would flatter
+    the GPU; the reference arm (--impl reference) runs in such a clean process too."""
+    name, n = WORKLOADS[workload]
+    return cpu_circuit_subprocess(name, n)
+
+
+def cpu_circuit_subprocess(name: str, n: int):
+    code = ("import json, sys; sys.path.insert(0, %r); import bench; "
+            "print(json.dumps(bench.cpu_sample_circuit(%r, %d)))" % (ROOT, name, n))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=3600)
+    if out.returncode != 0:
+        raise RuntimeError(f"cpu baseline subprocess failed: {out.stderr[-2000:]}")
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
 def model_validation(workload: str):
     """Measured error of the extrapolation model against full reference runs on a
     GPU box's host (tools/cpu_pin.py -> profiles/cpu_pin.json)."""
@@ -542,7 +560,7 @@ def run_ours(args):
                           "independent work (row blocks, operators regenerated locally); excludes the "
                           f"NCCL all-gather of psi ({16 * N // vr} bytes per rank)"}
         if world == 1 and vr == 1 and not args.no_cpu_baseline:
-            cb = cpu_sample(args.workload)
+            cb = cpu_sample_subprocess(args.workload)
             cb["extrapolated"] = not cb.get("full_run", True) if "components_s" in cb else False
             if cb["extrapolated"]:
                 cb["model_validation"] = model_validation(args.workload)

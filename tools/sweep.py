@@ -109,7 +109,7 @@ def main():
             # the reference registers a DJ oracle with its O(8^n) host is_unitary: bounded at n = 10
             if n <= (min(args.cpu_max, 10) if key == "dj" else args.cpu_max) and bench.oracle_available():
                 t0 = time.time()
-                cb = bench.cpu_sample_circuit(name, n)
+                cb = bench.cpu_circuit_subprocess(name, n)  # a torch-free process, like the reference's own
                 row["cpu_ms"] = cb["value"]
                 row["cpu_full"] = cb.get("full_run", n <= 8)
                 row["cpu_wall_s"] = time.time() - t0
