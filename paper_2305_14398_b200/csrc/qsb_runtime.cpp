@@ -303,6 +303,7 @@ struct qsb_plan {
     int tile = qsb::kTile32x32;
     int splits = 1;  // K2 split-K cluster size (warp-specialised tiles)
     bool streamk = false;  // K2 stream-K schedule (warp-specialised tiles)
+    int sk_group = 0;      // grouped tile numbering for GEMMs with a materialised B operand
     bool chain_k = false;  // K2c: every GEMM in one persistent dataflow launch
     int chain_splits = 1;
     // Row-block parts on one device: the plan's rows split into independent sub-plans
@@ -437,8 +438,9 @@ void upload_tables(qsb_plan* p, const qsb_circuit* c) {
 
 // K2c by default (QSB_CHAIN=1 / 0 force it on / off)
 constexpr bool kChainDefault = false;
-// Row blocks per group of the stream-K / data-parallel tile numbering (QSB_SK_GROUP; 0 = row-major)
-constexpr int kSkGroup = 0;
+// Row blocks per group of the stream-K / data-parallel tile numbering of GEMMs with a
+// materialised B operand (QSB_SK_GROUP; 0 = row-major)
+constexpr int kSkGroup = 16;
 // Row-block parts per plan by default (QSB_PARTS forces a count)
 int kPartsDefault(int64_t N) { return N <= 0 ? 1 : 1; }
 
@@ -825,12 +827,16 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
             const int per = static_cast<int>(std::max<long long>(1, I / P));
             p->sk.dp_waves = W;
             p->sk.enabled = 1;
-            // grouped tile numbering (sk_tile_coords): a wave spans kSkGroup row blocks, so
-            // materialised B column blocks are re-read per wave ~P / kSkGroup times, not ~tiles_n
+            // grouped tile numbering (sk_tile_coords) for GEMMs that stream a materialised B
+            // operand: a wave spans kSkGroup row blocks and ~P / kSkGroup B column blocks instead
+            // of ~2 row blocks and every column block (QFT-12 3M launch: DRAM read 12.7 -> 6.3 GB
+            // at the same duration, profiles/R2g_group_ab.md); generated-B GEMMs keep row-major
+            // waves, whose 64 CTAs per row block share A best (set per launch in enqueue)
             {
                 int gm = kSkGroup;
                 if (const char* e = std::getenv("QSB_SK_GROUP")) gm = std::max(0, std::atoi(e));
-                p->sk.group_m = gm;
+                p->sk_group = gm;
+                p->sk.group_m = 0;
             }
             p->sk.tiles_n = p->N / cols_t;
             p->sk.tiles = T;
@@ -1020,6 +1026,7 @@ void enqueue(qsb_plan* p, cudaStream_t s) {
         a.tmap_b_real = &p->tmap_b_real;
         a.splits = p->splits;
         a.sk = p->sk;  // flags start at zero and every owner re-arms its own (no memset between GEMMs)
+        a.sk.group_m = mat ? p->sk_group : 0;
         const bool gt = ev && p->per_gemm;
         if (gt) cuda_check(cudaEventRecord(p->gev[2 * (i - 1)], s), "event");
         cuda_check(qsb::launch_zgemm(a, p->tile, p->h->gemm_mode, s), "zgemm_gen_kernel");
