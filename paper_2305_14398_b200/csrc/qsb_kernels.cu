@@ -922,13 +922,12 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         if (MAT_B) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     }
+    __syncthreads();  // barriers initialised (synccheck's report at this barrier)
     // Programmatic dependent launch: everything above overlapped the previous
     // GEMM's tail; from here on we read its output (A) and overwrite its input
-    // (out), so wait for its completion. Then let the next GEMM start launching.
+    // (out), so every thread waits for its completion. Then let the next GEMM start launching.
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    __syncwarp();  // converged at the aligned CTA barrier (synccheck flagged lanes leaving griddepcontrol.wait apart)
-    __syncthreads();
 
     if (warp >= C::CONSUMER_WARPS) {
         // ------------------------------ producer warpgroup

@@ -3,7 +3,7 @@
 # CPU baseline, the reference arm, the BASELINE configs, the 8-way QFT-14 shard,
 # the default command's ncu launch list, the stream-K order A/B with DRAM bytes,
 # and the qubit sweep.
-TAG=${1:-R2e}
+TAG=${1:-R2z}
 O=gpurun_out/$TAG
 mkdir -p $O
 export PYTHONUNBUFFERED=1
@@ -17,11 +17,7 @@ for w in entangle-10 dj-11; do timeout 600 python bench.py --impl reference --wo
 timeout 900 python bench.py --workload qft-14 --virtual-ranks 8 --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_qft14_v8.json 2> $O/bench_qft14_v8.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_bench.log 2>&1; echo "ncu exit $?"
-timeout 900 python tools/env_ab.py qft:12,qft:11 "base:" "dp:QSB_SK_DP=1" > $O/sk_dp_ab.txt 2>&1
-for v in base dp; do
-  if [ $v = dp ]; then export QSB_SK_DP=1; else unset QSB_SK_DP; fi
-  timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-     -k regex:zgemm_ws_kernel -s 100 -c 6 --csv --log-file $O/dram_$v.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
-done
-unset QSB_SK_DP
+timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
+   -k 'regex:zgemm_ws_kernel<\(bool\)1, \(bool\)1, \(bool\)1, \(bool\)0>' -s 20 -c 1 -o $O/k2_3m_qft12 \
+   python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/ncu_3m.log 2>&1; echo "ncu full exit $?"
 timeout 2400 python tools/sweep.py --out $O/sweep.md > $O/sweep.log 2>&1; echo "sweep exit $?"
