@@ -81,6 +81,60 @@ uint64_t engine_bytes(int n) {  // two V buffers + psi + x
 
 // ---------------------------------------------------------------- compile
 
+// One pass over a registered matrix (rows in parallel chunks on the host's cores):
+// whether any entry has a nonzero imaginary part (the layer is real), and whether
+// every row has at most one nonzero — then per row its column (or -1) and value,
+// the per-row (column, value) layout the generator reads for monomial blocks (a
+// DJ oracle: 2^n entries instead of 4^n).
+struct FnInfo {
+    bool has_im = false;
+    bool mono = false;
+    std::vector<int32_t> cols;
+    std::vector<double> vre, vim;
+};
+
+FnInfo analyse_function(const qsb_function& fn, bool force_dense) {
+    FnInfo out;
+    const size_t d = static_cast<size_t>(fn.dim);
+    out.cols.assign(d, -1);
+    out.vre.assign(d, 0.0);
+    out.vim.assign(d, 0.0);
+    const size_t workers = d >= 512 ? std::min<size_t>(16, std::max(1u, std::thread::hardware_concurrency())) : 1;
+    std::vector<char> im(workers, 0), multi(workers, 0);
+    auto scan = [&](size_t w) {
+        const size_t r0 = d * w / workers, r1 = d * (w + 1) / workers;
+        bool any_im = false, many = false;
+        for (size_t r = r0; r < r1; ++r) {
+            const double* re = fn.re + r * d;
+            const double* ip = fn.im + r * d;
+            for (size_t k = 0; k < d; ++k) {
+                const double a = re[k], b = ip[k];
+                any_im = any_im || b != 0.0;
+                if (a == 0.0 && b == 0.0) continue;
+                if (out.cols[r] >= 0) {
+                    many = true;
+                    continue;
+                }
+                out.cols[r] = static_cast<int32_t>(k);
+                out.vre[r] = a;
+                out.vim[r] = b;
+            }
+        }
+        im[w] = any_im;
+        multi[w] = many;
+    };
+    if (workers <= 1) {
+        scan(0);
+    } else {
+        std::vector<std::thread> pool;
+        for (size_t w = 0; w < workers; ++w) pool.emplace_back(scan, w);
+        for (auto& t : pool) t.join();
+    }
+    out.has_im = std::any_of(im.begin(), im.end(), [](char v) { return v != 0; });
+    out.mono = !force_dense && std::none_of(multi.begin(), multi.end(), [](char v) { return v != 0; });
+    return out;
+}
+
 struct Compiled {
     int n = 0;
     uint32_t N = 0;
@@ -89,6 +143,7 @@ struct Compiled {
     std::vector<int> app_step;           // step of each layer
     std::vector<int> app_index;          // layer index within its step
     std::vector<int> used_functions;     // function indices referenced
+    std::vector<FnInfo> fn;              // analyse_function of every used function (by index)
 };
 
 struct Interval {
@@ -150,25 +205,9 @@ std::vector<int> first_fit(const qsb_circuit* c, int step, int* n_layers) {
     return layer;
 }
 
-// Every entry exactly zero? Large planes are scanned in parallel chunks.
-bool all_zero(const double* x, size_t n) {
-    auto chunk = [x](size_t b, size_t e) {
-        for (size_t i = b; i < e; ++i)
-            if (x[i] != 0.0) return false;
-        return true;
-    };
-    const size_t workers = n >= (size_t{1} << 20) ? std::min<size_t>(16, std::max(1u, std::thread::hardware_concurrency())) : 1;
-    if (workers <= 1) return chunk(0, n);
-    std::vector<char> ok(workers, 1);
-    std::vector<std::thread> pool;
-    for (size_t w = 0; w < workers; ++w)
-        pool.emplace_back([&, w] { ok[w] = chunk(n * w / workers, n * (w + 1) / workers); });
-    for (auto& t : pool) t.join();
-    return std::all_of(ok.begin(), ok.end(), [](char v) { return v != 0; });
-}
-
 // LayerDesc of one layer: non-identity blocks sorted by first qubit (fill_layer order).
-qsb::LayerDesc build_layer(const qsb_circuit* c, int step, const std::vector<int>& layer_of, int layer) {
+qsb::LayerDesc build_layer(const qsb_circuit* c, int step, const std::vector<int>& layer_of, int layer,
+                           const std::vector<FnInfo>& fn) {
     const int n = c->n_qubits;
     const int b = c->step_offsets[step];
     std::vector<int> ops;
@@ -210,9 +249,7 @@ qsb::LayerDesc build_layer(const qsb_circuit* c, int step, const std::vector<int
     for (int i = 0; i < nb; ++i) {
         const qsb::BlockDesc& blk = d.blocks[i];
         if (blk.kind == qsb::kBlockTable) {
-            const qsb_function& f = c->functions[reinterpret_cast<intptr_t>(blk.t_im)];
-            const size_t d2 = static_cast<size_t>(f.dim) * f.dim;
-            if (!all_zero(f.im, d2)) d.real = 0;
+            if (fn[reinterpret_cast<intptr_t>(blk.t_im)].has_im) d.real = 0;
         } else {
             for (int e = 0; e < 4; ++e)
                 if (blk.u_im[e] != 0.0) d.real = 0;
@@ -235,21 +272,27 @@ Compiled compile(const qsb_circuit* c) {
     out.N = 1u << c->n_qubits;
     out.n_steps = c->n_steps;
     std::vector<char> used(static_cast<size_t>(std::max(c->n_functions, 0)), 0);
-    for (int s = 0; s < c->n_steps; ++s) {
+    for (int s = 0; s < c->n_steps; ++s)
         for (int i = c->step_offsets[s]; i < c->step_offsets[s + 1]; ++i) {
             check_op(c, c->ops[i]);
             if (c->ops[i].kind == QSB_OP_FUNCTION) used[c->ops[i].function] = 1;
         }
+    out.fn.resize(used.size());
+    const bool force_dense = std::getenv("QSB_DENSE_TABLES") != nullptr;  // tests: exercise both layouts
+    for (size_t f = 0; f < used.size(); ++f)
+        if (used[f]) {
+            out.used_functions.push_back(static_cast<int>(f));
+            out.fn[f] = analyse_function(c->functions[f], force_dense);
+        }
+    for (int s = 0; s < c->n_steps; ++s) {
         int nl = 0;
         const std::vector<int> layer_of = first_fit(c, s, &nl);
         for (int l = 0; l < nl; ++l) {
-            out.app.push_back(build_layer(c, s, layer_of, l));
+            out.app.push_back(build_layer(c, s, layer_of, l, out.fn));
             out.app_step.push_back(s);
             out.app_index.push_back(l);
         }
     }
-    for (size_t f = 0; f < used.size(); ++f)
-        if (used[f]) out.used_functions.push_back(static_cast<int>(f));
     return out;
 }
 
@@ -354,43 +397,12 @@ void upload_tables(qsb_plan* p, const qsb_circuit* c) {
     const size_t nf = static_cast<size_t>(std::max(c->n_functions, 0));
     std::vector<size_t> off(nf, 0);
     std::vector<char> mono(nf, 0);
-    std::vector<std::vector<int32_t>> cols(nf);
-    std::vector<std::vector<double>> vre(nf), vim(nf);
     size_t total = 0;  // in doubles
-    const bool force_dense = std::getenv("QSB_DENSE_TABLES") != nullptr;  // tests: exercise both layouts
     for (int f : p->cc.used_functions) {
-        const qsb_function& fn = c->functions[f];
-        const size_t d = static_cast<size_t>(fn.dim);
-        cols[f].assign(d, -1);
-        vre[f].assign(d, 0.0);
-        vim[f].assign(d, 0.0);
-        // rows scanned in parallel chunks on the host's cores (a DJ-11 oracle is 4M entries)
-        std::atomic<bool> is_mono{!force_dense};
-        auto scan = [&](size_t r0, size_t r1) {
-            for (size_t r = r0; r < r1 && is_mono.load(std::memory_order_relaxed); ++r)
-                for (size_t k = 0; k < d; ++k) {
-                    const double a = fn.re[r * d + k], b = fn.im[r * d + k];
-                    if (a == 0.0 && b == 0.0) continue;
-                    if (cols[f][r] >= 0) {
-                        is_mono.store(false, std::memory_order_relaxed);
-                        return;
-                    }
-                    cols[f][r] = static_cast<int32_t>(k);
-                    vre[f][r] = a;
-                    vim[f][r] = b;
-                }
-        };
-        const size_t workers = d >= 512 ? std::min<size_t>(16, std::max(1u, std::thread::hardware_concurrency())) : 1;
-        if (workers <= 1 || !is_mono) {
-            if (is_mono) scan(0, d);
-        } else {
-            std::vector<std::thread> pool;
-            for (size_t w = 0; w < workers; ++w) pool.emplace_back(scan, d * w / workers, d * (w + 1) / workers);
-            for (auto& t : pool) t.join();
-        }
-        mono[f] = is_mono.load();
+        const size_t d = static_cast<size_t>(c->functions[f].dim);
+        mono[f] = p->cc.fn[f].mono;
         off[f] = total;
-        total += is_mono ? 2 * d + (d + 1) / 2 : 2 * d * d;
+        total += mono[f] ? 2 * d + (d + 1) / 2 : 2 * d * d;
     }
     if (total == 0) return;
     p->b.tables.ensure(total * sizeof(double));
@@ -403,11 +415,12 @@ void upload_tables(qsb_plan* p, const qsb_circuit* c) {
         const qsb_function& fn = c->functions[f];
         const size_t d = static_cast<size_t>(fn.dim);
         if (mono[f]) {
-            cuda_check(cudaMemcpyAsync(base + off[f], vre[f].data(), d * 8, cudaMemcpyHostToDevice, s),
+            const FnInfo& fi = p->cc.fn[f];
+            cuda_check(cudaMemcpyAsync(base + off[f], fi.vre.data(), d * 8, cudaMemcpyHostToDevice, s),
                        "upload function");
-            cuda_check(cudaMemcpyAsync(base + off[f] + d, vim[f].data(), d * 8, cudaMemcpyHostToDevice, s),
+            cuda_check(cudaMemcpyAsync(base + off[f] + d, fi.vim.data(), d * 8, cudaMemcpyHostToDevice, s),
                        "upload function");
-            cuda_check(cudaMemcpyAsync(base + off[f] + 2 * d, cols[f].data(), d * 4, cudaMemcpyHostToDevice, s),
+            cuda_check(cudaMemcpyAsync(base + off[f] + 2 * d, fi.cols.data(), d * 4, cudaMemcpyHostToDevice, s),
                        "upload function");
         } else {
             const size_t d2 = d * d;
