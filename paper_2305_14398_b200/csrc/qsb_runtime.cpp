@@ -894,6 +894,12 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     }
     // Plans executed on a caller's stream (qsb_plan_execute) must see the uploads.
     if (!borrow_cache) cuda_check(cudaStreamSynchronize(dc->stream), "cudaStreamSynchronize");
+    if (trace && !p->small) {
+        const auto t5 = tnow();
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        std::fprintf(stderr, "qsb plan: compile %.1f us, memory check + buffers %.1f us, tables %.1f us, rest %.1f us\n",
+                     us(t0, t1), us(t1, t2), us(t2, t3), us(t3, t5));
+    }
     const int gemms = p->small ? static_cast<int>(p->chain.size()) - 1 : static_cast<int>(p->chain.size()) - 1;
     qsb_plan_info& in = p->info;
     in.n_qubits = n;
