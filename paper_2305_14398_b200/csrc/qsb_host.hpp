@@ -127,6 +127,15 @@ struct DeviceCtx {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool owns_stream = true;  // virtual shards on one device share that device's first stream
+    double total_mem = 0.0;   // bytes of device memory (cudaGetDeviceProperties)
+    // Free device memory, queried only for allocations that are a visible share of the
+    // device (cudaMemGetInfo is a driver round trip on every plan of a cold host call).
+    bool fits(double bytes, double fraction) const {
+        if (bytes < 0.25 * total_mem) return true;
+        size_t free_b = 0, total_b = 0;
+        qsbh::cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+        return bytes <= fraction * static_cast<double>(free_b);
+    }
     qsbh::Buffers cache;
     void* nccl_comm = nullptr;  // ncclComm_t of this device in the handle's communicator (distinct devices)
     qsbh::DevBuf gathered;      // [2][N] psi all-gathered over NCCL  // reused by the host-API calls

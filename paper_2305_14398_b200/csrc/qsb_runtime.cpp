@@ -672,11 +672,9 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     }
     if (p->tile == qsb::kTileWs3MS) {
         // the sum plane costs 50% more V memory: fall back to in-register sums if it does not fit
-        size_t free_b = 0, total_b = 0;
         DeviceScope ds0(dc->device);
-        cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
         const double need = 2.0 * 3.0 * 8.0 * static_cast<double>(M) * static_cast<double>(N);
-        if (need > 0.9 * static_cast<double>(free_b)) p->tile = qsb::kTileWs3M;
+        if (!dc->fits(need, 0.9)) p->tile = qsb::kTileWs3M;
     }
     p->planes = p->small ? 2 : qsb::gemm_tile_planes(p->tile);
 
@@ -766,9 +764,7 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
         if (any) {
             const int bp = qsb::gemm_tile_b_planes(p->tile);
             const size_t bytes = static_cast<size_t>(bp) * static_cast<size_t>(N) * static_cast<size_t>(N) * 8;
-            size_t free_b = 0, total_b = 0;
-            cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-            if (static_cast<double>(bytes) < 0.9 * static_cast<double>(free_b)) {
+            if (dc->fits(static_cast<double>(bytes), 0.9)) {
                 p->b.lmat.ensure(bytes);
                 p->tmap_b = make_tmap(p->b.lmat.p, static_cast<int>(N), static_cast<int>(N),
                                       qsb::gemm_tile_cols(p->tile), bp);
@@ -1154,6 +1150,7 @@ qsb_status qsb_create(const qsb_options* options, qsb_handle** out) {
             min_mem = (min_mem == 0.0) ? mem : std::min(min_mem, mem);
             auto dc = std::make_unique<DeviceCtx>();
             dc->device = id;
+            dc->total_mem = static_cast<double>(prop.totalGlobalMem);
             // One stream per physical device: shards repeated on one GPU ("virtual shards")
             // run one after the other. Two stream-K GEMMs (persistent grids sized to the SM
             // count, owners spinning on contributors) running concurrently on one device
