@@ -493,10 +493,16 @@ def run_ours(args):
     e2e_clocks = None
     if vr > 1:
         e2e_ms, h2d, d2h, e2e_calls, e2e_cached = None, 0, 0, 0, None  # the projection times one shard
+        e2e_error = None
     else:
+        e2e_error = None
         with ClockSampler(local, "e2e") as eclk:
-            e2e_ms, h2d, d2h, e2e_calls, e2e_cached = e2e_measure(sim, flat, args, world, rank, N, begin, count,
-                                                                   s_ptr)
+            try:
+                e2e_ms, h2d, d2h, e2e_calls, e2e_cached = e2e_measure(sim, flat, args, world, rank, N, begin, count,
+                                                                       s_ptr)
+            except Exception as exc:  # keep the device-timed line: report the failure instead of dying
+                e2e_ms, h2d, d2h, e2e_calls, e2e_cached = None, 0, 0, 0, None
+                e2e_error = f"{type(exc).__name__}: {exc}"
         e2e_clocks = eclk.summary()
 
     if rank == 0:
@@ -539,11 +545,12 @@ def run_ours(args):
                                         "profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no FP64 entry"},
             "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "calls_timed": e2e_calls,
-                    "cold_call": "every call compiles the circuit and uploads its descriptors (QSB_FLAG_NO_PLAN_CACHE)"
-                                 if world == 1 else "every step creates the rank's plan, executes, all-gathers, D2H",
+                    "cold_call": "every call compiles the circuit and uploads its descriptors (QSB_FLAG_NO_PLAN_CACHE)",
                     "value_plan_cached": e2e_cached,
+                    "error": e2e_error,
                     "api": "qsb_simulate_full_state (C ABI)" if world == 1 else
-                           "qsb_plan_create/execute + NCCL all-gather + D2H",
+                           "qsb_simulate_full_state_sharded (C ABI: row block per rank, psi all-gathered over "
+                           "libqsb's NCCL communicator, whole psi to every rank's host planes)",
                     "clocks": e2e_clocks},
             "gpu_launches": (info.n_launches if info else 0) * args.steps,
             "clocks": clocks,
@@ -601,7 +608,6 @@ def e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr):
     import torch.distributed as dist
 
     from paper_2305_14398_b200 import native
-    from paper_2305_14398_b200.sharding import gather_state
 
     h2d = flat.nbytes()
     d2h = 16 * N
@@ -634,28 +640,37 @@ def e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr):
         cold.close()
         cached_ms, _ = timed_calls(sim._h)
         return cold_ms, h2d, d2h, calls, cached_ms
-    psi_re = torch.empty(N, dtype=torch.float64, device="cuda")
-    psi_im = torch.empty(N, dtype=torch.float64, device="cuda")
-    host = torch.empty(2, N, dtype=torch.float64, pin_memory=True)
-    times = []
-    for _ in range(steps):
-        dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        plan = sim.plan(flat, None, begin, count) if count > 0 else None
-        if plan is not None:
-            plan.execute(s_ptr)
-        gather_state(plan, psi_re, psi_im, begin, count, world, s_ptr)
-        host[0].copy_(psi_re, non_blocking=True)
-        host[1].copy_(psi_im, non_blocking=True)
-        torch.cuda.synchronize()
-        dt = (time.perf_counter() - t0) * 1e3
-        if plan is not None:
-            plan.close()
-        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        times.append(float(t.item()))
-    return sum(times) / len(times), h2d, d2h, len(times), None
+    # one process per GPU: every rank makes the C-ABI call qsb_simulate_full_state_sharded
+    # (its row block of U, psi all-gathered over libqsb's own NCCL communicator, the whole
+    # psi in every rank's host planes); max over ranks per call
+    from paper_2305_14398_b200.simulator import B200UnitarySimulator, Comm, nccl_unique_id
+
+    if count * world != N:
+        return None, h2d, d2h, 0, None  # ragged worlds keep trailing ranks idle: no sharded call
+    uid = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = Comm(sim, uid[0], world, rank)
+
+    def timed_calls(s2):
+        def one():
+            dist.barrier()
+            t0 = time.perf_counter()
+            s2.simulate_full_state_sharded(flat, None, comm)
+            t = torch.tensor([(time.perf_counter() - t0) * 1e3], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+
+        first = one()
+        reps = max(3, min(args.steps, int(20e3 / max(first, 1e-3))))  # identical on every rank
+        times = [one() for _ in range(reps)]
+        return sum(times) / len(times), len(times)
+
+    cold = B200UnitarySimulator(device=sim.device, gemm_mode=mode_of(args), flags=native.FLAG_NO_PLAN_CACHE)
+    cold_ms, calls = timed_calls(cold)
+    cold.close()
+    cached_ms, _ = timed_calls(sim)
+    comm.close()
+    return cold_ms, h2d, d2h, calls, cached_ms
 
 
 # --------------------------------------------------------------- state-vector engine arms

@@ -286,6 +286,13 @@ qsb_status qsb_comm_destroy(qsb_comm* comm);
 /* NCCL version (e.g. 22809) of the library in use; loads libnccl. */
 qsb_status qsb_nccl_version(int32_t* version);
 
+/* qsb_simulate_full_state for one process per GPU (a rank of `comm`): this rank
+ * computes rows [rank 2^n / n_ranks, +2^n / n_ranks) of U with no communication,
+ * the ranks' psi rows are all-gathered over NCCL, and every rank receives the whole
+ * psi in its host planes (length 2^n). Same plan cache as the single-process call. */
+qsb_status qsb_simulate_full_state_sharded(qsb_handle* handle, qsb_comm* comm, const qsb_circuit* circuit,
+                                           double* psi_re, double* psi_im);
+
 /* All-gather the psi rows of every rank's plan into full-length device planes
  * (2^n doubles each) on every rank, async on `stream`. Rank r's plan must own
  * rows [r * 2^n / n_ranks, (r + 1) * 2^n / n_ranks) (row blocks, not column blocks). */

@@ -1359,7 +1359,8 @@ static void drop_plan_cache(qsb_handle* h) {
 // when the handle has a single device), each computed with no communication;
 // psi rows and U rows land directly at their offsets in the host planes.
 static bool run_full_locked(qsb_handle* h, const qsb_circuit* c, const double* psi0_re, const double* psi0_im,
-                            double* psi_re, double* psi_im, double* u_re, double* u_im, bool allow_hit) {
+                            double* psi_re, double* psi_im, double* u_re, double* u_im, bool allow_hit,
+                            const qsb_comm* comm = nullptr) {
     validate_circuit_shape(c);
     check_guard(c, h->guard);
     const int64_t N = int64_t{1} << c->n_qubits;
@@ -1371,14 +1372,28 @@ static bool run_full_locked(qsb_handle* h, const qsb_circuit* c, const double* p
         while (p2 * 2 <= G) p2 *= 2;
         G = p2;
     }
-    const int64_t rows = N / G;
+    int64_t rows = N / G;
+    int64_t first_row = 0;  // row block g covers [first_row + g * rows, + rows)
+    if (comm) {
+        // one process per GPU: this rank's row block only, psi all-gathered over the communicator
+        if (comm->device != h->dev0().device)
+            raise(QSB_ERR_ARGUMENT, "communicator on device %d, handle on device %d", comm->device, h->dev0().device);
+        if (N % comm->n_ranks != 0 || (comm->n_ranks & (comm->n_ranks - 1)) != 0)
+            raise(QSB_ERR_ARGUMENT, "%d ranks do not split 2^%d rows into equal power-of-two blocks", comm->n_ranks,
+                  c->n_qubits);
+        G = 1;
+        rows = N / comm->n_ranks;
+        first_row = comm->rank * rows;
+    }
     // psi is all-gathered over NCCL (north star) whenever the shards sit on distinct
     // devices; repeated ids (virtual shards) cannot form a communicator.
     bool distinct = true;
     for (int a = 0; a < G; ++a)
         for (int b = a + 1; b < G; ++b) distinct = distinct && h->devs[a]->device != h->devs[b]->device;
-    const bool use_nccl = psi_re && !(h->flags & QSB_FLAG_COLUMN_BLOCKS) && distinct &&
+    const bool use_nccl = psi_re && !comm && !(h->flags & QSB_FLAG_COLUMN_BLOCKS) && distinct &&
                           (G > 1 || (h->flags & QSB_FLAG_NCCL_GATHER));
+    if (comm && (u_re || (h->flags & QSB_FLAG_COLUMN_BLOCKS)))
+        raise(QSB_ERR_ARGUMENT, "the one-process-per-GPU call returns psi of row-block plans only");
     double* gathered_host = nullptr;
     std::vector<double*> staged(G, nullptr);
     std::vector<std::vector<double>> vt(G);  // column blocks: V = U[:, cols]^T on the host
@@ -1389,7 +1404,7 @@ static bool run_full_locked(qsb_handle* h, const qsb_circuit* c, const double* p
     // Plans of the last call are kept (compiled descriptors, uploaded tables, V buffers,
     // CUDA graph): a call with the same circuit structure reuses them and checks the
     // registry matrices' contents against the kept copies while the GPU runs.
-    std::vector<char> key = plan_key(c, G, h->flags);
+    std::vector<char> key = plan_key(c, comm ? -(comm->n_ranks * 65536 + comm->rank) - 1 : G, h->flags);
     if (c->n_steps > 0)  // (a hit skips compile(), which checks every operation)
         for (int i = c->step_offsets[0]; i < c->step_offsets[c->n_steps]; ++i) check_op(c, c->ops[i]);
     const bool no_cache = (h->flags & QSB_FLAG_NO_PLAN_CACHE) != 0;
@@ -1398,7 +1413,7 @@ static bool run_full_locked(qsb_handle* h, const qsb_circuit* c, const double* p
         drop_plan_cache(h);
         try {
             for (int g = 0; g < G; ++g)
-                h->cached.push_back(make_plan(h, h->devs[g].get(), c, g * rows, rows, true).release());
+                h->cached.push_back(make_plan(h, h->devs[g].get(), c, first_row + g * rows, rows, true).release());
         } catch (...) {
             drop_plan_cache(h);
             throw;
@@ -1438,7 +1453,7 @@ static bool run_full_locked(qsb_handle* h, const qsb_circuit* c, const double* p
             if (psi_re && p->columns) {
                 // column blocks: every shard returns a full-length share of psi, summed below
                 staged[g] = static_cast<double*>(p->dc->stage_out(2 * static_cast<size_t>(N) * 8));
-            } else if (use_nccl) {
+            } else if (use_nccl || comm) {
                 // rows stay on the device for the all-gather below
             } else if (psi_re && p->small) {
                 // the one-CTA kernel writes psi straight into pinned staging (mapped): no copy call
@@ -1455,7 +1470,7 @@ static bool run_full_locked(qsb_handle* h, const qsb_circuit* c, const double* p
                 if (psi_re)
                     cuda_check(cudaMemcpyAsync(staged[g], p->b.psi.p, 2 * static_cast<size_t>(N) * 8,
                                                cudaMemcpyDeviceToHost, s), "download psi");
-            } else if (use_nccl) {
+            } else if (use_nccl || comm) {
             } else if (mapped_psi) {
                 // written by the kernel; read after the stream synchronisation below
             } else if (psi_re && p->M <= 65536) {
@@ -1495,6 +1510,28 @@ static bool run_full_locked(qsb_handle* h, const qsb_circuit* c, const double* p
         }
         // the GPU is running: check the registry matrices of a reused plan meanwhile
         const bool same = !hit || functions_unchanged(h, c);
+        if (comm && same && psi_re) {
+            // ncclAllGather of every rank's psi rows into this device's full psi, then D2H
+            const qsb_plan* p = plans[0];
+            DeviceCtx& d0 = *p->dc;
+            DeviceScope ds(d0.device);
+            d0.gathered.ensure(2 * static_cast<size_t>(N) * 8);
+            const NcclApi& nc = nccl_or_raise();
+            auto cm = static_cast<ncclComm_t>(comm->comm);
+            const double* src = psi_rows(p);
+            nccl_check(nc.group_start(), "ncclGroupStart");
+            ncclResult_t r = nc.all_gather(src, d0.gathered.as<double>(), static_cast<size_t>(rows), ncclFloat64, cm,
+                                           d0.stream);
+            if (r == ncclSuccess)
+                r = nc.all_gather(src + p->M, d0.gathered.as<double>() + N, static_cast<size_t>(rows), ncclFloat64, cm,
+                                  d0.stream);
+            const ncclResult_t end = nc.group_end();
+            nccl_check(r, "ncclAllGather (psi rows)");
+            nccl_check(end, "ncclGroupEnd");
+            gathered_host = static_cast<double*>(d0.stage_out(2 * static_cast<size_t>(N) * 8));
+            cuda_check(cudaMemcpyAsync(gathered_host, d0.gathered.p, 2 * static_cast<size_t>(N) * 8,
+                                       cudaMemcpyDeviceToHost, d0.stream), "download psi");
+        }
         if (use_nccl && same) {
             allgather_psi(h, plans, N, rows);
             // every device now holds all of psi; read device 0's copy
@@ -1573,6 +1610,16 @@ qsb_status qsb_simulate_full_state(qsb_handle* h, const qsb_circuit* c, double* 
     return guarded([&] {
         if (!h || !psi_re || !psi_im) raise(QSB_ERR_ARGUMENT, "null argument");
         run_full(h, c, nullptr, nullptr, psi_re, psi_im, nullptr, nullptr);
+    });
+}
+
+qsb_status qsb_simulate_full_state_sharded(qsb_handle* h, qsb_comm* comm, const qsb_circuit* c, double* psi_re,
+                                           double* psi_im) {
+    return guarded([&] {
+        if (!h || !comm || !psi_re || !psi_im) raise(QSB_ERR_ARGUMENT, "null argument");
+        std::lock_guard<std::mutex> lk(h->mu);
+        if (!run_full_locked(h, c, nullptr, nullptr, psi_re, psi_im, nullptr, nullptr, true, comm))
+            run_full_locked(h, c, nullptr, nullptr, psi_re, psi_im, nullptr, nullptr, false, comm);
     });
 }
 

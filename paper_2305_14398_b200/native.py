@@ -206,6 +206,7 @@ def lib() -> ctypes.CDLL:
         "qsb_nccl_version": (ctypes.c_int, [P]),
         "qsb_comm_create": (ctypes.c_int, [P, P, I32, I32, P]),
         "qsb_comm_destroy": (ctypes.c_int, [P]),
+        "qsb_simulate_full_state_sharded": (ctypes.c_int, [P, P, P, P, P]),
         "qsb_plan_allgather_state": (ctypes.c_int, [P, P, P, P, P]),
         "qsb_plan_allgather_unitary": (ctypes.c_int, [P, P, P, P, P]),
         "qsb_collapse": (ctypes.c_int, [P, P, P, I64, U64, P]),

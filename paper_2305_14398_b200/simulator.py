@@ -233,6 +233,17 @@ class B200UnitarySimulator(Simulator):
         native.check(native.lib().qsb_simulate_full_state(self._h, flat.ptr, native.dptr(re), native.dptr(im)))
         return StateVector(flat.n_qubits, re, im)
 
+    def simulate_full_state_sharded(self, circuit, registry, comm: "Comm") -> StateVector:
+        """One process per GPU: this rank's row block of U, psi all-gathered over NCCL
+        (qsb_simulate_full_state_sharded); every rank returns the whole psi."""
+        flat = self._flat(circuit, registry)
+        N = 1 << flat.n_qubits
+        re = np.empty(N)
+        im = np.empty(N)
+        native.check(native.lib().qsb_simulate_full_state_sharded(self._h, comm._c, flat.ptr, native.dptr(re),
+                                                                  native.dptr(im)))
+        return StateVector(flat.n_qubits, re, im)
+
     def simulate_from_state(self, circuit, registry, psi0_re: np.ndarray, psi0_im: np.ndarray) -> StateVector:
         flat = self._flat(circuit, registry)
         N = 1 << flat.n_qubits

@@ -107,3 +107,23 @@ def test_bench_gpus_beyond_visible_fails_loudly():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(torch.cuda.device_count() + 1),
                         "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=600)
     assert r.returncode == 2, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("name,n", [("qft", 5), ("entangle", 10), ("deutsch-jozsa", 11), ("qft", 12)])
+def test_sharded_host_call_one_rank(orc, name, n):
+    """qsb_simulate_full_state_sharded on a one-rank communicator: the rank's row
+    block is all of U, psi comes back through ncclAllGather — bit-identical to the
+    single-process call, cold and plan-cached."""
+    c, reg = q.make_named_circuit(name, n)
+    flat = native.flatten(c, reg)
+    plain = B200UnitarySimulator(device=0)
+    want = plain.simulate_full_state(flat)
+    plain.close()
+    for flags in (0, native.FLAG_NO_PLAN_CACHE):
+        sim = B200UnitarySimulator(device=0, flags=flags)
+        comm = Comm(sim, nccl_unique_id(), 1, 0)
+        for _ in range(2):
+            got = sim.simulate_full_state_sharded(flat, None, comm)
+            assert np.array_equal(got.re, want.re) and np.array_equal(got.im, want.im)
+        comm.close()
+        sim.close()
