@@ -1,15 +1,18 @@
 // qsb_nccl.hpp — NCCL for the one exchange of the row-sharded path (SURVEY.md
 // 8(e)): the all-gather of every shard's psi rows over NVLink / NVSwitch.
 //
-// libnccl is opened at first use (dlopen "libnccl.so.2": the copy torch already
-// loaded in this process when there is one, else the system library), so
-// libqsb.so keeps no link-time dependency and a missing NCCL surfaces as
-// QSB_ERR_NCCL on the calls that need it — never as a silent fallback.
+// libnccl is opened at first use, so libqsb.so keeps no link-time dependency and a
+// missing NCCL surfaces as QSB_ERR_NCCL on the calls that need it — never as a
+// silent fallback. Which copy: $QSB_NCCL_LIB when set (the Python binding points it
+// at the NCCL torch ships, so a torch imported later finds a compatible
+// libnccl.so.2 already loaded), else a libnccl.so.2 already in the process, else
+// the system's.
 #pragma once
 
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <string>
 #include <type_traits>
 
@@ -36,8 +39,11 @@ inline const NcclApi& nccl() {
     static const NcclApi api = [] {
         NcclApi a;
         void* lib = nullptr;
+        if (const char* path = std::getenv("QSB_NCCL_LIB"))
+            if (*path) lib = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+        if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL | RTLD_NOLOAD);
         for (const char* name : {"libnccl.so.2", "libnccl.so", "/usr/lib/x86_64-linux-gnu/libnccl.so.2"})
-            if ((lib = dlopen(name, RTLD_NOW | RTLD_LOCAL)) != nullptr) break;
+            if (!lib && (lib = dlopen(name, RTLD_NOW | RTLD_LOCAL)) != nullptr) break;
         if (!lib) {
             const char* e = dlerror();
             a.why = std::string("cannot load libnccl.so.2: ") + (e ? e : "unknown error");

@@ -167,6 +167,22 @@ def flat_from_arrays(n_qubits: int, step_offsets: np.ndarray, ops: np.ndarray,
 _lib = None
 
 
+def _point_at_torch_nccl() -> None:
+    """libqsb opens NCCL at first use. If it loaded the system libnccl.so.2 before torch
+    is imported, torch's libtorch_cuda would bind to that copy (same soname) and fail on
+    symbols of its own newer NCCL: point libqsb at the NCCL wheel torch uses, found on
+    sys.path without importing torch (QSB_NCCL_LIB set by the caller wins)."""
+    import sys
+
+    if os.environ.get("QSB_NCCL_LIB"):
+        return
+    for base in sys.path:
+        cand = os.path.join(base, "nvidia", "nccl", "lib", "libnccl.so.2")
+        if base and os.path.exists(cand):
+            os.environ["QSB_NCCL_LIB"] = cand
+            return
+
+
 def lib() -> ctypes.CDLL:
     """Load libqsb.so (fails loudly: no CPU fallback exists)."""
     global _lib
@@ -176,6 +192,7 @@ def lib() -> ctypes.CDLL:
         raise RuntimeError(
             f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
             "(there is no CPU fallback for the B200 path)")
+    _point_at_torch_nccl()
     L = ctypes.CDLL(LIB_PATH)
     P, I32, I64, U64, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
     sig = {

@@ -224,3 +224,23 @@ def test_gather_state_rejects_column_block_plans():
 
     with pytest.raises(ValueError, match="row-block"):
         gather_state(ColumnPlan(), None, None, 0, 4, 2)
+
+
+def test_nccl_loaded_before_torch_keeps_torch_importable():
+    """libqsb opens NCCL at first use; loading the system libnccl.so.2 before torch would
+    make torch's libtorch_cuda bind to it (same soname) and fail on its newer symbols.
+    The binding points libqsb at torch's NCCL wheel, so a later `import torch` works."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k != "QSB_NCCL_LIB"}
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_2305_14398_b200.simulator import nccl_version\n"
+            "v = nccl_version()\n"
+            "import torch, torch.distributed\n"
+            "print(v, torch.cuda.nccl.version() if hasattr(torch.cuda, 'nccl') else '')\n" % root)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert int(r.stdout.split()[0]) >= 22000
