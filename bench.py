@@ -217,10 +217,10 @@ def cpu_sample_circuit(name: str, n: int, repeats: int = 2, allow_full: bool = T
 
 
 def cpu_sample_subprocess(workload: str):
-    """cpu_sample in a fresh process that never imports torch or touches the GPU: the
-    reference's memory-bound serial products run up to 1.3-2x slower inside a process
-    that has loaded torch and run GPU work (measured on this image), which would flatter
-    the GPU; the reference arm (--impl reference) runs in such a clean process too."""
+    """cpu_sample in a fresh process that never imports torch or touches the GPU (run
+    before the bench initialises CUDA): the reference's memory-bound serial products ran
+    1.3-2x slower inside, or next to, a process holding a GPU context, which would
+    flatter the GPU; the reference arm (--impl reference) runs in such a clean process too."""
     name, n = WORKLOADS[workload]
     return cpu_circuit_subprocess(name, n)
 
@@ -373,7 +373,7 @@ class ClockSampler:
 
 # --------------------------------------------------------------- our arm
 
-def run_ours(args):
+def run_ours(args, cpu_baseline=None):
     import torch
     import torch.distributed as dist
 
@@ -566,8 +566,8 @@ def run_ours(args):
                 "method": f"rows [0, N/{vr}) of U timed alone on one B200: every rank does identical, "
                           "independent work (row blocks, operators regenerated locally); excludes the "
                           f"NCCL all-gather of psi ({16 * N // vr} bytes per rank)"}
-        if world == 1 and vr == 1 and not args.no_cpu_baseline:
-            cb = cpu_sample_subprocess(args.workload)
+        if world == 1 and vr == 1 and cpu_baseline is not None:
+            cb = cpu_baseline
             cb["extrapolated"] = not cb.get("full_run", True) if "components_s" in cb else False
             if cb["extrapolated"]:
                 cb["model_validation"] = model_validation(args.workload)
@@ -611,7 +611,6 @@ def e2e_measure(sim, flat, args, world, rank, N, begin, count, s_ptr):
 
     h2d = flat.nbytes()
     d2h = 16 * N
-    steps = max(1, min(args.steps, 3))
     if world == 1:
         from paper_2305_14398_b200.simulator import B200UnitarySimulator
 
@@ -859,7 +858,14 @@ def main():
         return run_reference(args)
     if args.backend != "dense":
         return run_sv(args)
-    return run_ours(args)
+    # the CPU baseline first, in a fresh process, before this process initialises CUDA:
+    # sampled next to a live GPU context the reference's single-threaded, memory-bound
+    # layer products ran ~1.5x slower (195 s vs 128-138 s per 4096^2 product on one box)
+    _, world, _ = dist_env()
+    cb = None
+    if world == 1 and args.virtual_ranks <= 1 and not args.no_cpu_baseline:
+        cb = cpu_sample_subprocess(args.workload)
+    return run_ours(args, cb)
 
 
 if __name__ == "__main__":

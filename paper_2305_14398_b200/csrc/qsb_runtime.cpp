@@ -454,8 +454,9 @@ constexpr bool kChainDefault = false;
 // Row blocks per group of the stream-K / data-parallel tile numbering of GEMMs with a
 // materialised B operand (QSB_SK_GROUP; 0 = row-major)
 constexpr int kSkGroup = 16;
-// Row-block parts per plan by default (QSB_PARTS forces a count)
-int kPartsDefault(int64_t N) { return N <= 0 ? 1 : 1; }
+// Row-block parts per plan by default (QSB_PARTS forces a count): none — measured slower
+// than the single chain at every size but Entangle-10 (profiles/R2d_parts_ab.txt)
+constexpr int kPartsDefault = 1;
 
 // Split-K factor for a warp-specialised tile grid of T output tiles (one CTA
 // per SM): the cluster size s in {1, 2, 4} whose T*s CTAs fill the last wave of
@@ -549,7 +550,7 @@ int pick_parts(int n, int64_t rows, int flags) {
     if (const char* e = std::getenv("QSB_PARTS"))
         parts = std::max(1, std::atoi(e));
     else
-        parts = kPartsDefault(N);
+        parts = kPartsDefault;
     while (parts > 1 && (rows % parts != 0 || rows / parts < 128 || ((rows / parts) & (rows / parts - 1)) != 0))
         parts /= 2;
     return parts;
