@@ -218,9 +218,9 @@ def cpu_sample_circuit(name: str, n: int, repeats: int = 2, allow_full: bool = T
 
 def cpu_sample_subprocess(workload: str):
     """cpu_sample in a fresh process that never imports torch or touches the GPU (run
-    before the bench initialises CUDA): the reference's memory-bound serial products ran
-    1.3-2x slower inside, or next to, a process holding a GPU context, which would
-    flatter the GPU; the reference arm (--impl reference) runs in such a clean process too."""
+    before the bench initialises CUDA), like the reference's own process and the
+    reference arm (--impl reference): in this container the reference's memory-bound
+    serial product ran 1.26x slower after a torch import and matmul in the same process."""
     name, n = WORKLOADS[workload]
     return cpu_circuit_subprocess(name, n)
 
@@ -858,9 +858,10 @@ def main():
         return run_reference(args)
     if args.backend != "dense":
         return run_sv(args)
-    # the CPU baseline first, in a fresh process, before this process initialises CUDA:
-    # sampled next to a live GPU context the reference's single-threaded, memory-bound
-    # layer products ran ~1.5x slower (195 s vs 128-138 s per 4096^2 product on one box)
+    # the CPU baseline first, in a fresh torch-free process, before this process initialises
+    # CUDA: the reference's own process never loads torch, and in this container the
+    # reference's single-threaded, memory-bound layer product ran 1.26x slower after a
+    # torch import and matmul in the same process
     _, world, _ = dist_env()
     cb = None
     if world == 1 and args.virtual_ranks <= 1 and not args.no_cpu_baseline:
