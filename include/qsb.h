@@ -262,7 +262,10 @@ qsb_status qsb_plan_gemm_times(qsb_plan* plan, double* ms, int32_t* kinds, int32
 qsb_status qsb_plan_set_initial_state(qsb_plan* plan, const double* re, const double* im, void* stream);
 
 /* Device pointers of the plan's results (valid until the next execute/destroy):
- * U rows (row_count x 2^n, leading dimension 2^n) and psi rows (row_count). */
+ * U rows (row_count x 2^n, leading dimension 2^n) and psi rows (row_count).
+ * A plan split into row-block parts (QSB_PARTS) keeps its U rows per part: this
+ * call then synchronises the device and assembles them into one block first
+ * (call it after the execute, not concurrently with one). */
 qsb_status qsb_plan_unitary_device(const qsb_plan* plan, const double** re, const double** im);
 qsb_status qsb_plan_state_device(const qsb_plan* plan, const double** re, const double** im);
 
