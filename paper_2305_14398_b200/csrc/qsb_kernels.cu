@@ -1994,7 +1994,7 @@ template <int N, int CS, int KSPLIT, int KCH, bool DBUF>
 __global__ void __launch_bounds__(MidCfg<N, CS, KSPLIT, KCH, DBUF>::THREADS, 1)
     mid_dmma_kernel(const SmallLayerDesc* __restrict__ layers, int nlayers, int all_staged, int transpose,
                     uint32_t row_begin, int M, const double* __restrict__ x, double* __restrict__ v_out,
-                    double* __restrict__ psi) {
+                    double* __restrict__ psi, int three_m) {
     using C = MidCfg<N, CS, KSPLIT, KCH, DBUF>;
     constexpr int S = C::S, VP = C::VP, OP = C::OP, NC = C::NC, KC = C::KC, SK = C::SK;
     constexpr int DW = static_cast<int>(sizeof(SmallLayerDesc) / 8);
@@ -2078,6 +2078,7 @@ __global__ void __launch_bounds__(MidCfg<N, CS, KSPLIT, KCH, DBUF>::THREADS, 1)
         unsigned long long next = 0;  // descriptor l + 1, in flight during this layer
         if (!all_staged && l + 1 < nlayers && tid < DW) next = __ldg(lsrc + static_cast<size_t>(l + 1) * DW + tid);
         double cr0[2] = {0.0, 0.0}, ci0[2] = {0.0, 0.0}, cr1[2] = {0.0, 0.0}, ci1[2] = {0.0, 0.0};
+        double t2a[2] = {0.0, 0.0}, t2b[2] = {0.0, 0.0};  // 3M: the Ai Bi products
         const uint32_t fmask = ~d.zmask & static_cast<uint32_t>(N - 1);
         const int f = __popc(fmask);
         double* ob = DBUF ? ops + (l & 1) * 2 * OP : ops;  // this layer's operator
@@ -2105,6 +2106,17 @@ __global__ void __launch_bounds__(MidCfg<N, CS, KSPLIT, KCH, DBUF>::THREADS, 1)
                     dmma((ks & 1) ? cr1 : cr0, vr[4 * ks], br);
                     dmma((ks & 1) ? ci1 : ci0, vi[4 * ks], br);
                 }
+            } else if (three_m) {
+                // 3M: T1 += Ar Br, T2 += Ai Bi, T3 += (Ar + Ai)(Br + Bi); Cr = T1 - T2,
+                // Ci = T3 - T1 - T2 (the sums in registers: two DADDs for one DMMA less)
+#pragma unroll
+                for (int ks = 0; ks < C::KS; ++ks) {
+                    const double ar = vr[4 * ks], ai = vi[4 * ks];
+                    const double br = ltr[4 * ks], bi = lti[4 * ks];
+                    dmma((ks & 1) ? cr1 : cr0, ar, br);
+                    dmma((ks & 1) ? t2b : t2a, ai, bi);
+                    dmma((ks & 1) ? ci1 : ci0, __dadd_rn(ar, ai), __dadd_rn(br, bi));
+                }
             } else {
 #pragma unroll
                 for (int ks = 0; ks < C::KS; ++ks) {
@@ -2116,6 +2128,16 @@ __global__ void __launch_bounds__(MidCfg<N, CS, KSPLIT, KCH, DBUF>::THREADS, 1)
                     dmma((ks & 1) ? ci1 : ci0, ai, br);
                 }
             }
+        }
+        if (three_m && !d.real) {  // (cr, ci) hold (T1, T3): combine with T2
+            const double t2[2] = {t2a[0] + t2b[0], t2a[1] + t2b[1]};
+            const double t1[2] = {cr0[0] + cr1[0], cr0[1] + cr1[1]};
+            const double t3[2] = {ci0[0] + ci1[0], ci0[1] + ci1[1]};
+            cr0[0] = t1[0] - t2[0];
+            cr0[1] = t1[1] - t2[1];
+            ci0[0] = t3[0] - t1[0] - t2[0];
+            ci0[1] = t3[1] - t1[1] - t2[1];
+            cr1[0] = cr1[1] = ci1[0] = ci1[1] = 0.0;
         }
         double o[4] = {cr0[0] + cr1[0], cr0[1] + cr1[1], ci0[0] + ci1[0], ci0[1] + ci1[1]};
         if (KSPLIT > 1 && kp > 0) {
@@ -2183,6 +2205,9 @@ __global__ void __launch_bounds__(MidCfg<N, CS, KSPLIT, KCH, DBUF>::THREADS, 1)
     }
 }
 
+// K2m complex layers: 3M (three DMMAs and two DADDs per k-step) or 4M (four DMMAs)
+constexpr int kMid3MDefault = 0;
+
 template <int N, int CS, int KSPLIT, int KCH, bool DBUF = false>
 static int launch_mid_t(const SmallLayerDesc* d_layers, int nlayers, int transpose, uint32_t row_begin, int M,
                         const double* x, double* v, double* psi, cudaStream_t st) {
@@ -2203,8 +2228,10 @@ static int launch_mid_t(const SmallLayerDesc* d_layers, int nlayers, int transpo
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    const char* e3 = std::getenv("QSB_MID_3M");  // complex layers as 3M (1) or 4M (0)
+    const int three_m = e3 && *e3 ? std::atoi(e3) : kMid3MDefault;
     return static_cast<int>(cudaLaunchKernelEx(&cfg, mid_dmma_kernel<N, CS, KSPLIT, KCH, DBUF>, d_layers, nlayers, all_staged,
-                                               transpose, row_begin, M, x, v, psi));
+                                               transpose, row_begin, M, x, v, psi, three_m));
 }
 
 // Fallback configurations (launch_small_circuit picks DBUF / fewer-warp variants

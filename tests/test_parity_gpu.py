@@ -931,3 +931,22 @@ def test_grouped_tile_numbering(monkeypatch, sim, orc, group, name, n):
     assert rel_frob(u[0], u[1], base[0], base[1]) <= 1e-12
     re, im = orc.fsv(flat)
     assert rel_frob(psi.re, psi.im, re, im) <= TOL
+
+
+@pytest.mark.parametrize("name,n", [("qft", 6), ("qft", 7), ("qft", 8), ("deutsch-jozsa", 7)])
+def test_mid_cluster_chain_3m(monkeypatch, sim, orc, name, n):
+    """K2m with complex layers as 3M (QSB_MID_3M=1: three DMMAs, sums in registers)
+    against the 4M K2m (1e-12) and the oracle (1e-10)."""
+    import paper_2305_14398_b200 as q
+    from paper_2305_14398_b200 import native
+
+    c, reg = q.make_named_circuit(name, n)
+    flat = native.flatten(c, reg)
+    monkeypatch.setenv("QSB_MID_3M", "0")
+    a = sim.build_unitary(flat)
+    monkeypatch.setenv("QSB_MID_3M", "1")
+    b = sim.build_unitary(flat)
+    psi = sim.simulate_full_state(flat)
+    assert rel_frob(b[0], b[1], a[0], a[1]) <= 1e-12
+    re, im = orc.fsv(flat)
+    assert rel_frob(psi.re, psi.im, re, im) <= TOL
