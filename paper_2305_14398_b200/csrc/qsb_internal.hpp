@@ -159,5 +159,6 @@ int ws_partial_values(int tile);          // accumulator values per consumer thr
 int gemm_tile_rows(int tile);
 int gemm_tile_cols(int tile);
 size_t small_circuit_smem_bytes(int M, int N);
+int mid_three_m();  // K2m computes complex layers as 3M (1) or 4M (0)
 
 }  // namespace qsb

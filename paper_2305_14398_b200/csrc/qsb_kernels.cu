@@ -2205,8 +2205,14 @@ __global__ void __launch_bounds__(MidCfg<N, CS, KSPLIT, KCH, DBUF>::THREADS, 1)
     }
 }
 
-// K2m complex layers: 3M (three DMMAs and two DADDs per k-step) or 4M (four DMMAs)
-constexpr int kMid3MDefault = 0;
+// K2m complex layers: 3M (three DMMAs and two DADDs per k-step) or 4M (four DMMAs).
+// 3M measured faster where complex layers dominate (QFT-8 264 -> 251 us, QFT-7 77.9 ->
+// 75.9 us; real-layer chains unchanged: profiles/R2p_mid3m_ab.txt). QSB_MID_3M=0 / 1.
+constexpr int kMid3MDefault = 1;
+int mid_three_m() {
+    const char* e3 = std::getenv("QSB_MID_3M");
+    return e3 && *e3 ? std::atoi(e3) : kMid3MDefault;
+}
 
 template <int N, int CS, int KSPLIT, int KCH, bool DBUF = false>
 static int launch_mid_t(const SmallLayerDesc* d_layers, int nlayers, int transpose, uint32_t row_begin, int M,
@@ -2228,8 +2234,7 @@ static int launch_mid_t(const SmallLayerDesc* d_layers, int nlayers, int transpo
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const char* e3 = std::getenv("QSB_MID_3M");  // complex layers as 3M (1) or 4M (0)
-    const int three_m = e3 && *e3 ? std::atoi(e3) : kMid3MDefault;
+    const int three_m = mid_three_m();  // complex layers as 3M (1) or 4M (0)
     return static_cast<int>(cudaLaunchKernelEx(&cfg, mid_dmma_kernel<N, CS, KSPLIT, KCH, DBUF>, d_layers, nlayers, all_staged,
                                                transpose, row_begin, M, x, v, psi, three_m));
 }

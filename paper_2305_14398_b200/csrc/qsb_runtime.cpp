@@ -924,7 +924,17 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
             in.n_real_gemms += real ? 1 : 0;
             in.gemm_hw_flops += (real ? 4.0 : (three ? 6.0 : 8.0)) * mn2;
         }
-        if (p->small) in.gemm_hw_flops = in.gemm_flops;
+        if (p->small) {
+            // K2s (N <= 32): 4M for every layer; K2m (N >= 64): real layers two products,
+            // complex layers 3M (or 4M with QSB_MID_3M=0)
+            in.gemm_hw_flops = in.gemm_flops;
+            if (N >= 128 || (N == 64 && !std::getenv("QSB_SMALL_CLASSIC"))) {
+                in.gemm_hw_flops = 0.0;
+                const double complex_f = qsb::mid_three_m() ? 6.0 : 8.0;
+                for (size_t i = 1; i < p->chain.size(); ++i)
+                    in.gemm_hw_flops += (p->chain[i].real ? 4.0 : complex_f) * mn2;
+            }
+        }
     }
     in.v_planes = p->planes;
     return p;
