@@ -83,6 +83,7 @@ struct SkArgs {
     int maxc = 0;           // partial slots per tile
     int dp_waves = 0;       // whole-tile data-parallel waves before the stream-K range
     int group_m = 0;        // tile numbering: groups of this many row blocks (0: row-major)
+    int zero_skip = 0;      // materialised operand: clear structurally zero B tiles instead of loading them
     double* ws = nullptr;   // [P owner CTAs][maxc][values][256 consumer threads]
     int* flags = nullptr;   // [P owner CTAs], zero between launches (each owner re-arms its own)
     int* dbg = nullptr;     // QSB_SK_DEBUG: protocol anomaly counters

@@ -948,11 +948,21 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
             const uint32_t tma_bar = sFull + 8 * s;
             const uint32_t bBase = stage + C::A_BYTES;
             if (MAT_B) {
+                // operator tiles the layer's structure makes exactly zero (row and column
+                // disagree on an identity / control bit above the tile: most tiles of a
+                // controlled-phase or permutation layer) are cleared in shared memory
+                // instead of streamed from the materialised operator — same DMMAs, no bytes
+                constexpr uint32_t LOW = (1u << C::LOWBITS) - 1u;
+                const bool zero = sk.zero_skip &&
+                                  ((static_cast<uint32_t>(ktg * C::BK) ^ static_cast<uint32_t>(n0)) & layer.zmask &
+                                   ~LOW) != 0;
                 if (ptid == 0) {
-                    mbar_expect_tx(tma_bar, C::A_TMA_BYTES + C::B_BYTES);
+                    mbar_expect_tx(tma_bar, C::A_TMA_BYTES + (zero ? 0 : C::B_BYTES));
                     tma_load_3d(stage, &tmA, tma_bar, ktg * C::BK, m0, 0);
-                    tma_load_3d(bBase, &tmB, tma_bar, ktg * C::BK, n0, 0);
+                    if (!zero) tma_load_3d(bBase, &tmB, tma_bar, ktg * C::BK, n0, 0);
                 }
+                if (zero)
+                    for (int o = ptid * 16; o < C::B_BYTES; o += 16 * 32 * C::PRODUCER_WARPS) sts128(bBase + o, 0.0, 0.0);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(sFull + 8 * s);
                 continue;

@@ -347,6 +347,7 @@ struct qsb_plan {
     int splits = 1;  // K2 split-K cluster size (warp-specialised tiles)
     bool streamk = false;  // K2 stream-K schedule (warp-specialised tiles)
     int sk_group = 0;      // grouped tile numbering for GEMMs with a materialised B operand
+    int zero_skip = 1;     // materialised B: structurally zero tiles cleared, not loaded (QSB_MATB_DENSE=1: off)
     bool chain_k = false;  // K2c: every GEMM in one persistent dataflow launch
     int chain_splits = 1;
     // Row-block parts on one device: the plan's rows split into independent sub-plans
@@ -699,6 +700,7 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
     // per element on the producer warps (they queue behind DMMA on the shared FP64
     // pipe) are materialised once by K1t and streamed to K2 by TMA instead.
     p->mat.assign(p->chain.size(), 0);
+    p->zero_skip = std::getenv("QSB_MATB_DENSE") ? 0 : 1;
     // K2c (one persistent launch for the whole chain, dataflow between GEMMs by row
     // block) where the per-GEMM launch, fill and tail are a visible share of a GEMM:
     // mid sizes, 3M sum-plane tiles, every operator generated in shared memory (a chain
@@ -1053,6 +1055,7 @@ void enqueue(qsb_plan* p, cudaStream_t s) {
         a.splits = p->splits;
         a.sk = p->sk;  // flags start at zero and every owner re-arms its own (no memset between GEMMs)
         a.sk.group_m = mat ? p->sk_group : 0;
+        a.sk.zero_skip = p->zero_skip;
         const bool gt = ev && p->per_gemm;
         if (gt) cuda_check(cudaEventRecord(p->gev[2 * (i - 1)], s), "event");
         cuda_check(qsb::launch_zgemm(a, p->tile, p->h->gemm_mode, s), "zgemm_gen_kernel");
