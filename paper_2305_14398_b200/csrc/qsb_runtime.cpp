@@ -453,8 +453,11 @@ void upload_tables(qsb_plan* p, const qsb_circuit* c) {
 // K2c by default (QSB_CHAIN=1 / 0 force it on / off)
 constexpr bool kChainDefault = false;
 // Row blocks per group of the stream-K / data-parallel tile numbering of GEMMs with a
-// materialised B operand (QSB_SK_GROUP; 0 = row-major)
-constexpr int kSkGroup = 16;
+// materialised B operand (QSB_SK_GROUP; 0 = row-major). Row-major since the structurally
+// zero B tiles are no longer loaded: the waves' 64 CTAs per row block then share A best
+// (QFT-12 3M launch 0.43 GB read with row-major waves, 3.7 GB with groups of 16:
+// profiles/R2s_group_zeroskip.md)
+constexpr int kSkGroup = 0;
 // Row-block parts per plan by default (QSB_PARTS forces a count): none — measured slower
 // than the single chain at every size but Entangle-10 (profiles/R2d_parts_ab.txt)
 constexpr int kPartsDefault = 1;
@@ -839,11 +842,10 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
             const int per = static_cast<int>(std::max<long long>(1, I / P));
             p->sk.dp_waves = W;
             p->sk.enabled = 1;
-            // grouped tile numbering (sk_tile_coords) for GEMMs that stream a materialised B
-            // operand: a wave spans kSkGroup row blocks and ~P / kSkGroup B column blocks instead
-            // of ~2 row blocks and every column block (QFT-12 3M launch: DRAM read 12.7 -> 6.3 GB
-            // at the same duration, profiles/R2g_group_ab.md); generated-B GEMMs keep row-major
-            // waves, whose 64 CTAs per row block share A best (set per launch in enqueue)
+            // grouped tile numbering (sk_tile_coords, QSB_SK_GROUP) for GEMMs that stream a
+            // materialised B operand, set per launch in enqueue: halved the DRAM read of a QFT-12
+            // 3M launch while every B tile was loaded (12.7 -> 6.3 GB, profiles/R2g_group_ab.md);
+            // with zero tiles skipped, row-major waves read the least (kSkGroup = 0)
             {
                 int gm = kSkGroup;
                 if (const char* e = std::getenv("QSB_SK_GROUP")) gm = std::max(0, std::atoi(e));
