@@ -838,6 +838,8 @@ std::unique_ptr<qsb_plan> make_plan(qsb_handle* h, DeviceCtx* dc, const qsb_circ
             int W = T % P == 0 ? T / P : std::max(0, T / P - 1);
             if (const char* e = std::getenv("QSB_SK_DP"))
                 if (*e && std::atoi(e) == 0) W = 0;
+            if (const char* e = std::getenv("QSB_SK_WAVES"))  // A/B: data-parallel waves forced
+                if (*e) W = std::min(std::max(0, std::atoi(e)), T / P);
             const long long I = static_cast<long long>(T - W * P) * KT;
             const int per = static_cast<int>(std::max<long long>(1, I / P));
             p->sk.dp_waves = W;
