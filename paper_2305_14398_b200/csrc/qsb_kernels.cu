@@ -639,16 +639,25 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 // n0..n0+BN) of `layer` generated into the stage at bBase by the 128 producer
 // threads (ptid), in the consumers' swizzled layout. Zero tiles are cleared;
 // monomial layers write zeros plus the hits; others fold block entries per element.
+// `zero_stages` (per producer thread, bit s = stage s's B region still holds the zeros
+// this thread wrote there): a zero tile in a stage that already holds zeros needs no
+// stores — the clearing costs producer issue slots next to the DMMAs.
 template <bool THREE_M, bool SUMPLANE, bool REAL>
-__device__ __forceinline__ void ws_produce_b(const LayerDesc& layer, uint32_t bBase, int ptid, int ktg, int n0) {
+__device__ __forceinline__ void ws_produce_b(const LayerDesc& layer, uint32_t bBase, int ptid, int ktg, int n0,
+                                             int stage, uint32_t& zero_stages) {
     using C = WsCfg<THREE_M, SUMPLANE, REAL>;
     constexpr int BN = C::BN;
     const TilePrefix tp = tile_prefix<C::LOWBITS>(layer, static_cast<uint32_t>(ktg * C::BK),
                                                   static_cast<uint32_t>(n0));
     if (tp.zero) {
-        // whole operator tile is zero: clear the B planes of this stage
-        for (int o = ptid * 16; o < C::B_BYTES; o += 16 * 32 * C::PRODUCER_WARPS) sts128(bBase + o, 0.0, 0.0);
-    } else if (layer.monomial) {
+        // whole operator tile is zero: clear the B planes of this stage (unless they are)
+        if (!((zero_stages >> stage) & 1u))
+            for (int o = ptid * 16; o < C::B_BYTES; o += 16 * 32 * C::PRODUCER_WARPS) sts128(bBase + o, 0.0, 0.0);
+        zero_stages |= 1u << stage;
+        return;
+    }
+    zero_stages &= ~(1u << stage);
+    if (layer.monomial) {
         // one nonzero per operator row: thread = (line n, half of the 8 k-chunks);
         // an entry is nonzero only where the row's column is this line's
         static_assert(32 * C::PRODUCER_WARPS == 2 * BN, "two producer threads per tile line");
@@ -934,6 +943,7 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::PRODUCER_REGS));
         const int ptid = tid - 32 * C::CONSUMER_WARPS;
         int kc = 0;  // stage counter across segments
+        uint32_t zero_stages = 0;  // stages whose B region this thread left zero
         int seg = 0, tile, seg_k0, seg_k1;
         long long it = it_begin;
         while (next_segment(seg, it, tile, seg_k0, seg_k1)) {
@@ -961,8 +971,9 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
                     tma_load_3d(stage, &tmA, tma_bar, ktg * C::BK, m0, 0);
                     if (!zero) tma_load_3d(bBase, &tmB, tma_bar, ktg * C::BK, n0, 0);
                 }
-                if (zero)
+                if (zero && !((zero_stages >> s) & 1u))
                     for (int o = ptid * 16; o < C::B_BYTES; o += 16 * 32 * C::PRODUCER_WARPS) sts128(bBase + o, 0.0, 0.0);
+                zero_stages = zero ? (zero_stages | (1u << s)) : (zero_stages & ~(1u << s));
                 __syncwarp();
                 if (lane == 0) mbar_arrive(sFull + 8 * s);
                 continue;
@@ -971,7 +982,7 @@ __global__ void __launch_bounds__(WsCfg<THREE_M, SUMPLANE, REAL>::THREADS, 1)
                 mbar_expect_tx(tma_bar, C::A_TMA_BYTES);
                 tma_load_3d(stage, &tmA, tma_bar, ktg * C::BK, m0, 0);
             }
-            ws_produce_b<THREE_M, SUMPLANE, REAL>(layer, bBase, ptid, ktg, n0);
+            ws_produce_b<THREE_M, SUMPLANE, REAL>(layer, bBase, ptid, ktg, n0, s, zero_stages);
             __syncwarp();
             if (lane == 0) mbar_arrive(sFull + 8 * s);
         }
@@ -1500,10 +1511,14 @@ __global__ void __launch_bounds__(ChainCfg::THREADS, 1)
                     mbar_expect_tx(tma_bar, a_bytes);
                     tma_load_3d(stage, ta, tma_bar, ktg * C::BK, m0, 0);
                 }
-                if (real)
-                    ws_produce_b<true, true, true>(L, stage + C::A_BYTES, ptid, ktg, n0);
-                else
-                    ws_produce_b<true, true, false>(L, stage + C::A_BYTES, ptid, ktg, n0);
+                // (the real and 3M variants clear different B sizes: no zero-stage reuse across them)
+                if (real) {
+                    uint32_t none = 0;
+                    ws_produce_b<true, true, true>(L, stage + C::A_BYTES, ptid, ktg, n0, s, none);
+                } else {
+                    uint32_t none = 0;
+                    ws_produce_b<true, true, false>(L, stage + C::A_BYTES, ptid, ktg, n0, s, none);
+                }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(sFull + 8 * s);
             }
