@@ -244,3 +244,26 @@ def test_nccl_loaded_before_torch_keeps_torch_importable():
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 0, r.stderr[-2000:]
     assert int(r.stdout.split()[0]) >= 22000
+
+
+def test_bench_reference_arm_line():
+    """`bench.py --impl reference` (the driver's reference arm) prints one JSON line
+    with the contract's keys, timing the unmodified reference library on this host."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    import oracle
+
+    if not oracle.reference_available():
+        pytest.skip("oracle/_ref not built")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--workload", "qft-4",
+                        "--steps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "ms"
+    assert line["higher_is_better"] is False and line["config"]["workload"] == "qft-4"
+    assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["extrapolated"] is False
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
