@@ -10,7 +10,7 @@ import sys
 
 def main(out, inputs):
     runs = []
-    seen = set()
+    seen = set()  # (workload, threads): the first input that has it wins
     for spec in inputs:
         path, _, note = spec.partition(":")
         for line in open(path):
@@ -18,9 +18,10 @@ def main(out, inputs):
             if not line.startswith("{"):
                 continue
             d = json.loads(line)
-            if d["workload"] in seen:
+            key = (d["workload"], d.get("threads"))
+            if key in seen:
                 continue
-            seen.add(d["workload"])
+            seen.add(key)
             runs.append({"workload": d["workload"], "threads": d.get("threads"),
                          "measured_ms": d["measured_ms"], "model_ms": d["model_ms"],
                          "model_error": d["model_error"], "source": path, "conditions": note})
