@@ -119,7 +119,8 @@ def cpu_full_run(name: str, n: int) -> float:
     return ref.L.refsh_time_simulate(prog.h, b"unitary-parallel", n) * 1e3
 
 
-def cpu_sample_circuit(name: str, n: int, repeats: int = 2, allow_full: bool = True):
+def cpu_sample_circuit(name: str, n: int, repeats: int = 2, allow_full: bool = True,
+                       full_limit_s: float = FULL_RUN_LIMIT_S):
     """Time the reference CPU path (oracle/_ref: the unmodified reference library)
     on this host's cores for one circuit. When the component model below predicts
     at most FULL_RUN_LIMIT_S, the whole UnitarySimulator::simulate_full_state
@@ -180,7 +181,7 @@ def cpu_sample_circuit(name: str, n: int, repeats: int = 2, allow_full: bool = T
         total = (n_steps + extra) * fold + n_steps * gemm_par + extra * gemm_ser
         comps = {"fold": fold, "gemm_parallel": gemm_par, "gemm_serial": gemm_ser, "steps": n_steps,
                  "extra_layers": extra, "model_s": total, "gemm_serial_samples": ser_samples}
-        if allow_full and total <= FULL_RUN_LIMIT_S:
+        if allow_full and total <= full_limit_s:
             return {"value": cpu_full_run(name, n), "unit": "ms", "cores": cores, "kind": kind,
                     "sample": f"full reference UnitarySimulator::simulate_full_state of {workload} "
                               f"(unitary-parallel, {cores} threads, one run)",
@@ -225,9 +226,9 @@ def cpu_sample_subprocess(workload: str):
     return cpu_circuit_subprocess(name, n)
 
 
-def cpu_circuit_subprocess(name: str, n: int):
+def cpu_circuit_subprocess(name: str, n: int, full_limit_s: float = FULL_RUN_LIMIT_S):
     code = ("import json, sys; sys.path.insert(0, %r); import bench; "
-            "print(json.dumps(bench.cpu_sample_circuit(%r, %d)))" % (ROOT, name, n))
+            "print(json.dumps(bench.cpu_sample_circuit(%r, %d, full_limit_s=%r)))" % (ROOT, name, n, full_limit_s))
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=3600)
     if out.returncode != 0:
         raise RuntimeError(f"cpu baseline subprocess failed: {out.stderr[-2000:]}")
