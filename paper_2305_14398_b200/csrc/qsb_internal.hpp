@@ -128,7 +128,8 @@ int launch_expand(const LayerDesc& layer, uint32_t row_begin, int M, int N, doub
 int gemm_tile_planes(int tile);  // planes of the V buffers a tile variant reads/writes (2, or 3 with Vr+Vi)
 int launch_zgemm(const GemmArgs& a, int tile, int gemm_mode, void* stream);
 // K1t: transposed operator planes for a materialised B (planes 2: re, im; 3: + re+im)
-int launch_expand_t(const LayerDesc& layer, int N, double* out, int planes, void* stream);
+// skip_zero: leave the entries of tiles K2 clears instead of loading (GemmArgs.sk.zero_skip) unwritten
+int launch_expand_t(const LayerDesc& layer, int N, double* out, int planes, void* stream, int skip_zero = 0);
 int gemm_tile_b_planes(int tile);
 // transpose = 1: column blocks (operands L^T, V = U[:, cols]^T). max_free_bits: the
 // largest number of free index bits (f) of any layer after the first — 2^f candidate

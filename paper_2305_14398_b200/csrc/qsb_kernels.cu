@@ -1286,15 +1286,20 @@ static int launch_ws_any(const GemmArgs& a, void* stream) {
 // K1t: the layer operator transposed, Lt[p][n][k] = L[k][n] for planes re, im
 // (and re + im when planes == 3): the TMA source of a materialised B operand.
 // Entries are layer_entry's (bit-exact); consecutive threads write consecutive k.
+// skip_zero: entries inside K2 operator tiles that K2 clears instead of loading (row and
+// column disagree on a zmask bit above the 64-wide tile: sk.zero_skip) are not written —
+// K2 never reads them, so a controlled-phase layer's expansion writes ~1/32 of the plane.
 __global__ void __launch_bounds__(256) expand_t_kernel(const __grid_constant__ LayerDesc d, int N,
-                                                       double* __restrict__ out, int planes) {
+                                                       double* __restrict__ out, int planes, int skip_zero) {
     const size_t plane = static_cast<size_t>(N) * N;
     const size_t pairs = plane / 2;
     const uint32_t half_n = static_cast<uint32_t>(N) / 2;
+    const uint32_t skip_mask = skip_zero ? (d.zmask & ~63u) : 0u;
     for (size_t p = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; p < pairs;
          p += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const uint32_t n = static_cast<uint32_t>(p / half_n);
         const uint32_t k = static_cast<uint32_t>(p % half_n) * 2;
+        if ((k ^ n) & skip_mask) continue;
         double r0, i0, r1, i1;
         layer_entry(d, k, n, r0, i0);
         layer_entry(d, k + 1, n, r1, i1);
@@ -1305,12 +1310,12 @@ __global__ void __launch_bounds__(256) expand_t_kernel(const __grid_constant__ L
     }
 }
 
-int launch_expand_t(const LayerDesc& layer, int N, double* out, int planes, void* stream) {
+int launch_expand_t(const LayerDesc& layer, int N, double* out, int planes, void* stream, int skip_zero) {
     const size_t pairs = static_cast<size_t>(N) * N / 2;
     int blocks = static_cast<int>((pairs + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
-    expand_t_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(layer, N, out, planes);
+    expand_t_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(layer, N, out, planes, skip_zero);
     return static_cast<int>(cudaGetLastError());
 }
 

@@ -1049,7 +1049,7 @@ void enqueue(qsb_plan* p, cudaStream_t s) {
                        "expand_kernel");
         else if (mat)
             cuda_check(qsb::launch_expand_t(p->chain[i], p->N, p->b.lmat.as<double>(),
-                                            qsb::gemm_tile_b_planes(p->tile), s),
+                                            qsb::gemm_tile_b_planes(p->tile), s, p->zero_skip),
                        "expand_t_kernel");
         qsb::GemmArgs a{&p->tmap[cur], &p->chain[i], p->b.v[1 - cur].as<double>(), p->M, p->N};
         a.tmap_b = mat ? &p->tmap_b : nullptr;
